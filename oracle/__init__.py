@@ -1,0 +1,359 @@
+"""CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this package.  The product path (paper_2509_21221_b200/) never does.
+
+ctypes wrapper over oracle/liboracle.so (plain C++, see oracle.h) plus small pure-Python
+helpers (brute force over path multisets, digests) that pin the oracle in tests.
+"""
+from __future__ import annotations
+
+import ctypes
+import itertools
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+ABSENT = np.iinfo(np.int32).max
+OBJ_SUM, OBJ_MINIMAX = 0, 1
+P = ctypes.c_void_p
+
+
+class OrcInstance(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_int32), ("n", ctypes.c_int32), ("max_cap", ctypes.c_int32),
+                ("M", ctypes.c_int64), ("cap", P), ("alive", P), ("src", P), ("snk", P), ("link", P)]
+
+
+class OrcResult(ctypes.Structure):
+    _fields_ = [("F", ctypes.c_int64), ("cost", ctypes.c_int64), ("A", ctypes.c_int32),
+                ("rounds", ctypes.c_int32), ("F_dec", ctypes.c_int64), ("cost_dec", ctypes.c_int64),
+                ("dangling", ctypes.c_int32), ("pre_rounds", ctypes.c_int32), ("digest", ctypes.c_uint64)]
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        L = ctypes.CDLL(path)
+        IP = ctypes.POINTER(OrcInstance)
+        L.orc_eq1.argtypes = [ctypes.c_int32] * 3 + [P, P, ctypes.c_int32, P, P, ctypes.c_int64, P, P, P]
+        L.orc_ssp.argtypes = [IP, P, P, P, P, P, P, P, P]
+        L.orc_ssp_batch.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [P] * 6 + [P, P, P, ctypes.c_int32]
+        L.orc_network_simplex.argtypes = [IP, P, P]
+        L.orc_certify.argtypes = [IP, ctypes.c_int64, ctypes.c_int64, P, P, P, P]
+        L.orc_anneal_table.argtypes = [ctypes.c_double, ctypes.c_double, P, P, P, ctypes.c_int64]
+        L.orc_rounds_create.restype = P
+        L.orc_rounds_create.argtypes = [IP, ctypes.c_uint64, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.orc_rounds_destroy.argtypes = [P]
+        L.orc_rounds_run.argtypes = [P, ctypes.c_int32, P, P, P, P, P]
+        L.orc_rounds_apply_churn.argtypes = [P, P, P, ctypes.c_int64]
+        L.orc_rounds_export.argtypes = [P] + [P] * 8
+        L.orc_rounds_digest.restype = ctypes.c_uint64
+        L.orc_rounds_digest.argtypes = [P]
+        L.orc_rounds_instance.argtypes = [P] + [P] * 5
+        L.orc_llama_victim.restype = ctypes.c_int32
+        L.orc_llama_victim.argtypes = [P, ctypes.c_uint64, ctypes.c_uint64]
+        L.orc_pipeline_batch.argtypes = ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [P] * 6
+                                         + [ctypes.c_int32, P, P, ctypes.c_int64, P, ctypes.c_uint64, ctypes.c_int64,
+                                            ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P])
+        _LIB = L
+    return _LIB
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+@dataclass
+class Instance:
+    """One instance, host numpy arrays (layouts of oracle.h / include/gwtf.h)."""
+    S: int
+    n: int
+    max_cap: int
+    M: int
+    cap: np.ndarray            # [S][n] i32
+    src: np.ndarray            # [n] i32
+    snk: np.ndarray            # [n] i32
+    link: np.ndarray           # [S-1][n][n] i32, dest-major
+    alive: np.ndarray = None   # [S][n] u8
+
+    def __post_init__(self):
+        self.cap = np.ascontiguousarray(self.cap, np.int32)
+        self.src = np.ascontiguousarray(self.src, np.int32)
+        self.snk = np.ascontiguousarray(self.snk, np.int32)
+        self.link = np.ascontiguousarray(np.asarray(self.link, np.int32).reshape(max(self.S - 1, 0), self.n, self.n))
+        if self.alive is None:
+            self.alive = np.ones((self.S, self.n), np.uint8)
+        self.alive = np.ascontiguousarray(self.alive, np.uint8)
+
+    def c(self) -> OrcInstance:
+        o = OrcInstance()
+        o.S, o.n, o.max_cap, o.M = self.S, self.n, self.max_cap, self.M
+        o.cap, o.alive, o.src, o.snk = _ptr(self.cap), _ptr(self.alive), _ptr(self.src), _ptr(self.snk)
+        o.link = _ptr(self.link) if self.link.size else None
+        return o
+
+    def cap_eff(self):
+        return np.where(self.alive != 0, self.cap, 0)
+
+
+def instance_from_batch(bt, b: int, link=None, src=None, snk=None) -> Instance:
+    """Instance b of a generated host batch (gen.Batch); Eq. 1 batches pass link/src/snk from eq1()."""
+    cfg = bt.cfg
+    return Instance(cfg.S, cfg.n, cfg.max_cap, int(bt.supply[b]), bt.cap[b],
+                    bt.src[b] if src is None else src, bt.snk[b] if snk is None else snk,
+                    bt.link[b] if link is None else link, bt.alive[b])
+
+
+def eq1(S, n, L, comp, loc, dloc, lat, bw, size_kbit):
+    """Oracle Eq. 1 in integer half-units -> (src[n], snk[n], link[S-1][n][n])."""
+    src = np.zeros(n, np.int32)
+    snk = np.zeros(n, np.int32)
+    link = np.zeros((max(S - 1, 0), n, n), np.int32)
+    comp = np.ascontiguousarray(comp, np.int32)
+    loc = np.ascontiguousarray(loc, np.int32)
+    lat = np.ascontiguousarray(lat, np.int32)
+    bw = np.ascontiguousarray(bw, np.int32)
+    lib().orc_eq1(S, n, L, _ptr(comp), _ptr(loc), int(dloc), _ptr(lat), _ptr(bw), int(size_kbit),
+                  _ptr(src), _ptr(snk), _ptr(link) if link.size else None)
+    return src, snk, link
+
+
+def eq1_batch(bt):
+    """Oracle Eq. 1 for every instance of a host gen.Batch -> (src[B][n], snk[B][n], link[B][S-1][n][n])."""
+    cfg = bt.cfg
+    B = bt.B
+    src = np.zeros((B, cfg.n), np.int32)
+    snk = np.zeros((B, cfg.n), np.int32)
+    link = np.zeros((B, max(cfg.S - 1, 0), cfg.n, cfg.n), np.int32)
+    for b in range(B):
+        src[b], snk[b], link[b] = eq1(cfg.S, cfg.n, cfg.L, bt.comp[b], bt.loc[b], bt.dloc[b], bt.lat[b], bt.bw[b],
+                                      cfg.size_kbit)
+    return src, snk, link
+
+
+@dataclass
+class SSPResult:
+    F: int
+    cost: int
+    A: int
+    node_flow: np.ndarray
+    src_flow: np.ndarray
+    snk_flow: np.ndarray
+    arc_flow: np.ndarray
+    curve: np.ndarray = None
+
+
+def ssp(I: Instance, curve: bool = False) -> SSPResult:
+    """Canonical SSP."""
+    F = ctypes.c_int64()
+    cost = ctypes.c_int64()
+    A = ctypes.c_int32()
+    nf = np.zeros((I.S, I.n), np.int32)
+    sf = np.zeros(I.n, np.int32)
+    kf = np.zeros(I.n, np.int32)
+    af = np.zeros((max(I.S - 1, 0), I.n, I.n), np.int32)
+    cv = np.zeros(I.M + 1, np.int64) if curve else None
+    c = I.c()
+    rc = lib().orc_ssp(ctypes.byref(c), ctypes.byref(F), ctypes.byref(cost), ctypes.byref(A), _ptr(nf), _ptr(sf),
+                       _ptr(kf), _ptr(af) if af.size else None, _ptr(cv))
+    if rc != 0:
+        raise RuntimeError(f"oracle SSP internal check failed rc={rc}")
+    r = SSPResult(F.value, cost.value, A.value, nf, sf, kf, af)
+    if curve:
+        r.curve = cv[: F.value + 1]
+    return r
+
+
+def network_simplex(I: Instance):
+    F = ctypes.c_int64()
+    cost = ctypes.c_int64()
+    c = I.c()
+    rc = lib().orc_network_simplex(ctypes.byref(c), ctypes.byref(F), ctypes.byref(cost))
+    if rc != 0:
+        raise RuntimeError(f"network simplex failed rc={rc}")
+    return F.value, cost.value
+
+
+def certify(I: Instance, F, cost, node_flow, src_flow, snk_flow, arc_flow) -> int:
+    c = I.c()
+    arrs = [np.ascontiguousarray(a, np.int32) for a in (node_flow, src_flow, snk_flow, arc_flow)]
+    return lib().orc_certify(ctypes.byref(c), int(F), int(cost), *[_ptr(a) if a.size else None for a in arrs])
+
+
+def anneal_table(T0: float, alpha: float):
+    w = ctypes.c_int32()
+    K = ctypes.c_int32()
+    rc = lib().orc_anneal_table(T0, alpha, ctypes.byref(w), ctypes.byref(K), None, 0)
+    if rc:
+        raise ValueError(f"anneal table rc={rc}")
+    t = np.zeros((K.value + 1) * w.value, np.uint32)
+    lib().orc_anneal_table(T0, alpha, ctypes.byref(w), ctypes.byref(K), _ptr(t), t.size)
+    return t.reshape(K.value + 1, w.value), w.value, K.value
+
+
+class Rounds:
+    """Synchronous decentralized rounds of one instance."""
+
+    def __init__(self, I: Instance, seed=0, inst_id=0, T0=1.7, alpha=0.95, objective=OBJ_SUM, W=5, deny_after=3):
+        self.I = I
+        c = I.c()
+        self.h = lib().orc_rounds_create(ctypes.byref(c), seed, inst_id, T0, alpha, objective, W, deny_after)
+        if not self.h:
+            raise ValueError("orc_rounds_create rejected the parameters")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_rounds_destroy(self.h)
+            self.h = None
+
+    def run(self, max_rounds, digests=False):
+        rr = ctypes.c_int32()
+        F = ctypes.c_int64()
+        C = ctypes.c_int64()
+        dg = ctypes.c_int32()
+        d = np.zeros(max(max_rounds, 1), np.uint64) if digests else None
+        lib().orc_rounds_run(self.h, max_rounds, ctypes.byref(rr), ctypes.byref(F), ctypes.byref(C),
+                             ctypes.byref(dg), _ptr(d))
+        out = dict(rounds=rr.value, F_dec=F.value, cost_dec=C.value, dangling=dg.value)
+        if digests:
+            out["digests"] = d[: rr.value]
+        return out
+
+    def apply_churn(self, alive_new=None, updates=None):
+        a = None if alive_new is None else np.ascontiguousarray(alive_new, np.uint8)
+        u = None if updates is None else np.ascontiguousarray(updates, np.int32).reshape(-1, 5)
+        lib().orc_rounds_apply_churn(self.h, _ptr(a), _ptr(u) if u is not None and u.size else None,
+                                     0 if u is None else u.shape[0])
+
+    def export(self):
+        I = self.I
+        up = np.zeros((I.S, I.n, I.max_cap), np.int32)
+        dn = np.zeros_like(up)
+        sd = np.zeros(I.M, np.int32)
+        su = np.zeros(I.M, np.int32)
+        k = np.zeros((I.S, I.n), np.int32)
+        dw = np.zeros_like(k)
+        q = ctypes.c_int32()
+        r = ctypes.c_int64()
+        lib().orc_rounds_export(self.h, _ptr(up), _ptr(dn), _ptr(sd), _ptr(su), _ptr(k), _ptr(dw), ctypes.byref(q),
+                                ctypes.byref(r))
+        return dict(up=up, down=dn, src_down=sd, snk_up=su, kacc=k, deny=dw, quiet=q.value, round=r.value)
+
+    def digest(self) -> int:
+        return int(lib().orc_rounds_digest(self.h))
+
+    def instance(self) -> Instance:
+        I = self.I
+        ce = np.zeros((I.S, I.n), np.int32)
+        al = np.zeros((I.S, I.n), np.uint8)
+        src = np.zeros(I.n, np.int32)
+        snk = np.zeros(I.n, np.int32)
+        link = np.zeros((max(I.S - 1, 0), I.n, I.n), np.int32)
+        lib().orc_rounds_instance(self.h, _ptr(ce), _ptr(al), _ptr(src), _ptr(snk), _ptr(link) if link.size else None)
+        return Instance(I.S, I.n, I.max_cap, I.M, I.cap.copy(), src, snk, link, al)
+
+    def llama_victim(self, draw_stage: int, draw_pick: int) -> int:
+        return int(lib().orc_llama_victim(self.h, draw_stage, draw_pick))
+
+
+def pipeline_batch(cfg, cap, alive, src, snk, link, supply, churn_kind=0, alive_new=None, updates=None,
+                   victim_draws=None, seed=0, inst_base=0, T0=1.7, alpha=0.95, objective=OBJ_SUM, W=5, deny_after=3,
+                   max_rounds=None, threads=None):
+    """Whole bench-step workload per instance (oracle.h orc_pipeline_batch)."""
+    B = cap.shape[0]
+    out = (OrcResult * B)()
+    max_rounds = cfg.max_rounds if max_rounds is None else max_rounds
+    threads = threads or os.cpu_count() or 1
+    arrs = [np.ascontiguousarray(a) for a in (cap, alive, src, snk, link, supply)]
+    un = None if updates is None else np.ascontiguousarray(updates, np.int32)
+    an = None if alive_new is None else np.ascontiguousarray(alive_new, np.uint8)
+    vd = None if victim_draws is None else np.ascontiguousarray(victim_draws, np.uint64)
+    rc = lib().orc_pipeline_batch(B, cfg.S, cfg.n, cfg.max_cap, *[_ptr(a) for a in arrs], churn_kind, _ptr(an),
+                                  _ptr(un) if un is not None and un.size else None, 0 if un is None else un.shape[0],
+                                  _ptr(vd), seed, inst_base, T0, alpha, objective, W, deny_after, max_rounds, threads,
+                                  out)
+    if rc != 0:
+        raise RuntimeError(f"oracle pipeline failed rc={rc}")
+    names = [f[0] for f in OrcResult._fields_]
+    return {k: np.array([getattr(out[b], k) for b in range(B)]) for k in names}
+
+
+# ----------------------------------------------------------------------------------------
+# Pure-Python pins (independent of liboracle)
+# ----------------------------------------------------------------------------------------
+def brute_force(I: Instance):
+    """Max flow value and min cost by exhaustive enumeration of path multisets (SPEC S:212,
+    SURVEY C7).  Every unit of flow follows a path D -> (0,i0) -> ... -> (S-1,i_{S-1}) -> D;
+    a flow is a multiset of such paths within node capacities.  Tiny instances only."""
+    S, n = I.S, I.n
+    ce = I.cap_eff()
+    paths = []
+    for combo in itertools.product(range(n), repeat=S):
+        c = int(I.src[combo[0]]) if I.src[combo[0]] != ABSENT else None
+        if c is None or ce[0, combo[0]] == 0:
+            continue
+        ok = True
+        for s in range(S - 1):
+            w = I.link[s, combo[s + 1], combo[s]]
+            if w == ABSENT or ce[s + 1, combo[s + 1]] == 0:
+                ok = False
+                break
+            c += int(w)
+        if not ok or I.snk[combo[-1]] == ABSENT:
+            continue
+        paths.append((combo, c + int(I.snk[combo[-1]])))
+    best = [0, 0]
+    rem = ce.astype(np.int64).copy()
+
+    def rec(k, F, cost):
+        if F > best[0] or (F == best[0] and cost < best[1]):
+            best[0], best[1] = F, cost
+        if k == len(paths) or F == I.M:
+            return
+        combo, c = paths[k]
+        m = min([int(rem[s, combo[s]]) for s in range(S)] + [I.M - F])
+        for t in range(m, -1, -1):
+            for s in range(S):
+                rem[s, combo[s]] -= t
+            rec(k + 1, F + t, cost + t * c)
+            for s in range(S):
+                rem[s, combo[s]] += t
+
+    rec(0, 0, 0)
+    return best[0], best[1]
+
+
+def mix64(z: int) -> int:
+    m = (1 << 64) - 1
+    z &= m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def digest_state(st: dict, S: int, n: int, MC: int, M: int) -> int:
+    """Python re-statement of the round-state digest of DESIGN.md 2.3 (order-independent sum)."""
+    m = (1 << 64) - 1
+    up = st["up"].reshape(-1)
+    dn = st["down"].reshape(-1)
+    vals = []
+    for p in range(up.size):
+        u, d = int(up[p]), int(dn[p])
+        state = (2 if u != -1 else 0) | (1 if d != -1 else 0)
+        eu = 0 if u == -1 else (1 + u if u >= 0 else (1 << 40) + (-2 - u))
+        ed = 0 if d == -1 else (1 + d if d >= 0 else (1 << 41) + (-2 - d))
+        vals += [state, eu, ed]
+    vals += [0 if int(x) == -1 else 1 + int(x) for x in st["src_down"]]
+    vals += [0 if int(x) == -1 else 1 + int(x) for x in st["snk_up"]]
+    for g in range(S * n):
+        vals += [int(st["kacc"].reshape(-1)[g]) & 0xFFFFFFFF, int(st["deny"].reshape(-1)[g]) & 0xFFFFFFFF]
+    vals.append(int(st["quiet"]) & 0xFFFFFFFF)
+    return sum(mix64(mix64(pos) ^ v) for pos, v in enumerate(vals)) & m

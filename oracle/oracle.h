@@ -1,0 +1,112 @@
+/* oracle/oracle.h -- plain, slow, obviously-correct CPU oracle.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code with the CUDA product path (paper_2509_21221_b200/);
+ * the only common module is the seeded input generator gen/.
+ *
+ * Every function cites the PAPER.md (P:line) / SPEC.md (S:line) passage or
+ * the DESIGN.md reading it follows.  Parity status of each function is listed
+ * in DESIGN.md section 3 ("what pins the oracle").
+ *
+ * Graph: data node D is source
+ * and sink; relays (s,i), s in [0,S), i in [0,n); capacity cap_e = alive?cap:0;
+ * arc costs are integers, INT32_MAX = absent link.
+ *   link[s][v][u] = d(u in stage s -> v in stage s+1)        (dest-major)
+ *   src[i] = d(D -> (0,i)),  snk[i] = d((S-1,i) -> D)
+ */
+#ifndef GWTF_ORACLE_H
+#define GWTF_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t S, n, max_cap;
+  int64_t M;               /* data-node supply (microbatches) */
+  const int32_t* cap;      /* [S][n] */
+  const uint8_t* alive;    /* [S][n], NULL = all alive */
+  const int32_t* src;      /* [n] */
+  const int32_t* snk;      /* [n] */
+  const int32_t* link;     /* [S-1][n][n] dest-major */
+} orc_instance;
+
+/* Eq. 1 in integer half-units: D2 = 2*d =
+ * c_i + c_j + lam_ij + lam_ji + floor(4*size/(beta_ij+beta_ji)), data node c_D = 0.
+ * comp/loc [S][n], lat/bw [L][L]; outputs src[n], snk[n], link[S-1][n][n]. */
+int orc_eq1(int32_t S, int32_t n, int32_t L, const int32_t* comp, const int32_t* loc, int32_t dloc,
+            const int32_t* lat, const int32_t* bw, int64_t size_kbit,
+            int32_t* src, int32_t* snk, int32_t* link);
+
+/* Canonical successive shortest paths.  Outputs the
+ * max-flow value F, its min cost, the augmentation count A and the canonical
+ * assignment.  Arrays may be NULL.  Returns 0, or <0 on internal check failure. */
+int orc_ssp(const orc_instance* I, int64_t* F, int64_t* cost, int32_t* A,
+            int32_t* node_flow /*[S][n]*/, int32_t* src_flow /*[n]*/, int32_t* snk_flow /*[n]*/,
+            int32_t* arc_flow /*[S-1][n][n] dest-major*/, int64_t* cost_curve /*[M+1] or NULL*/);
+
+/* Batch SSP over B instances laid out as the C-ABI does, T threads. */
+int orc_ssp_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const int32_t* cap,
+                  const uint8_t* alive, const int32_t* src, const int32_t* snk, const int32_t* link,
+                  const int64_t* supply, int64_t* F, int64_t* cost, int32_t* A, int32_t threads);
+
+/* Independent cross-check: primal network simplex with strongly feasible
+ * spanning trees (Cunningham) on the node-split graph plus a bypass arc. */
+int orc_network_simplex(const orc_instance* I, int64_t* F, int64_t* cost);
+
+/* Certificates (SURVEY C3 iv): returns 0 iff the assignment is conserved and
+ * within capacity, has value F and cost `cost`, is a maximum flow (F == M or
+ * no residual s*-t* path) and is optimal (no negative residual cycle;
+ * Bellman-Ford potentials with non-negative reduced costs).  >0 = which check failed. */
+int orc_certify(const orc_instance* I, int64_t F, int64_t cost, const int32_t* node_flow,
+                const int32_t* src_flow, const int32_t* snk_flow, const int32_t* arc_flow);
+
+/* Annealing threshold table thr[k][delta] = min(2^32-1, floor(exp(-delta/(T0*alpha^k))*2^32))
+ * (DESIGN.md 2.4).  width = first delta with thr[0][delta] == 0, K = first k
+ * with thr[k][1] == 0.  table may be NULL (sizes only); cap = table capacity in entries. */
+int orc_anneal_table(double T0, double alpha, int32_t* width, int32_t* K, uint32_t* table, int64_t cap);
+
+/* ---- decentralized rounds, GWTF-SYNC ---- */
+typedef struct orc_rounds orc_rounds;
+enum { ORC_OBJ_SUM = 0, ORC_OBJ_MINIMAX = 1 };
+orc_rounds* orc_rounds_create(const orc_instance* I, uint64_t seed, int64_t inst_id, double T0,
+                              double alpha, int32_t objective, int32_t steady_window, int32_t deny_after);
+void orc_rounds_destroy(orc_rounds* R);
+/* Run rounds until W quiet rounds or max_rounds.  digests[r] = state digest after round r. */
+int orc_rounds_run(orc_rounds* R, int32_t max_rounds, int32_t* rounds_run, int64_t* F_dec,
+                   int64_t* cost_dec, int32_t* dangling, uint64_t* digests);
+/* Churn: new alive mask [S][n] (NULL = unchanged) and edge updates
+ * [k][5] = {b (ignored), s, v_dst, u_src, new_cost}; s = -1 -> src[v_dst], s = S-1 -> snk[u_src]. */
+int orc_rounds_apply_churn(orc_rounds* R, const uint8_t* alive_new, const int32_t* updates, int64_t k);
+/* State export: up/down [S][n][max_cap] (encoded pointers), src_down/snk_up [M],
+ * kacc/deny [S][n], quiet, round. */
+int orc_rounds_export(const orc_rounds* R, int32_t* up, int32_t* down, int32_t* src_down, int32_t* snk_up,
+                      int32_t* kacc, int32_t* deny, int32_t* quiet, int64_t* round);
+uint64_t orc_rounds_digest(const orc_rounds* R);
+/* The instance as currently masked (after churn): cap_eff [S][n], src [n], snk [n], link [S-1][n][n]. */
+int orc_rounds_instance(const orc_rounds* R, int32_t* cap_eff, uint8_t* alive, int32_t* src, int32_t* snk,
+                        int32_t* link);
+/* LLaMA "crash during backward" victim rule; returns victim gid or -1. */
+int32_t orc_llama_victim(const orc_rounds* R, uint64_t draw_stage, uint64_t draw_pick);
+
+/* Whole per-instance workload of one bench step, for the cpu_baseline and
+ * the full-size parity samples: pre-churn rounds to quiescence, churn, cold SSP on
+ * the masked graph, repair rounds.  churn_kind 0 none, 1 random (alive_new +
+ * updates), 2 victim.  Per-instance outputs [B]. */
+typedef struct {
+  int64_t F, cost; int32_t A, rounds; int64_t F_dec, cost_dec; int32_t dangling, pre_rounds;
+  uint64_t digest;
+} orc_result;
+int orc_pipeline_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const int32_t* cap,
+                       const uint8_t* alive, const int32_t* src, const int32_t* snk, const int32_t* link,
+                       const int64_t* supply, int32_t churn_kind, const uint8_t* alive_new,
+                       const int32_t* updates, int64_t k_updates, const uint64_t* victim_draws,
+                       uint64_t seed, int64_t inst_base, double T0, double alpha, int32_t objective,
+                       int32_t W, int32_t deny_after, int32_t max_rounds, int32_t threads,
+                       orc_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
