@@ -1,0 +1,315 @@
+"""bench.py -- instances/sec of the GWTF routing hot path (BASELINE.json metric) on N B200s.
+
+One step = one pass of the whole hot path over this GPU's batch of the churn protocol
+(SURVEY.md 8(d)): apply_churn (crash/rejoin masks) -> cold exact SSP solve on the masked
+graph -> decentralized repair rounds to steady state -> (N>1) NCCL all_gather of the
+per-instance results.  The pre-churn converged state is built once (untimed) and restored
+before every step (untimed, like the L2 flush).  Workload: configs[1] of BASELINE.json
+(GPT-like 300M: 6 stages x 16 clients, 64 microbatches, 10% churn), B instances per GPU
+(weak scaling).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config gpt]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gwtf", choices=["gwtf", "reference"])
+    ap.add_argument("--config", default="gpt")
+    ap.add_argument("--batch", type=int, default=0, help="instances per GPU (default: the config's B)")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle instances for cpu_baseline (0 = auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e and cpu baseline (profiling runs)")
+    return ap.parse_args()
+
+
+def workload_name(cfg):
+    return (f"{cfg.name}: {cfg.S} stages x {cfg.n} clients/stage, M={cfg.M} microbatches, caps U{{{cfg.cap[0]}..{cfg.cap[1]}}}, "
+            + ("Eq.1 costs over 10 locations" if cfg.cost_kind == gen.COST_EQ1 else f"costs U{{{cfg.cost[0]}..{cfg.cost[1]}}}")
+            + f", churn={cfg.churn}")
+
+
+def algorithmic_bytes_ssp(cfg, A_total):
+    """an SSP shortest-path step examines every forward arc once:
+    bytes/augmentation = E x sizeof(cost), E = (S-1) n^2 + 2n, int32 costs."""
+    E = (cfg.S - 1) * cfg.n * cfg.n + 2 * cfg.n
+    return float(A_total) * E * 4
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.stop = index, [], threading.Event()
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(cfg, sample, inst0=0):
+    """The oracle (as it stands) on the host cores, on a bounded sample of the same workload."""
+    from tests import harness
+    threads = os.cpu_count() or 1
+    t = time.perf_counter()
+    harness.oracle_pipeline(cfg, inst0, sample, seed=0, threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": sample / dt, "unit": "instances/s", "cores": threads, "kind": "oracle",
+            "sample": f"{sample} instances of the same workload (full step: pre-churn rounds + churn + SSP + repair rounds), "
+                      f"{dt:.2f} s on {threads} threads"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle as it stands on the host cores, same metric/config."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample or max(64, threads * 48)
+    from tests import harness
+    for w in range(max(args.warmup, 0)):
+        harness.oracle_pipeline(cfg, w * sample, min(sample, 64), seed=0, threads=threads)
+    t = time.perf_counter()
+    for k in range(args.steps):
+        harness.oracle_pipeline(cfg, k * sample, sample, seed=0, threads=threads)
+    dt = time.perf_counter() - t
+    value = args.steps * sample / dt
+    line = {"impl": "reference", "metric": "min-cost-flow instances solved/sec", "value": value,
+            "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "instances_per_step": sample, "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": "instances/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{sample} instances per step (bounded sample of the workload)"},
+            "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = gen.CONFIGS[args.config]
+    if args.batch:
+        cfg = cfg.with_(B=args.batch)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21221_b200 import Flow
+    from paper_2509_21221_b200.dist import gather_results
+    from tests import harness
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B = cfg.B
+    inst0 = rank * B  # weak scaling: every rank owns B instances
+    mr = cfg.max_rounds
+
+    # ---------------- untimed setup: inputs resident in HBM, pre-churn converged state ----------
+    bt, src, snk, link = harness.device_inputs(cfg, inst0, B, device=dev)
+    fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0, inst_base=inst0)
+    fl.decentralized_rounds(mr)
+    an, upd = None, None
+    if cfg.churn == "random":
+        an, upd = harness.churn_inputs(cfg, inst0, bt.alive, device=dev)
+    elif cfg.churn == "victim":
+        st = fl.export_round_state()
+        an = torch.from_numpy(gen.llama_victims(st["up"].cpu().numpy(), st["down"].cpu().numpy(),
+                                                bt.alive.cpu().numpy(), gen.victim_draws(cfg, inst0, B))).to(dev)
+    fl.snapshot()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    sol = fl.solve_batch()
+    rr = fl.decentralized_rounds(mr)
+    stream = fl.stream
+
+    def step():
+        fl.apply_churn(an, upd)
+        fl.solve_batch(out=sol)
+        fl.decentralized_rounds(mr, out=rr)
+        return gather_results(sol, rr, world)
+
+    def prep():
+        fl.restore()
+        flush.random_(0, 255)  # evict L2 between timed steps
+
+    for _ in range(args.warmup):
+        prep()
+        step()
+    torch.cuda.synchronize()
+
+    fl.set_profiling(True)
+    total_ms = 0.0
+    A_total = 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            prep()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            ev0.record(stream)
+            g = step()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            total_ms += ev0.elapsed_time(ev1)
+            A_total += int(sol.augmentations.sum().item())
+    ktimes = fl.kernel_times()
+    fl.set_profiling(False)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = world * B * args.steps / (total_ms / 1e3)
+
+    # ---------------- roofline of the dominant kernel ----------------
+    peak, peak_src = load_peaks()
+    dom = max(ktimes, key=lambda k: ktimes[k][0])
+    dom_ms, dom_launches = ktimes[dom]
+    roof = {"kernel": dom, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src, "traffic": None}
+    if dom == "ssp_kernel":
+        alg = algorithmic_bytes_ssp(cfg, A_total)
+        roof["achieved"] = alg / (dom_ms / 1e3) / 1e9
+        roof["algorithmic_bytes_per_launch"] = alg / max(dom_launches, 1)
+    else:
+        # rounds: per round every slot's (up, down) state and every relay's advertiser row of the
+        # next stage is read once; units from the rounds actually run
+        rounds_total = int(rr.rounds_run.sum().item()) * args.steps
+        per_round = cfg.S * cfg.n * cfg.max_cap * 8 + cfg.S * cfg.n * cfg.n * 4 + 2 * cfg.M * 4
+        alg = float(rounds_total) * per_round
+        roof["achieved"] = alg / (dom_ms / 1e3) / 1e9
+        roof["algorithmic_bytes_per_launch"] = alg / max(dom_launches, 1)
+    roof["frac"] = roof["achieved"] / peak
+    kshare = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / total_ms if total_ms else None}
+              for k, v in ktimes.items()}
+
+    line = {"metric": "min-cost-flow instances solved/sec", "value": value, "unit": "instances/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+            "config": {"workload": workload_name(cfg), "instances_per_gpu": B, "global_instances": world * B,
+                       "max_rounds": mr, "l2": "flushed (256 MiB write) between timed steps; state restore untimed",
+                       "parallelism": f"instance-sharded x{world}"},
+            "roofline": roof, "kernels": kshare, "clocks": clk.summary(),
+            "gpu_launches": None}
+    # launches of our kernels per step: churn (edge updates if any + state clear) + ssp + rounds
+    per_step = 1 + (1 if upd is not None and upd.shape[0] else 0) + 1 + 1
+    line["gpu_launches"] = per_step * args.steps
+
+    if rank == 0 and not (args.quick or args.no_e2e):
+        line["e2e"] = e2e(cfg, B, inst0, dev, args)
+    if rank == 0 and not (args.quick or args.no_cpu_baseline):
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample or max(64, (os.cpu_count() or 1) * 32))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e(cfg, B, inst0, dev, args):
+    """The same metric end to end through the public API from pinned host buffers: create (H2D of
+    every input), base rounds, churn (H2D masks), exact solve, repair rounds, D2H of results."""
+    import torch
+
+    from paper_2509_21221_b200 import Flow
+    from tests import harness
+    bt, src, snk, link = harness.device_inputs(cfg, inst0, B, device=dev)
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    h = {k: pin(v) for k, v in dict(cap=bt.cap, alive=bt.alive, src=src, snk=snk, link=link, supply=bt.supply).items()}
+    an = upd = None
+    if cfg.churn == "random":
+        a, u = harness.churn_inputs(cfg, inst0, bt.alive, device=dev)
+        an, upd = pin(a), (pin(u) if u is not None else None)
+    h2d = sum(v.numel() * v.element_size() for v in h.values()) + (an.numel() if an is not None else 0) + (
+        upd.numel() * 4 if upd is not None else 0)
+    d2h = B * (8 + 8 + 4 + 4) + B * (4 + 8 + 8 + 4) * 2
+    times = []
+    for it in range(2 + max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        fl = Flow(h["cap"], h["src"], h["snk"], h["link"], h["supply"], max_cap=cfg.max_cap, alive=h["alive"],
+                  seed=0, inst_base=inst0, host=True)
+        fl.decentralized_rounds(cfg.max_rounds)
+        if cfg.churn == "random":
+            fl.apply_churn(an, upd)
+        elif cfg.churn == "victim":
+            st = fl.export_round_state()
+            a = gen.llama_victims(st["up"].numpy(), st["down"].numpy(), h["alive"].numpy(), gen.victim_draws(cfg, inst0, B))
+            fl.apply_churn(torch.from_numpy(a).pin_memory())
+        fl.solve_batch()
+        fl.decentralized_rounds(cfg.max_rounds)
+        fl.close()
+        torch.cuda.synchronize()
+        if it >= 2:
+            times.append(time.perf_counter() - t)
+    tm = float(np.median(times))
+    return {"value": B / tm, "unit": "instances/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "what": "create from pinned host buffers + base rounds + churn + exact solve + repair rounds + D2H results "
+                    "(wall clock, median; includes the base convergence the device-timed step restores)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -239,3 +239,58 @@ def linkdrop_to_updates(linkdrop, inst_offset: int = 0):
     out[:, 0] += inst_offset
     out[:, 4] = ABSENT
     return out
+
+
+# ----------------------------------------------------------------------------------------
+# Python twins of the counter hash (for the LLaMA victim draws) and the victim rule.  The
+# victim rule is harness logic (which relay crashes "during backward"): it
+# reads only slot occupancy of an exported round state, never the method's arithmetic.
+# ----------------------------------------------------------------------------------------
+_M64 = (1 << 64) - 1
+GEN_F_VICTIM_STAGE, GEN_F_VICTIM_PICK = 15, 16
+
+
+def mix64(z: int) -> int:
+    z &= _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def instance_seed(cfg: Config, inst: int, base_seed: int = BASE_SEED) -> int:
+    return mix64(base_seed ^ (cfg.cfg_id << 48) ^ inst)
+
+
+def draw(iseed: int, field_id: int, idx: int) -> int:
+    return mix64(mix64((iseed + field_id * 0x9E3779B97F4A7C15) & _M64) ^ idx)
+
+
+def pick(x: int, m: int) -> int:
+    return ((x >> 32) * m) >> 32
+
+
+def victim_draws(cfg: Config, inst0: int, B: int, base_seed: int = BASE_SEED) -> np.ndarray:
+    out = np.zeros((B, 2), np.uint64)
+    for b in range(B):
+        s = instance_seed(cfg, inst0 + b, base_seed)
+        out[b] = (draw(s, GEN_F_VICTIM_STAGE, 0), draw(s, GEN_F_VICTIM_PICK, 0))
+    return out
+
+
+def llama_victims(up, down, alive, draws) -> np.ndarray:
+    """'Crash during backward': draw a stage; among its alive relays holding a PAIRED slot
+    (ascending index) crash the drawn one; if none, try the next stage.  up/down [B][S][n][MC]
+    (numpy, exported round state), alive [B][S][n].  Returns the new alive mask."""
+    up, down, alive = np.asarray(up), np.asarray(down), np.asarray(alive)
+    B, S, n, _ = up.shape
+    paired = ((up != -1) & (down != -1)).any(axis=3) & (alive != 0)
+    out = alive.copy()
+    for b in range(B):
+        s0 = pick(int(draws[b, 0]), S)
+        for t in range(S):
+            s = (s0 + t) % S
+            cand = np.nonzero(paired[b, s])[0]
+            if cand.size:
+                out[b, s, cand[pick(int(draws[b, 1]), cand.size)]] = 0
+                break
+    return out

@@ -282,8 +282,9 @@ def pipeline_batch(cfg, cap, alive, src, snk, link, supply, churn_kind=0, alive_
                                   out)
     if rc != 0:
         raise RuntimeError(f"oracle pipeline failed rc={rc}")
-    names = [f[0] for f in OrcResult._fields_]
-    return {k: np.array([getattr(out[b], k) for b in range(B)]) for k in names}
+    dt = {"digest": np.uint64, "F": np.int64, "cost": np.int64, "F_dec": np.int64, "cost_dec": np.int64}
+    return {k: np.array([getattr(out[b], k) for b in range(B)], dtype=dt.get(k, np.int32))
+            for k, _ in OrcResult._fields_}
 
 
 # ----------------------------------------------------------------------------------------

@@ -1,0 +1,565 @@
+// gwtf_api.cpp -- host side of the C-ABI declared in include/gwtf.h: validation, the handle's
+// device workspace, the annealing threshold table and kernel orchestration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gwtf.h"
+#include "gwtf_internal.h"
+
+namespace gwtf {
+size_t ssp_global_ws_bytes(const Problem& P);
+}
+
+using namespace gwtf;
+
+namespace {
+
+thread_local std::string g_err;
+
+gwtf_status fail(gwtf_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct Timer {
+  std::string name;
+  cudaEvent_t a, b;
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct gwtf_flow_s {
+  Problem P{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t flags = 0;
+  int num_sms = 148;
+  bool poisoned = false;
+  bool has_assignment = false;
+  std::vector<void*> allocs;
+  // snapshot of the mutable state
+  std::vector<std::pair<void*, size_t>> mutable_bufs;
+  std::vector<void*> snap;
+  bool has_snapshot = false;
+  // host-pointer mode scratch (device copies of outputs)
+  std::vector<DevBuf> scratch;
+  // profiling
+  bool profiling = false;
+  std::vector<Timer> pending;
+  std::vector<std::string> names;
+  std::vector<float> ms;
+  std::vector<int32_t> launches;
+  int32_t* bad_flag = nullptr;
+};
+
+namespace {
+
+bool host_mode(const gwtf_flow_s* h) { return (h->flags & GWTF_HOST_PTRS) != 0; }
+
+gwtf_status cuda_fail(gwtf_flow_s* h, cudaError_t e, const char* where) {
+  if (h) h->poisoned = true;
+  return fail(GWTF_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(h, expr)                                           \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return cuda_fail((h), _e, #expr);  \
+  } while (0)
+
+template <class T>
+gwtf_status alloc(gwtf_flow_s* h, T** p, size_t count, bool is_mutable = false) {
+  if (count == 0) count = 1;
+  void* q = nullptr;
+  if (cudaMalloc(&q, count * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GWTF_E_NOMEM, "cudaMalloc failed (" + std::to_string(count * sizeof(T)) + " bytes)");
+  }
+  h->allocs.push_back(q);
+  if (is_mutable) h->mutable_bufs.push_back({q, count * sizeof(T)});
+  *p = static_cast<T*>(q);
+  return GWTF_OK;
+}
+
+// device scratch slot i of at least `bytes` (host-pointer mode)
+void* scratch(gwtf_flow_s* h, size_t i, size_t bytes) {
+  if (h->scratch.size() <= i) h->scratch.resize(i + 1);
+  DevBuf& b = h->scratch[i];
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    b.bytes = bytes;
+  }
+  return b.p;
+}
+
+void prof_begin(gwtf_flow_s* h, const char* name, Timer* t) {
+  if (!h->profiling) return;
+  t->name = name;
+  cudaEventCreate(&t->a);
+  cudaEventCreate(&t->b);
+  cudaEventRecord(t->a, h->stream);
+}
+void prof_end(gwtf_flow_s* h, Timer* t) {
+  if (!h->profiling) return;
+  cudaEventRecord(t->b, h->stream);
+  h->pending.push_back(*t);
+}
+
+// Annealing thresholds thr[k][delta] = min(2^32-1, floor(exp(-delta/(T0 alpha^k)) 2^32))
+// ("T reduced after each accepted change by a factor alpha"),
+// IEEE double with the host libm, no fast-math.
+uint32_t thr_value(double T0, double alpha, int k, int delta) {
+  const double T = T0 * std::pow(alpha, (double)k);
+  const double v = std::floor(std::exp(-(double)delta / T) * 4294967296.0);
+  if (v >= 4294967295.0) return 4294967295u;
+  if (v <= 0.0) return 0u;
+  return (uint32_t)v;
+}
+
+gwtf_status anneal_table(double T0, double alpha, std::vector<uint32_t>& t, int32_t& width, int32_t& K) {
+  if (!(T0 > 0.0)) {
+    width = 1;
+    K = 0;
+    t.assign(1, 0);
+    return GWTF_OK;
+  }
+  if (!(alpha > 0.0 && alpha < 1.0)) return fail(GWTF_E_INVALID, "alpha must be in (0,1) when T0 > 0");
+  width = 1;
+  while (thr_value(T0, alpha, 0, width) != 0)
+    if (++width > (1 << 20)) return fail(GWTF_E_INVALID, "T0 too large: annealing table wider than 2^20");
+  K = 0;
+  while (thr_value(T0, alpha, K, 1) != 0)
+    if (++K > (1 << 16)) return fail(GWTF_E_INVALID, "alpha too close to 1: more than 2^16 temperature levels");
+  if ((int64_t)(K + 1) * width > (1 << 24)) return fail(GWTF_E_INVALID, "annealing table too large");
+  t.assign((size_t)(K + 1) * width, 0);
+  for (int k = 0; k <= K; ++k)
+    for (int d = 1; d < width; ++d) t[(size_t)k * width + d] = thr_value(T0, alpha, k, d);
+  return GWTF_OK;
+}
+
+// copy an input array (host or device) to a device buffer on the stream
+gwtf_status copy_in(gwtf_flow_s* h, void* dst, const void* src, size_t bytes) {
+  CK(h, cudaMemcpyAsync(dst, src, bytes, host_mode(h) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                        h->stream));
+  return GWTF_OK;
+}
+
+// outputs: in host mode write to device scratch, then copy out after the launch
+struct OutMap {
+  void* user;
+  void* dev;
+  size_t bytes;
+};
+
+template <class T>
+gwtf_status map_out(gwtf_flow_s* h, T* user, size_t count, size_t slot, T** dev, std::vector<OutMap>& maps) {
+  if (!user) { *dev = nullptr; return GWTF_OK; }
+  if (!host_mode(h)) { *dev = user; return GWTF_OK; }
+  void* d = scratch(h, slot, std::max<size_t>(count * sizeof(T), 16));
+  if (!d) return fail(GWTF_E_NOMEM, "output scratch allocation failed");
+  *dev = static_cast<T*>(d);
+  maps.push_back({user, d, count * sizeof(T)});
+  return GWTF_OK;
+}
+
+gwtf_status finish_out(gwtf_flow_s* h, const std::vector<OutMap>& maps) {
+  for (const OutMap& m : maps) CK(h, cudaMemcpyAsync(m.user, m.dev, m.bytes, cudaMemcpyDeviceToHost, h->stream));
+  if (host_mode(h)) CK(h, cudaStreamSynchronize(h->stream));
+  return GWTF_OK;
+}
+
+gwtf_status enter(gwtf_flow_s* h) {
+  if (!h) return fail(GWTF_E_INVALID, "NULL handle");
+  if (h->poisoned) return fail(GWTF_E_CUDA, "handle poisoned by an earlier CUDA error");
+  CK(h, cudaSetDevice(h->device));
+  return GWTF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gwtf_last_error(void) { return g_err.c_str(); }
+int32_t gwtf_abi_version(void) { return GWTF_ABI_VERSION; }
+
+gwtf_status gwtf_eq1_cost_tiles(int32_t B, int32_t S, int32_t n, int32_t L, const int32_t* comp, const int32_t* loc,
+                                const int32_t* dloc, const int32_t* lat, const int32_t* bw, int64_t size_kbit,
+                                int32_t* src_out, int32_t* snk_out, int32_t* link_out, void* stream) {
+  if (B < 1 || S < 1 || n < 1 || L < 1 || size_kbit < 0)
+    return fail(GWTF_E_INVALID, "eq1: B, S, n, L must be >= 1 and size >= 0");
+  if (!comp || !loc || !dloc || !lat || !bw || !src_out || !snk_out || (S > 1 && !link_out))
+    return fail(GWTF_E_INVALID, "eq1: NULL array");
+  cudaError_t e = launch_eq1(B, S, n, L, comp, loc, dloc, lat, bw, size_kbit, src_out, snk_out, link_out,
+                             (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(GWTF_E_CUDA, std::string("eq1: ") + cudaGetErrorString(e));
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
+  if (!d || !out) return fail(GWTF_E_INVALID, "NULL desc/out");
+  *out = nullptr;
+  if (d->abi_version != GWTF_ABI_VERSION) return fail(GWTF_E_INVALID, "abi_version mismatch");
+  const int64_t B = d->num_instances, S = d->num_stages, n = d->clients_per_stage, MC = d->max_cap;
+  if (B < 1 || S < 1 || n < 1) return fail(GWTF_E_INVALID, "num_instances, num_stages, clients_per_stage must be >= 1");
+  if (MC < 0 || MC > 32) return fail(GWTF_E_INVALID, "max_cap must be in [0, 32]");
+  if (n > 4096) return fail(GWTF_E_UNSUPPORTED, "clients_per_stage > 4096");
+  if (S * n >= (1 << 21)) return fail(GWTF_E_UNSUPPORTED, "S*n >= 2^21");
+  if (!d->cap || !d->src_cost || !d->snk_cost || !d->supply || (S > 1 && !d->link_cost))
+    return fail(GWTF_E_INVALID, "NULL input array");
+  if (d->steady_window < 1 || d->deny_after < 1) return fail(GWTF_E_INVALID, "steady_window, deny_after must be >= 1");
+  if (d->objective != GWTF_OBJ_SUM && d->objective != GWTF_OBJ_MINIMAX) return fail(GWTF_E_INVALID, "objective");
+  std::vector<uint32_t> thr;
+  int32_t width = 1, K = 0;
+  gwtf_status st = anneal_table(d->T0, d->alpha, thr, width, K);
+  if (st != GWTF_OK) return st;
+
+  gwtf_flow_s* h = new gwtf_flow_s();
+  h->device = d->device;
+  h->stream = (cudaStream_t)d->stream;
+  h->flags = d->flags;
+  auto bail = [&](gwtf_status s) {
+    gwtf_flow_destroy(h);
+    return s;
+  };
+  if (cudaSetDevice(h->device) != cudaSuccess) { cudaGetLastError(); delete h; return fail(GWTF_E_CUDA, "cudaSetDevice"); }
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  Problem& P = h->P;
+  P.B = (int32_t)B; P.S = (int32_t)S; P.n = (int32_t)n; P.MC = (int32_t)MC;
+  P.ld = (int32_t)((n + 3) / 4 * 4);
+  const size_t Sn = (size_t)S * n, nb = (size_t)(S - 1);
+
+  // supply -> host for validation and Mmax
+  std::vector<int64_t> sup(B);
+  if (host_mode(h)) std::memcpy(sup.data(), d->supply, B * sizeof(int64_t));
+  else if (cudaMemcpy(sup.data(), d->supply, B * sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(fail(GWTF_E_INVALID, "supply is not a readable device pointer"));
+  }
+  int64_t Mmax = 0;
+  for (int64_t v : sup) {
+    if (v < 0) return bail(fail(GWTF_E_INVALID, "negative supply"));
+    Mmax = std::max(Mmax, v);
+  }
+  if (Mmax >= (1 << 24)) return bail(fail(GWTF_E_UNSUPPORTED, "supply >= 2^24"));
+  P.Mmax = std::max<int64_t>(Mmax, 1);
+  P.Lcap = (int32_t)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(Mmax, n * std::max<int64_t>(MC, 1)), n * n));
+
+  gwtf_status s;
+#define AL(ptr, cnt, mut) if ((s = alloc(h, &(ptr), (cnt), (mut))) != GWTF_OK) return bail(s)
+  AL(P.tile, B * nb * n * P.ld, true);
+  AL(P.src, B * n, true);
+  AL(P.snk, B * n, true);
+  AL(P.cap, B * Sn, false);
+  AL(P.alive, B * Sn, true);
+  AL(P.supply, B, false);
+  AL(P.g, B * Sn, false);
+  AL(P.src_f, B * n, false);
+  AL(P.snk_f, B * n, false);
+  AL(P.arcs, B * nb * P.Lcap, false);
+  AL(P.arc_cnt, B * std::max<size_t>(nb, 1), false);
+  const size_t nslot = B * Sn * std::max<int64_t>(MC, 1);
+  AL(P.up, nslot, true);
+  AL(P.down, nslot, true);
+  AL(P.src_down, B * P.Mmax, true);
+  AL(P.snk_up, B * P.Mmax, true);
+  AL(P.kacc, B * Sn, true);
+  AL(P.deny, B * Sn, true);
+  AL(P.quiet, B, true);
+  AL(P.round, B, true);
+  AL(P.scost, nslot, false);
+  AL(P.adv_cost, B * Sn, false);
+  AL(P.adv_slot, B * Sn, false);
+  AL(P.req_slot, B * (Sn + 1), false);
+  AL(P.req_target, B * (Sn + 1), false);
+  AL(P.prop, B * Sn * 6, false);
+  AL(P.prop_key, B * Sn, false);
+  AL(P.prop_touch, B * Sn * 4, false);
+  AL(P.res, B * (Sn * std::max<int64_t>(MC, 1) + 2 * P.Mmax), false);
+  AL(P.counters, 8, false);
+  AL(h->bad_flag, 4, false);
+  uint32_t* thr_d = nullptr;
+  AL(thr_d, thr.size(), false);
+  int32_t* link_tmp = nullptr;
+  if (nb) AL(link_tmp, B * nb * n * n, false);
+#undef AL
+  P.thr = thr_d;
+  P.thr_width = width;
+  P.thr_K = K;
+  P.seed = d->seed;
+  P.inst_base = d->inst_base;
+  P.objective = d->objective;
+  P.W = d->steady_window;
+  P.deny_after = d->deny_after;
+
+  // global workspace for the shared-memory-overflow tier of the exact solve
+  if (ssp_smem_bytes(P) > 227 * 1024 || (h->flags & GWTF_FORCE_GLOBAL_TIER)) {
+    P.ws_teams = (int32_t)std::min<int64_t>(h->num_sms, B);
+    P.ws_per_team = ssp_global_ws_bytes(P);
+    uint8_t* ws = nullptr;
+    if ((s = alloc(h, &ws, (size_t)P.ws_teams * P.ws_per_team)) != GWTF_OK) return bail(s);
+    P.ws = ws;
+  }
+
+  // inputs
+  if ((s = copy_in(h, P.cap, d->cap, B * Sn * 4)) != GWTF_OK) return bail(s);
+  if (d->alive) {
+    if ((s = copy_in(h, P.alive, d->alive, B * Sn)) != GWTF_OK) return bail(s);
+  } else if (cudaMemsetAsync(P.alive, 1, B * Sn, h->stream) != cudaSuccess) {
+    return bail(cuda_fail(h, cudaGetLastError(), "memset alive"));
+  }
+  if ((s = copy_in(h, P.src, d->src_cost, B * n * 4)) != GWTF_OK) return bail(s);
+  if ((s = copy_in(h, P.snk, d->snk_cost, B * n * 4)) != GWTF_OK) return bail(s);
+  if ((s = copy_in(h, P.supply, d->supply, B * 8)) != GWTF_OK) return bail(s);
+  if (nb) {
+    if ((s = copy_in(h, link_tmp, d->link_cost, B * nb * n * n * 4)) != GWTF_OK) return bail(s);
+    if (launch_pad_tiles(P, link_tmp, h->stream) != cudaSuccess) return bail(cuda_fail(h, cudaGetLastError(), "pad"));
+  }
+  if (cudaMemcpyAsync(thr_d, thr.data(), thr.size() * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+    return bail(cuda_fail(h, cudaGetLastError(), "thr upload"));
+
+  // validation scans: costs in [0, 2^30) or absent, caps in [0, max_cap]
+  int32_t* mm = h->bad_flag;  // [0] max cost, [1] min cost, [2] max cap, [3] min cap
+  const int32_t init[4] = {INT32_MIN, INT32_MAX, INT32_MIN, INT32_MAX};
+  CK(h, cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
+  CK(h, launch_scan_costs(P.src, B * n, mm + 0, mm + 1, h->stream));
+  CK(h, launch_scan_costs(P.snk, B * n, mm + 0, mm + 1, h->stream));
+  if (nb) CK(h, launch_scan_costs(link_tmp, B * nb * n * n, mm + 0, mm + 1, h->stream));
+  CK(h, launch_scan_costs(P.cap, B * Sn, mm + 2, mm + 3, h->stream));
+  int32_t got[4];
+  CK(h, cudaMemcpyAsync(got, mm, sizeof(got), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (got[1] < 0) return bail(fail(GWTF_E_INVALID, "negative cost"));
+  const int64_t maxc = std::max<int32_t>(got[0], 0);
+  if (maxc >= (1 << 30)) return bail(fail(GWTF_E_INVALID, "cost >= 2^30 (other than GWTF_ABSENT)"));
+  if (got[3] < 0 || got[2] > MC) return bail(fail(GWTF_E_INVALID, "cap outside [0, max_cap]"));
+  const long double bound = (long double)(2 * S * n + 2) * (long double)maxc;
+  if (bound >= (long double)(1ull << 42)) return bail(fail(GWTF_E_OVERFLOW, "(2Sn+2)*maxcost >= 2^42"));
+  if (bound * (long double)Mmax >= (long double)(1ull << 62)) return bail(fail(GWTF_E_OVERFLOW, "(2Sn+2)*maxcost*M >= 2^62"));
+  if (link_tmp) {
+    cudaFree(link_tmp);
+    h->allocs.erase(std::find(h->allocs.begin(), h->allocs.end(), (void*)link_tmp));
+  }
+  CK(h, launch_init_round_state(P, h->stream));
+  CK(h, cudaMemsetAsync(P.arc_cnt, 0, B * std::max<size_t>(nb, 1) * 4, h->stream));
+  *out = h;
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_solve_batch(gwtf_flow_t h, int64_t* flow_value, int64_t* total_cost, int32_t* augmentations,
+                                  int32_t* inst_status) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!flow_value || !total_cost) return fail(GWTF_E_INVALID, "flow_value/total_cost must not be NULL");
+  const size_t B = h->P.B;
+  std::vector<OutMap> maps;
+  SspOut o{};
+  if ((s = map_out(h, flow_value, B, 0, &o.F, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, total_cost, B, 1, &o.cost, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, augmentations, B, 2, &o.A, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, inst_status, B, 3, &o.status, maps)) != GWTF_OK) return s;
+  Timer t;
+  prof_begin(h, "ssp_kernel", &t);
+  CK(h, launch_ssp(h->P, o, h->stream, h->num_sms, (h->flags & GWTF_FORCE_GLOBAL_TIER) != 0));
+  prof_end(h, &t);
+  h->has_assignment = true;
+  return finish_out(h, maps);
+}
+
+gwtf_status gwtf_flow_decentralized_rounds(gwtf_flow_t h, int32_t max_rounds, int32_t* rounds_run, int64_t* dec_flow,
+                                           int64_t* dec_cost, int32_t* dangling, uint64_t* round_digests) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (max_rounds < 0) return fail(GWTF_E_INVALID, "max_rounds < 0");
+  const size_t B = h->P.B;
+  std::vector<OutMap> maps;
+  RoundsOut o{};
+  o.max_rounds = max_rounds;
+  if ((s = map_out(h, rounds_run, B, 4, &o.rounds_run, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, dec_flow, B, 5, &o.F_dec, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, dec_cost, B, 6, &o.cost_dec, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, dangling, B, 7, &o.dangling, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, round_digests, B * std::max(max_rounds, 1), 8, &o.digests, maps)) != GWTF_OK) return s;
+  Timer t;
+  prof_begin(h, "rounds_kernel", &t);
+  CK(h, launch_rounds(h->P, o, h->stream, h->num_sms));
+  prof_end(h, &t);
+  return finish_out(h, maps);
+}
+
+gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const int32_t* edge_updates, int64_t k) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (k < 0 || (k > 0 && !edge_updates)) return fail(GWTF_E_INVALID, "edge_updates/k");
+  const Problem& P = h->P;
+  const uint8_t* a = alive_new;
+  const int32_t* u = k > 0 ? edge_updates : nullptr;
+  if (host_mode(h)) {
+    if (alive_new) {
+      void* d = scratch(h, 9, (size_t)P.B * P.S * P.n);
+      if (!d) return fail(GWTF_E_NOMEM, "scratch");
+      CK(h, cudaMemcpyAsync(d, alive_new, (size_t)P.B * P.S * P.n, cudaMemcpyHostToDevice, h->stream));
+      a = (const uint8_t*)d;
+    }
+    if (u) {
+      void* d = scratch(h, 10, (size_t)k * 20);
+      if (!d) return fail(GWTF_E_NOMEM, "scratch");
+      CK(h, cudaMemcpyAsync(d, edge_updates, (size_t)k * 20, cudaMemcpyHostToDevice, h->stream));
+      u = (const int32_t*)d;
+    }
+  }
+  CK(h, cudaMemsetAsync(h->bad_flag, 0, 4, h->stream));
+  Timer t;
+  prof_begin(h, "churn", &t);
+  CK(h, launch_churn(P, a, u, k, h->bad_flag, h->stream));
+  prof_end(h, &t);
+  h->has_assignment = false;
+  if (u) {
+    int32_t bad = 0;
+    CK(h, cudaMemcpyAsync(&bad, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (bad) return fail(GWTF_E_INVALID, "edge update out of range (valid updates were applied)");
+  }
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_get_assignment(gwtf_flow_t h, int32_t* node_flow, int32_t* src_flow, int32_t* snk_flow,
+                                     int32_t* arc_flow_dense) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!h->has_assignment) return fail(GWTF_E_STATE, "no solve_batch since create/churn");
+  const Problem& P = h->P;
+  const size_t Sn = (size_t)P.S * P.n, nb = (size_t)(P.S - 1);
+  const cudaMemcpyKind kind = host_mode(h) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (node_flow) CK(h, cudaMemcpyAsync(node_flow, P.g, P.B * Sn * 4, kind, h->stream));
+  if (src_flow) CK(h, cudaMemcpyAsync(src_flow, P.src_f, (size_t)P.B * P.n * 4, kind, h->stream));
+  if (snk_flow) CK(h, cudaMemcpyAsync(snk_flow, P.snk_f, (size_t)P.B * P.n * 4, kind, h->stream));
+  if (arc_flow_dense && nb) {
+    const size_t bytes = (size_t)P.B * nb * P.n * P.n * 4;
+    int32_t* dst = arc_flow_dense;
+    if (host_mode(h)) {
+      dst = (int32_t*)scratch(h, 11, bytes);
+      if (!dst) return fail(GWTF_E_NOMEM, "scratch");
+    }
+    CK(h, cudaMemsetAsync(dst, 0, bytes, h->stream));
+    CK(h, launch_dense_arcs(P, dst, h->stream));
+    if (host_mode(h)) CK(h, cudaMemcpyAsync(arc_flow_dense, dst, bytes, cudaMemcpyDeviceToHost, h->stream));
+  }
+  if (host_mode(h)) CK(h, cudaStreamSynchronize(h->stream));
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_export_round_state(gwtf_flow_t h, int32_t* up, int32_t* down, int32_t* src_down,
+                                         int32_t* snk_up, int32_t* kacc, int32_t* deny, int32_t* quiet,
+                                         int64_t* round) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  const Problem& P = h->P;
+  const size_t Sn = (size_t)P.S * P.n;
+  const size_t nslot = (size_t)P.B * Sn * P.MC;
+  const cudaMemcpyKind kind = host_mode(h) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (up && nslot) CK(h, cudaMemcpyAsync(up, P.up, nslot * 4, kind, h->stream));
+  if (down && nslot) CK(h, cudaMemcpyAsync(down, P.down, nslot * 4, kind, h->stream));
+  if (src_down) CK(h, cudaMemcpyAsync(src_down, P.src_down, (size_t)P.B * P.Mmax * 4, kind, h->stream));
+  if (snk_up) CK(h, cudaMemcpyAsync(snk_up, P.snk_up, (size_t)P.B * P.Mmax * 4, kind, h->stream));
+  if (kacc) CK(h, cudaMemcpyAsync(kacc, P.kacc, P.B * Sn * 4, kind, h->stream));
+  if (deny) CK(h, cudaMemcpyAsync(deny, P.deny, P.B * Sn * 4, kind, h->stream));
+  if (quiet) CK(h, cudaMemcpyAsync(quiet, P.quiet, (size_t)P.B * 4, kind, h->stream));
+  if (round) CK(h, cudaMemcpyAsync(round, P.round, (size_t)P.B * 8, kind, h->stream));
+  if (host_mode(h)) CK(h, cudaStreamSynchronize(h->stream));
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_snapshot(gwtf_flow_t h) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!h->has_snapshot) {
+    for (auto& mb : h->mutable_bufs) {
+      void* q = nullptr;
+      if (cudaMalloc(&q, mb.second) != cudaSuccess) { cudaGetLastError(); return fail(GWTF_E_NOMEM, "snapshot"); }
+      h->snap.push_back(q);
+    }
+    h->has_snapshot = true;
+  }
+  for (size_t i = 0; i < h->mutable_bufs.size(); ++i)
+    CK(h, cudaMemcpyAsync(h->snap[i], h->mutable_bufs[i].first, h->mutable_bufs[i].second, cudaMemcpyDeviceToDevice,
+                          h->stream));
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_restore(gwtf_flow_t h) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!h->has_snapshot) return fail(GWTF_E_STATE, "no snapshot");
+  for (size_t i = 0; i < h->mutable_bufs.size(); ++i)
+    CK(h, cudaMemcpyAsync(h->mutable_bufs[i].first, h->snap[i], h->mutable_bufs[i].second, cudaMemcpyDeviceToDevice,
+                          h->stream));
+  h->has_assignment = false;
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_set_profiling(gwtf_flow_t h, int32_t on) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  h->profiling = on != 0;
+  for (Timer& t : h->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  h->pending.clear();
+  h->names.clear();
+  h->ms.clear();
+  h->launches.clear();
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_kernel_times(gwtf_flow_t h, const char** names, float* ms, int32_t* launches, int32_t cap,
+                                   int32_t* count) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  for (Timer& t : h->pending) {
+    CK(h, cudaEventSynchronize(t.b));
+    float v = 0.f;
+    CK(h, cudaEventElapsedTime(&v, t.a, t.b));
+    size_t i = std::find(h->names.begin(), h->names.end(), t.name) - h->names.begin();
+    if (i == h->names.size()) { h->names.push_back(t.name); h->ms.push_back(0.f); h->launches.push_back(0); }
+    h->ms[i] += v;
+    h->launches[i] += 1;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  h->pending.clear();
+  const int32_t c = (int32_t)h->names.size();
+  if (count) *count = c;
+  for (int32_t i = 0; i < std::min(c, cap); ++i) {
+    if (names) names[i] = h->names[i].c_str();
+    if (ms) ms[i] = h->ms[i];
+    if (launches) launches[i] = h->launches[i];
+  }
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_destroy(gwtf_flow_t h) {
+  if (!h) return GWTF_OK;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  for (Timer& t : h->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+  for (void* p : h->allocs) cudaFree(p);
+  for (void* p : h->snap) cudaFree(p);
+  for (DevBuf& b : h->scratch) if (b.p) cudaFree(b.p);
+  cudaGetLastError();
+  delete h;
+  return GWTF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Internal declarations shared by the host API (gwtf_api.cpp) and the kernels (*.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gwtf {
+
+constexpr int32_t kAbsent = INT32_MAX;
+constexpr int kHopBits = 20;                 // packed key = cost << 20 | hops
+constexpr uint64_t kKeyInf = ~0ull;
+constexpr int32_t kNone = -1;                // round-state pointer encoding
+
+// Everything a kernel needs about a batch; all pointers are device pointers owned by the handle.
+struct Problem {
+  int32_t B, S, n, ld, MC;     // ld = row stride of the padded tiles (n rounded up to 4)
+  int64_t Mmax;                // max supply over the batch (SRC/SNK slot arrays)
+  int32_t Lcap;                // positive-arc list capacity per boundary
+  int32_t* tile;               // [B][S-1][n][ld] dest-major, padding = kAbsent
+  int32_t* src;                // [B][n]
+  int32_t* snk;                // [B][n]
+  int32_t* cap;                // [B][S][n]
+  uint8_t* alive;              // [B][S][n]
+  int64_t* supply;             // [B]
+  // exact-solve state (persistent for get_assignment)
+  int32_t* g;                  // [B][S][n]
+  int32_t* src_f;              // [B][n]
+  int32_t* snk_f;              // [B][n]
+  uint32_t* arcs;              // [B][S-1][Lcap]  (u << 20 | v << 8 | f)
+  int32_t* arc_cnt;            // [B][S-1]
+  // round state
+  int32_t* up;                 // [B][S*n*MC]
+  int32_t* down;               // [B][S*n*MC]
+  int32_t* src_down;           // [B][Mmax]
+  int32_t* snk_up;             // [B][Mmax]
+  int32_t* kacc;               // [B][S*n]
+  int32_t* deny;               // [B][S*n]
+  int32_t* quiet;              // [B]
+  int64_t* round;              // [B]
+  // round scratch (global; L1/L2 resident per team)
+  int64_t* scost;              // [B][S*n*MC] cost to sink per slot
+  int64_t* adv_cost;           // [B][S*n]
+  int32_t* adv_slot;           // [B][S*n]
+  int32_t* req_slot;           // [B][S*n + 1]  requester slot (index S*n = data node)
+  int32_t* req_target;         // [B][S*n + 1]  target gid, -1 = D-sink, -2 none
+  int32_t* prop;               // [B][S*n][6]   proposal: kind, x, y, z, t0..t3 packed below
+  uint64_t* prop_key;          // [B][S*n]
+  int64_t* prop_touch;         // [B][S*n][4]   reservation ids touched
+  uint64_t* res;               // [B][S*n*MC + 2*Mmax] reservation minima
+  // parameters of the rounds
+  uint64_t seed;
+  int64_t inst_base;
+  int32_t objective, W, deny_after;
+  const uint32_t* thr;         // [(K+1)][width]
+  int32_t thr_width, thr_K;
+  // persistent work queue counter(s)
+  int32_t* counters;           // [8]
+  // global workspace for teams whose instance does not fit in shared memory
+  uint8_t* ws;
+  size_t ws_per_team;
+  int32_t ws_teams;
+};
+
+struct SspOut {
+  int64_t* F; int64_t* cost; int32_t* A; int32_t* status;
+};
+
+struct RoundsOut {
+  int32_t max_rounds;
+  int32_t* rounds_run; int64_t* F_dec; int64_t* cost_dec; int32_t* dangling; uint64_t* digests;
+};
+
+// launchers (return cudaGetLastError())
+size_t ssp_smem_bytes(const Problem& P);
+size_t ssp_global_ws_bytes(const Problem& P);
+cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, bool force_global);
+cudaError_t launch_rounds(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms);
+cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st);
+cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32_t* upd, int64_t k,
+                         int32_t* bad_flag, cudaStream_t st);
+cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st);
+cudaError_t launch_dense_arcs(const Problem& P, int32_t* dense, cudaStream_t st);
+cudaError_t launch_eq1(int32_t B, int32_t S, int32_t n, int32_t L, const int32_t* comp, const int32_t* loc,
+                       const int32_t* dloc, const int32_t* lat, const int32_t* bw, int64_t size_kbit,
+                       int32_t* src, int32_t* snk, int32_t* link, cudaStream_t st);
+cudaError_t launch_scan_costs(const int32_t* v, int64_t count, int32_t* out_max, int32_t* out_min,
+                              cudaStream_t st);
+
+}  // namespace gwtf

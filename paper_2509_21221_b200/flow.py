@@ -1,0 +1,195 @@
+"""Thin Python binding of the C-ABI (include/gwtf.h).  Argument marshalling only: every step of
+the hot path runs in libgwtf.so's sm_100a kernels.  PyTorch supplies device memory and streams.
+
+Two modes, mirroring GWTF_HOST_PTRS:
+  * device (default): inputs/outputs are CUDA torch tensors on the handle's device; calls are
+    asynchronous on the stream;
+  * host: inputs/outputs are host (ideally pinned) torch tensors; the library copies.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+ABSENT = 2**31 - 1
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _need(t, dtype, shape, name, device):
+    if t is None:
+        raise ValueError(f"{name} is required")
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected {dtype} {tuple(shape)}, got {t.dtype} {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if device is None:
+        if t.is_cuda:
+            raise ValueError(f"{name} must be a host tensor on a host-pointer handle")
+    elif t.device != device:
+        raise ValueError(f"{name} must live on {device}")
+    return t
+
+
+def eq1_cost_tiles(comp, loc, dloc, lat, bw, size_kbit: int, stream=None):
+    """Eq. 1 on the device in integer half-units -> (src[B][n], snk[B][n],
+    link[B][S-1][n][n]).  All inputs int32 CUDA tensors."""
+    B, S, n = comp.shape
+    L = lat.shape[1]
+    dev = comp.device
+    src = torch.empty((B, n), dtype=torch.int32, device=dev)
+    snk = torch.empty((B, n), dtype=torch.int32, device=dev)
+    link = torch.empty((B, max(S - 1, 0), n, n), dtype=torch.int32, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check("gwtf_eq1_cost_tiles", lib().gwtf_eq1_cost_tiles(
+        B, S, n, L, _ptr(comp), _ptr(loc), _ptr(dloc), _ptr(lat), _ptr(bw), int(size_kbit),
+        _ptr(src), _ptr(snk), _ptr(link) if link.numel() else None, st.cuda_stream))
+    return src, snk, link
+
+
+@dataclass
+class SolveResult:
+    flow_value: torch.Tensor
+    total_cost: torch.Tensor
+    augmentations: torch.Tensor
+    status: torch.Tensor
+
+
+@dataclass
+class RoundsResult:
+    rounds_run: torch.Tensor
+    dec_flow: torch.Tensor
+    dec_cost: torch.Tensor
+    dangling: torch.Tensor
+    digests: torch.Tensor | None
+
+
+class Flow:
+    """A batch of B routing instances living on one device (gwtf_flow_t)."""
+
+    def __init__(self, cap, src_cost, snk_cost, link_cost, supply, *, max_cap, alive=None, seed=0, inst_base=0,
+                 T0=1.7, alpha=0.95, objective=_lib.OBJ_SUM, steady_window=5, deny_after=3, stream=None,
+                 host=False, force_global_tier=False):
+        B, S, n = cap.shape
+        self.B, self.S, self.n, self.max_cap = B, S, n, max_cap
+        self.host = host
+        if host:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+            dev_check = None
+        else:
+            self.device = cap.device
+            dev_check = cap.device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _need(cap, torch.int32, (B, S, n), "cap", dev_check)
+        _need(src_cost, torch.int32, (B, n), "src_cost", dev_check)
+        _need(snk_cost, torch.int32, (B, n), "snk_cost", dev_check)
+        if S > 1:
+            _need(link_cost, torch.int32, (B, S - 1, n, n), "link_cost", dev_check)
+        _need(supply, torch.int64, (B,), "supply", dev_check)
+        if alive is not None:
+            _need(alive, torch.uint8, (B, S, n), "alive", dev_check)
+        self.Mmax = max(1, int(supply.max().item())) if B else 1
+        d = _lib.ProblemDesc()
+        d.abi_version = _lib.GWTF_ABI_VERSION
+        d.num_instances, d.num_stages, d.clients_per_stage, d.max_cap = B, S, n, max_cap
+        d.cap, d.alive, d.src_cost, d.snk_cost = _ptr(cap), _ptr(alive), _ptr(src_cost), _ptr(snk_cost)
+        d.link_cost = _ptr(link_cost) if S > 1 else None
+        d.supply = _ptr(supply)
+        d.seed, d.inst_base, d.T0, d.alpha = seed, inst_base, T0, alpha
+        d.objective, d.steady_window, d.deny_after = objective, steady_window, deny_after
+        d.device = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        d.stream = self.stream.cuda_stream
+        d.flags = (_lib.GWTF_HOST_PTRS if host else 0) | (_lib.GWTF_FORCE_GLOBAL_TIER if force_global_tier else 0)
+        h = ctypes.c_void_p()
+        check("gwtf_flow_create", lib().gwtf_flow_create(ctypes.byref(d), ctypes.byref(h)))
+        self.h = h
+
+    # -- helpers
+    def _out(self, shape, dtype):
+        if self.host:
+            return torch.empty(shape, dtype=dtype, pin_memory=True)
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().gwtf_flow_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- API
+    def solve_batch(self, out: SolveResult | None = None) -> SolveResult:
+        B = self.B
+        if out is None:
+            out = SolveResult(self._out((B,), torch.int64), self._out((B,), torch.int64),
+                              self._out((B,), torch.int32), self._out((B,), torch.int32))
+        check("gwtf_flow_solve_batch", lib().gwtf_flow_solve_batch(
+            self.h, _ptr(out.flow_value), _ptr(out.total_cost), _ptr(out.augmentations), _ptr(out.status)))
+        return out
+
+    def decentralized_rounds(self, max_rounds: int, digests: bool = False, out: RoundsResult | None = None):
+        B = self.B
+        if out is None:
+            out = RoundsResult(self._out((B,), torch.int32), self._out((B,), torch.int64),
+                               self._out((B,), torch.int64), self._out((B,), torch.int32),
+                               self._out((B, max(max_rounds, 1)), torch.int64) if digests else None)
+        check("gwtf_flow_decentralized_rounds", lib().gwtf_flow_decentralized_rounds(
+            self.h, max_rounds, _ptr(out.rounds_run), _ptr(out.dec_flow), _ptr(out.dec_cost), _ptr(out.dangling),
+            _ptr(out.digests)))
+        return out
+
+    def apply_churn(self, alive_new=None, edge_updates=None):
+        k = 0 if edge_updates is None else int(edge_updates.shape[0])
+        check("gwtf_flow_apply_churn", lib().gwtf_flow_apply_churn(
+            self.h, _ptr(alive_new), _ptr(edge_updates) if k else None, k))
+
+    def get_assignment(self, dense_arcs: bool = True):
+        B, S, n = self.B, self.S, self.n
+        nf = self._out((B, S, n), torch.int32)
+        sf = self._out((B, n), torch.int32)
+        kf = self._out((B, n), torch.int32)
+        af = self._out((B, max(S - 1, 0), n, n), torch.int32) if dense_arcs else None
+        check("gwtf_flow_get_assignment", lib().gwtf_flow_get_assignment(
+            self.h, _ptr(nf), _ptr(sf), _ptr(kf), _ptr(af) if af is not None and af.numel() else None))
+        return nf, sf, kf, af
+
+    def export_round_state(self):
+        B, S, n, MC, M = self.B, self.S, self.n, self.max_cap, self.Mmax
+        st = dict(up=self._out((B, S, n, MC), torch.int32), down=self._out((B, S, n, MC), torch.int32),
+                  src_down=self._out((B, M), torch.int32), snk_up=self._out((B, M), torch.int32),
+                  kacc=self._out((B, S, n), torch.int32), deny=self._out((B, S, n), torch.int32),
+                  quiet=self._out((B,), torch.int32), round=self._out((B,), torch.int64))
+        check("gwtf_flow_export_round_state", lib().gwtf_flow_export_round_state(
+            self.h, *[_ptr(st[k]) for k in ("up", "down", "src_down", "snk_up", "kacc", "deny", "quiet", "round")]))
+        return st
+
+    def snapshot(self):
+        check("gwtf_flow_snapshot", lib().gwtf_flow_snapshot(self.h))
+
+    def restore(self):
+        check("gwtf_flow_restore", lib().gwtf_flow_restore(self.h))
+
+    def set_profiling(self, on: bool):
+        check("gwtf_flow_set_profiling", lib().gwtf_flow_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_times(self) -> dict:
+        cap = 16
+        names = (ctypes.c_char_p * cap)()
+        ms = (ctypes.c_float * cap)()
+        nl = (ctypes.c_int32 * cap)()
+        cnt = ctypes.c_int32()
+        check("gwtf_flow_kernel_times", lib().gwtf_flow_kernel_times(
+            self.h, names, ctypes.cast(ms, ctypes.c_void_p), ctypes.cast(nl, ctypes.c_void_p), cap,
+            ctypes.cast(ctypes.byref(cnt), ctypes.c_void_p)))
+        return {names[i].decode(): (ms[i], nl[i]) for i in range(min(cnt.value, cap))}
