@@ -1,0 +1,140 @@
+"""CPU-side checks of the boundary and of the host logic: the C-ABI library loads and exports every
+symbol include/gwtf.h declares (no compute calls without a GPU); the harness victim rule equals the
+oracle's; the generator is deterministic; instance sharding over 2 gloo ranks gathers the same
+results as one process."""
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def libgwtf():
+    subprocess.run(["make", "-s", "-C", ROOT, "paper_2509_21221_b200/libgwtf.so"], check=True)
+    return ctypes.CDLL(os.path.join(ROOT, "paper_2509_21221_b200", "libgwtf.so"))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "gwtf.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:gwtf_status|const char\*|int32_t)\s+(gwtf_\w+)\s*\(", src, re.M)))
+
+
+def test_header_symbols_exported(libgwtf):
+    syms = declared_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(libgwtf, s), s
+    nm = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2509_21221_b200", "libgwtf.so")],
+                        capture_output=True, text=True).stdout
+    exported = {l.split()[-1] for l in nm.splitlines() if " T " in l}
+    assert set(syms) <= exported
+
+
+def test_binding_declares_every_symbol():
+    from paper_2509_21221_b200 import _lib
+    assert set(declared_symbols()) == set(_lib.EXPORTS)
+
+
+def test_abi_version_and_null_handles(libgwtf):
+    libgwtf.gwtf_abi_version.restype = ctypes.c_int32
+    assert libgwtf.gwtf_abi_version() == 1
+    libgwtf.gwtf_flow_create.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    assert libgwtf.gwtf_flow_create(None, None) == 1      # GWTF_E_INVALID, no device touched
+    libgwtf.gwtf_flow_destroy.argtypes = [ctypes.c_void_p]
+    assert libgwtf.gwtf_flow_destroy(None) == 0           # NULL is a no-op
+    libgwtf.gwtf_flow_solve_batch.argtypes = [ctypes.c_void_p] * 5
+    assert libgwtf.gwtf_flow_solve_batch(None, None, None, None, None) == 1
+    libgwtf.gwtf_last_error.restype = ctypes.c_char_p
+    assert b"NULL" in libgwtf.gwtf_last_error()
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2509_21221_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f
+
+
+def test_generator_deterministic_and_counter_based():
+    cfg = gen.CONFIGS["gpt"]
+    a = gen.generate(cfg, 0, 10)
+    b = gen.generate(cfg, 0, 10)
+    c = gen.generate(cfg, 5, 3)  # instances 5..7 regenerate independently
+    for f in ("cap", "alive", "comp", "loc", "dloc", "lat", "bw"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))
+        assert np.array_equal(getattr(a, f)[5:8], getattr(c, f))
+    t = gen.generate(gen.CONFIGS["tiny"], 0, 2000)
+    assert t.cap.min() == 1 and t.cap.max() == 3 and t.src.min() == 1 and t.src.max() == 20
+    g = gen.generate(gen.CONFIGS["churn"], 0, 50)
+    assert abs(g.alive.mean() - 0.9) < 0.02
+
+
+def test_victim_rule_python_equals_oracle():
+    cfg = gen.CONFIGS["llama"].with_(S=6, n=8, M=40)
+    bt = gen.generate(cfg, 0, 8)
+    src, snk, link = oracle.eq1_batch(bt)
+    draws = gen.victim_draws(cfg, 0, 8)
+    for b in range(8):
+        I = oracle.instance_from_batch(bt, b, link[b], src[b], snk[b])
+        R = oracle.Rounds(I, seed=1, inst_id=b)
+        R.run(200)
+        st = R.export()
+        v = R.llama_victim(int(draws[b, 0]), int(draws[b, 1]))
+        an = gen.llama_victims(st["up"][None], st["down"][None], bt.alive[b][None], draws[b:b + 1])
+        want = bt.alive[b].copy().reshape(-1)
+        if v >= 0:
+            want[v] = 0
+        assert np.array_equal(an[0].reshape(-1), want)
+
+
+def test_shard_ranges():
+    from paper_2509_21221_b200.dist import shard_range
+    for total in (1, 7, 16384):
+        for world in (1, 2, 3, 8):
+            rs = [shard_range(total, world, r) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == total
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+
+
+_GLOO_WORKER = r"""
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, {root!r})
+from paper_2509_21221_b200.dist import gather_results, totals, shard_range
+from types import SimpleNamespace as NS
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+lo, hi = shard_range(10, w, r)
+ids = torch.arange(lo, hi)
+sol = NS(flow_value=ids * 2, total_cost=ids * 3, augmentations=ids.int(), status=torch.zeros_like(ids).int())
+rr = NS(rounds_run=ids.int() + 1, dec_flow=ids, dec_cost=ids * 5, dangling=torch.zeros_like(ids).int())
+g = gather_results(sol, rr, w)
+t = totals(g)
+if r == 0:
+    assert g.shape == (10, 8), g.shape
+    assert torch.equal(g[:, 0], torch.arange(10) * 2) and torch.equal(g[:, 6], torch.arange(10) * 5)
+    assert t["total_cost"] == 3 * 45
+    print("GLOO_OK")
+dist.destroy_process_group()
+"""
+
+
+def test_gather_over_two_gloo_ranks(tmp_path):
+    script = tmp_path / "w.py"
+    script.write_text(_GLOO_WORKER.format(root=ROOT))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29617")
+    procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r), WORLD_SIZE="2"),
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=120) for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    assert "GLOO_OK" in outs[0][0]
