@@ -280,15 +280,6 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   AL(P.deny, B * Sn, true);
   AL(P.quiet, B, true);
   AL(P.round, B, true);
-  AL(P.scost, nslot, false);
-  AL(P.adv_cost, B * Sn, false);
-  AL(P.adv_slot, B * Sn, false);
-  AL(P.req_slot, B * (Sn + 1), false);
-  AL(P.req_target, B * (Sn + 1), false);
-  AL(P.prop, B * Sn * 6, false);
-  AL(P.prop_key, B * Sn, false);
-  AL(P.prop_touch, B * Sn * 4, false);
-  AL(P.res, B * (Sn * std::max<int64_t>(MC, 1) + 2 * P.Mmax), false);
   AL(P.counters, 8, false);
   AL(h->bad_flag, 4, false);
   uint32_t* thr_d = nullptr;
@@ -312,6 +303,15 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     uint8_t* ws = nullptr;
     if ((s = alloc(h, &ws, (size_t)P.ws_teams * P.ws_per_team)) != GWTF_OK) return bail(s);
     P.ws = ws;
+  }
+
+  // global scratch of the rounds kernel when an instance does not fit in shared memory
+  if (!rounds_use_smem(P)) {
+    const int tpi = rounds_tpi(P);
+    P.ws_rounds_teams = (int32_t)std::min<int64_t>((int64_t)h->num_sms * std::max(1, 2048 / tpi), B);
+    uint8_t* wr = nullptr;
+    if ((s = alloc(h, &wr, (size_t)P.ws_rounds_teams * rounds_ws_bytes(P, false))) != GWTF_OK) return bail(s);
+    P.ws_rounds = wr;
   }
 
   // inputs

@@ -36,16 +36,9 @@ struct Problem {
   int32_t* deny;               // [B][S*n]
   int32_t* quiet;              // [B]
   int64_t* round;              // [B]
-  // round scratch (global; L1/L2 resident per team)
-  int64_t* scost;              // [B][S*n*MC] cost to sink per slot
-  int64_t* adv_cost;           // [B][S*n]
-  int32_t* adv_slot;           // [B][S*n]
-  int32_t* req_slot;           // [B][S*n + 1]  requester slot (index S*n = data node)
-  int32_t* req_target;         // [B][S*n + 1]  target gid, -1 = D-sink, -2 none
-  int32_t* prop;               // [B][S*n][6]   proposal: kind, x, y, z, t0..t3 packed below
-  uint64_t* prop_key;          // [B][S*n]
-  int64_t* prop_touch;         // [B][S*n][4]   reservation ids touched
-  uint64_t* res;               // [B][S*n*MC + 2*Mmax] reservation minima
+  // per-team scratch of the rounds kernel when the instance does not fit in shared memory
+  uint8_t* ws_rounds;
+  int32_t ws_rounds_teams;
   // parameters of the rounds
   uint64_t seed;
   int64_t inst_base;
@@ -72,6 +65,9 @@ struct RoundsOut {
 // launchers (return cudaGetLastError())
 size_t ssp_smem_bytes(const Problem& P);
 size_t ssp_global_ws_bytes(const Problem& P);
+size_t rounds_ws_bytes(const Problem& P, bool smem);
+int rounds_tpi(const Problem& P);
+bool rounds_use_smem(const Problem& P);
 cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, bool force_global);
 cudaError_t launch_rounds(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms);
 cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st);

@@ -2,15 +2,20 @@
 //
 // PAPER.md:241-263 (Request Flow / Request Change / Request Redirect, simulated annealing,
 // steady state) and :269 (DENY).  One team of TPI threads per instance, persistent over an
-// atomic instance queue; every phase is relay-parallel and phases are separated by team
-// barriers, so each phase reads the snapshot the definition names:
-//   R0a self-pairing (round-start costs) | R0 cost-to-sink back to front + advertisements |
-//   R1 one Request Flow per node | R2 grants in requester order | R3 commit |
-//   R4 Change / Redirect / DENY proposals on the post-R3 state (counter RNG, integer
-//   annealing thresholds) | R5 deterministic reservations (64-bit atomicMin, order free) |
-//   R6 commit winners | R7 quiet counter, optional state digest.
-// Round state lives in global memory (L1/L2 resident for the team); reservation minima are
-// read with ld.global.cg because they are produced by L2 atomics.
+// atomic instance queue; every phase is relay-parallel (thread t owns relays t, t+TPI, ...)
+// and phases are separated by team barriers, so each phase reads the snapshot the
+// definition names:
+//   summaries | R0a self-pairing (round-start costs) | R0 cost-to-sink back to front +
+//   advertisements | R1 one Request Flow per node | R2 grants in requester order | R3 commit |
+//   summaries | R4 Change / Redirect / DENY proposals on the post-R3 state (counter RNG,
+//   integer annealing thresholds) + R5 deterministic reservations (64-bit atomicMin, order
+//   free) | R6 commit winners | R7 quiet counter, optional state digest.
+// Index arithmetic uses multiply-shift division (no runtime integer division on the hot
+// path).  The per-instance state either lives in global memory (L1/L2 resident; reservation
+// minima read with ld.global.cg since they are produced by L2 atomics) or is staged in
+// shared memory (tiles by TMA bulk copy) when it fits.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gwtf {
@@ -20,6 +25,26 @@ namespace {
 constexpr int64_t INF = INT64_MAX;
 constexpr uint64_t RES_NONE = ~0ull;
 enum { K_NONE = 0, K_CHANGE = 1, K_REDIRECT = 2, K_DENY = 3 };
+enum { ST_FREE = 0, ST_OUT = 1, ST_IN = 2, ST_PAIRED = 3 };
+
+int getenv_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// q = x / d for 0 <= x < 2^31 by multiply-shift (Granlund-Montgomery)
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __host__ __device__ void init(uint32_t div) {
+    d = div;
+    shr = 0;
+    while ((1u << shr) < div) ++shr;
+    mul = div == 1 ? 0u : (uint32_t)(((1ull << 32) * ((1ull << shr) - div)) / div + 1);
+  }
+  __device__ __forceinline__ int div(int x) const {
+    return d == 1 ? x : (int)((__umulhi((uint32_t)x, mul) + (uint32_t)x) >> shr);
+  }
+};
 
 __device__ __forceinline__ uint64_t mix(uint64_t z) {  // splitmix64 finalizer
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -30,80 +55,85 @@ __device__ __forceinline__ uint32_t pick(uint64_t x, uint32_t m) {
   return (uint32_t)(((x >> 32) * (uint64_t)m) >> 32);
 }
 __device__ __forceinline__ int64_t sadd(int64_t a, int64_t b) { return (a == INF || b == INF) ? INF : a + b; }
+__device__ __forceinline__ int64_t cst(int32_t c) { return c == kAbsent ? INF : (int64_t)c; }
+
+// per-relay slot summary: first IN slot, first FREE slot (63 = none), #PAIRED, has OUT
+struct Summ {
+  uint32_t w;
+  __device__ int first_in() const { return (int)(w & 63u); }
+  __device__ int first_free() const { return (int)((w >> 6) & 63u); }
+  __device__ int npaired() const { return (int)((w >> 12) & 63u); }
+  __device__ bool has_out() const { return (w >> 18) & 1u; }
+  __device__ bool has_in() const { return first_in() != 63; }
+};
 
 struct Inst {
   const Problem* P;
-  int S, n, ld, MC, Sn;
-  int64_t M;
-  int inst;
+  int S, n, ld, MC, Sn, M, inst;
+  FastDiv dn, dmc;
   int32_t *up, *down, *src_down, *snk_up, *kacc, *deny;
   int64_t *scost, *adv_cost;
-  int32_t *adv_slot, *req_slot, *req_target, *prop;
+  int32_t *req_slot, *req_target, *grant, *prop, *ptouch, *capv;
+  uint32_t* summ;
   uint64_t *pkey, *res;
-  int64_t* ptouch;
-  const int32_t *tile, *src, *snk, *cap;
+  const int32_t *tile, *src, *snk;
   const uint8_t* alive;
+  uint64_t hpre;  // mix(mix(mix(seed) ^ inst) ^ round), uniform over the round
 
-  __device__ int capE(int v) const { return alive[v] ? cap[v] : 0; }
   __device__ int st(int p) const { return (up[p] != kNone ? 2 : 0) | (down[p] != kNone ? 1 : 0); }
+  __device__ int relay(int32_t p) const { return dmc.div(p); }           // slot index -> gid
+  __device__ int64_t c_link(int s, int u, int v) const { return cst(tile[((size_t)s * n + v) * ld + u]); }
   // d(a, b) between nodes; -1 = data node D.  Missing / absent = INF.
   __device__ int64_t d(int a, int b) const {
-    int32_t c = kAbsent;
-    if (a < 0) {
-      if (b >= 0 && b < n) c = src[b];
-    } else if (b < 0) {
-      if (a / n == S - 1) c = snk[a % n];
-    } else {
-      const int sa = a / n;
-      if (b / n == sa + 1) c = tile[((size_t)sa * n + (b % n)) * ld + (a % n)];
-    }
-    return c == kAbsent ? INF : (int64_t)c;
+    if (a < 0) return (b >= 0 && b < n) ? cst(src[b]) : INF;
+    const int sa = dn.div(a);
+    if (b < 0) return sa == S - 1 ? cst(snk[a - sa * n]) : INF;
+    const int sb = dn.div(b);
+    return sb == sa + 1 ? c_link(sa, a - sa * n, b - sb * n) : INF;
   }
-  __device__ int64_t res_up(int32_t p) const { return p >= 0 ? p : (int64_t)Sn * MC + (-2 - p); }
-  __device__ int64_t res_dn(int32_t p) const { return p >= 0 ? p : (int64_t)Sn * MC + P->Mmax + (-2 - p); }
+  __device__ int32_t res_up(int32_t p) const { return p >= 0 ? p : Sn * MC + (-2 - p); }
+  __device__ int32_t res_dn(int32_t p) const { return p >= 0 ? p : Sn * MC + (int32_t)P->Mmax + (-2 - p); }
   __device__ void set_up_of(int32_t p, int32_t v) { if (p >= 0) up[p] = v; else snk_up[-2 - p] = v; }
   __device__ void set_down_of(int32_t p, int32_t v) { if (p >= 0) down[p] = v; else src_down[-2 - p] = v; }
-  __device__ uint64_t h(uint64_t round, int gid, int stream) const {
-    return mix(mix(mix(mix(P->seed) ^ (uint64_t)(P->inst_base + inst)) ^ round) ^ ((uint64_t)gid * 4 + stream));
+  __device__ void set_round(uint64_t round) {
+    hpre = mix(mix(mix(P->seed) ^ (uint64_t)(P->inst_base + inst)) ^ round);
   }
-};
+  __device__ uint64_t h(int gid, int stream) const { return mix(hpre ^ ((uint64_t)gid * 4 + stream)); }
 
-struct SlotScan {
-  int first_in, first_free, npaired;
-  bool has_out;
+  __device__ uint32_t summarize(int v) const {
+    uint32_t fi = 63, ff = 63, np = 0, ho = 0;
+    const int c = capv[v], base = v * MC;
+    for (int j = 0; j < c; ++j) {
+      const int t = st(base + j);
+      if (t == ST_IN && fi == 63) fi = j;
+      if (t == ST_FREE && ff == 63) ff = j;
+      np += t == ST_PAIRED;
+      ho |= t == ST_OUT;
+    }
+    return fi | (ff << 6) | (np << 12) | (ho << 18);
+  }
+  __device__ int nth_paired(int v, int q) const {
+    const int c = capv[v], base = v * MC;
+    for (int j = 0; j < c; ++j)
+      if (st(base + j) == ST_PAIRED) { if (q == 0) return base + j; --q; }
+    return -1;
+  }
 };
-__device__ __forceinline__ SlotScan scan_slots(const Inst& I, int v) {
-  SlotScan r{-1, -1, 0, false};
-  const int c = I.capE(v);
-  for (int j = 0; j < c; ++j) {
-    const int p = v * I.MC + j, t = I.st(p);
-    if (t == 2 && r.first_in < 0) r.first_in = p;
-    if (t == 0 && r.first_free < 0) r.first_free = p;
-    if (t == 1) r.has_out = true;
-    if (t == 3) r.npaired++;
-  }
-  return r;
-}
-__device__ __forceinline__ int nth_paired(const Inst& I, int v, int q) {
-  const int c = I.capE(v);
-  for (int j = 0; j < c; ++j) {
-    const int p = v * I.MC + j;
-    if (I.st(p) == 3) { if (q == 0) return p; --q; }
-  }
-  return -1;
-}
 
 template <int TPI>
 __device__ void compute_costs(const Team<TPI>& T, const Inst& I) {
+  const int per = I.n * I.MC;
   for (int s = I.S - 1; s >= 0; --s) {
-    for (int t = T.tid; t < I.n * I.MC; t += TPI) {
-      const int v = s * I.n + t / I.MC, j = t % I.MC, p = v * I.MC + j;
+    for (int t = T.tid; t < per; t += TPI) {
+      const int i = I.dmc.div(t), j = t - i * I.MC, v = s * I.n + i, p = v * I.MC + j;
       int64_t c = INF;
-      if (j < I.capE(v)) {
+      if (j < I.capv[v]) {
         const int32_t dn = I.down[p];
-        if (dn == kNone) c = INF;
-        else if (dn <= -2) c = I.d(v, -1);
-        else c = sadd(I.d(v, dn / I.MC), I.scost[dn]);
+        if (dn <= -2) c = cst(I.snk[i]);
+        else if (dn >= 0) {
+          const int w = I.relay(dn);
+          c = sadd(I.c_link(s, i, w - (s + 1) * I.n), I.scost[dn]);
+        }
       }
       I.scost[p] = c;
     }
@@ -113,15 +143,72 @@ __device__ void compute_costs(const Team<TPI>& T, const Inst& I) {
 
 __device__ uint64_t digest_elem(uint64_t pos, uint64_t val) { return mix(mix(pos) ^ val); }
 
-template <int TPI>
-__global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const RoundsOut o) {
+// ---- per-team workspace layout ---------------------------------------------------------
+__host__ __device__ inline size_t al16r(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ inline bool rounds_tile_in_smem(const Problem& P) {
+  return (size_t)(P.S > 1 ? P.S - 1 : 0) * P.n * P.ld * 4 <= 16384;
+}
+struct RoundsLayout {
+  size_t res, scost, adv_cost, pkey, up, down, src_down, snk_up, kacc, deny, req_slot, req_target, grant, prop,
+      ptouch, capv, summ, tile, total;
+};
+// smem: everything of one instance; otherwise only the per-instance scratch (the state
+// arrays then live in the handle's global buffers)
+__host__ __device__ inline RoundsLayout rounds_layout(const Problem& P, bool smem) {
+  RoundsLayout L;
+  size_t o = 0;
+  const size_t Sn = (size_t)P.S * P.n, ns = Sn * P.MC, M = (size_t)P.Mmax;
+  L.res = o; o += al16r((ns + 2 * M) * 8);
+  L.scost = o; o += al16r(ns * 8);
+  L.adv_cost = o; o += al16r(Sn * 8);
+  L.pkey = o; o += al16r(Sn * 8);
+  L.up = o; if (smem) o += al16r(ns * 4);
+  L.down = o; if (smem) o += al16r(ns * 4);
+  L.src_down = o; if (smem) o += al16r(M * 4);
+  L.snk_up = o; if (smem) o += al16r(M * 4);
+  L.kacc = o; if (smem) o += al16r(Sn * 4);
+  L.deny = o; if (smem) o += al16r(Sn * 4);
+  L.req_slot = o; o += al16r((Sn + 1) * 4);
+  L.req_target = o; o += al16r((Sn + 1) * 4);
+  L.grant = o; o += al16r((Sn + 1) * 4);
+  L.prop = o; o += al16r(Sn * 4 * 4);
+  L.ptouch = o; o += al16r(Sn * 4 * 4);
+  L.capv = o; o += al16r(Sn * 4);
+  L.summ = o; o += al16r(Sn * 4);
+  L.tile = o; if (smem && rounds_tile_in_smem(P)) o += al16r((size_t)(P.S > 1 ? P.S - 1 : 0) * P.n * P.ld * 4);
+  L.total = o + 16;  // + mbarrier
+  return L;
+}
+
+template <bool kSmem>
+__device__ __forceinline__ uint64_t ld_res(const uint64_t* p) {
+  if constexpr (kSmem) return *(volatile const uint64_t*)p;
+  else return __ldcg(p);
+}
+template <bool kSmem>
+__device__ __forceinline__ void st_res(uint64_t* p, uint64_t v) {
+  if constexpr (kSmem) *p = v;
+  else __stcg(p, v);
+}
+
+template <int TPI, bool kSmem>
+__global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const RoundsOut o, const size_t ws_bytes) {
+  extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ uint64_t sh_u64[8][2];
   __shared__ int sh_i32[8][4];
   __shared__ int sh_inst[8];
+  __shared__ int tma_init[8];
+  __shared__ uint32_t tma_phase_of[8];
+  if (threadIdx.x < 8) { tma_init[threadIdx.x] = 0; tma_phase_of[threadIdx.x] = 0; }
+  __syncthreads();
   const Team<TPI> T{(int)(threadIdx.x % TPI), (int)(threadIdx.x / TPI)};
   const int lane = threadIdx.x & 31;
   const int S = P.S, n = P.n, MC = P.MC, Sn = S * n;
   const int nres = Sn * MC + 2 * (int)P.Mmax;
+  const int teams_per_cta = blockDim.x / TPI;
+  const RoundsLayout Lr = rounds_layout(P, kSmem);
+  uint8_t* base = kSmem ? dsm + (size_t)T.id * ws_bytes
+                        : P.ws_rounds + (size_t)(blockIdx.x * teams_per_cta + T.id) * ws_bytes;
 
   for (;;) {
     if (T.tid == 0) sh_inst[T.id] = atomicAdd(&P.counters[1], 1);
@@ -130,54 +217,98 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
     if (b >= P.B) break;
     Inst I;
     I.P = &P; I.S = S; I.n = n; I.ld = P.ld; I.MC = MC; I.Sn = Sn; I.inst = b;
-    I.M = P.supply[b];
+    I.dn.init((uint32_t)n);
+    I.dmc.init((uint32_t)(MC > 0 ? MC : 1));
+    I.M = (int)P.supply[b];
     I.up = P.up + (size_t)b * Sn * MC;
     I.down = P.down + (size_t)b * Sn * MC;
     I.src_down = P.src_down + (size_t)b * P.Mmax;
     I.snk_up = P.snk_up + (size_t)b * P.Mmax;
     I.kacc = P.kacc + (size_t)b * Sn;
     I.deny = P.deny + (size_t)b * Sn;
-    I.scost = P.scost + (size_t)b * Sn * MC;
-    I.adv_cost = P.adv_cost + (size_t)b * Sn;
-    I.adv_slot = P.adv_slot + (size_t)b * Sn;
-    I.req_slot = P.req_slot + (size_t)b * (Sn + 1);
-    I.req_target = P.req_target + (size_t)b * (Sn + 1);
-    I.prop = P.prop + (size_t)b * Sn * 6;
-    I.pkey = P.prop_key + (size_t)b * Sn;
-    I.ptouch = P.prop_touch + (size_t)b * Sn * 4;
-    I.res = P.res + (size_t)b * nres;
     I.tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
     I.src = P.src + (size_t)b * n;
     I.snk = P.snk + (size_t)b * n;
-    I.cap = P.cap + (size_t)b * Sn;
     I.alive = P.alive + (size_t)b * Sn;
-    const int M = (int)I.M;
+    I.res = (uint64_t*)(base + Lr.res);
+    I.scost = (int64_t*)(base + Lr.scost);
+    I.adv_cost = (int64_t*)(base + Lr.adv_cost);
+    I.pkey = (uint64_t*)(base + Lr.pkey);
+    I.req_slot = (int32_t*)(base + Lr.req_slot);
+    I.req_target = (int32_t*)(base + Lr.req_target);
+    I.grant = (int32_t*)(base + Lr.grant);
+    I.prop = (int32_t*)(base + Lr.prop);
+    I.ptouch = (int32_t*)(base + Lr.ptouch);
+    I.capv = (int32_t*)(base + Lr.capv);
+    I.summ = (uint32_t*)(base + Lr.summ);
+    const int M = I.M;
+    const int32_t* cap_g = P.cap + (size_t)b * Sn;
+    for (int k = T.tid; k < Sn; k += TPI) I.capv[k] = I.alive[k] ? cap_g[k] : 0;
+    int32_t* g_up = I.up;
+    int32_t* g_down = I.down;
+    int32_t* g_src_down = I.src_down;
+    int32_t* g_snk_up = I.snk_up;
+    int32_t* g_kacc = I.kacc;
+    int32_t* g_deny = I.deny;
+    if constexpr (kSmem) {  // stage the round state (and small tiles, by TMA) in shared memory
+      uint64_t* mbar = (uint64_t*)(base + Lr.total - 16);
+      I.up = (int32_t*)(base + Lr.up);
+      I.down = (int32_t*)(base + Lr.down);
+      I.src_down = (int32_t*)(base + Lr.src_down);
+      I.snk_up = (int32_t*)(base + Lr.snk_up);
+      I.kacc = (int32_t*)(base + Lr.kacc);
+      I.deny = (int32_t*)(base + Lr.deny);
+      const int32_t* gtile = I.tile;
+      const bool tile_smem = rounds_tile_in_smem(P);
+      if (tile_smem) I.tile = (const int32_t*)(base + Lr.tile);
+      const uint32_t tbytes = tile_smem ? (uint32_t)((size_t)(S - 1) * n * P.ld * 4) : 0u;
+      if (T.tid == 0 && tbytes) {
+        if (tma_init[T.id] == 0) { mbar_init(mbar, 1); fence_barrier_init(); tma_init[T.id] = 1; }
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(mbar, tbytes);
+        for (uint32_t off = 0; off < tbytes; off += 32768u)
+          bulk_g2s(base + Lr.tile + off, (const uint8_t*)gtile + off, tbytes - off < 32768u ? tbytes - off : 32768u,
+                   mbar);
+      }
+      for (int k = T.tid; k < Sn * MC; k += TPI) { I.up[k] = g_up[k]; I.down[k] = g_down[k]; }
+      for (int k = T.tid; k < M; k += TPI) { I.src_down[k] = g_src_down[k]; I.snk_up[k] = g_snk_up[k]; }
+      for (int k = T.tid; k < Sn; k += TPI) { I.kacc[k] = g_kacc[k]; I.deny[k] = g_deny[k]; }
+      T.sync();
+      if (tbytes) {  // barrier init visible; every thread waits on the transaction barrier
+        const uint32_t ph = tma_phase_of[T.id];
+        mbar_wait(mbar, ph);
+        T.sync();
+        if (T.tid == 0) tma_phase_of[T.id] = ph ^ 1u;
+      }
+    }
 
-    for (int k = T.tid; k < nres; k += TPI) __stcg(&I.res[k], RES_NONE);
+    for (int k = T.tid; k < nres; k += TPI) st_res<kSmem>(&I.res[k], RES_NONE);
     int quiet = 0;  // quiet = 0 at the start of every call (DESIGN.md 2.3 R7)
     uint64_t round = (uint64_t)P.round[b];
     int r = 0;
     T.sync();
     while (r < o.max_rounds) {
       int changed = 0;
-      // ---------- R0a self-pairing (costs of the round-start state) ----------
+      I.set_round(round);
+      // ---------- slot summaries; R0a candidates (IN and OUT at one relay) ----------
       int cand = 0;
       for (int v = T.tid; v < Sn; v += TPI) {
-        if (!I.alive[v]) continue;
-        const SlotScan sc = scan_slots(I, v);
-        cand |= (sc.first_in >= 0 && sc.has_out);
+        const uint32_t w = I.summarize(v);
+        I.summ[v] = w;
+        cand |= (w & 63u) != 63u && ((w >> 18) & 1u);
       }
       if (T.sync_or(cand)) {
+        // ---------- R0a self-pairing, costs of the round-start state ----------
         compute_costs(T, I);
         for (int v = T.tid; v < Sn; v += TPI) {
-          if (!I.alive[v]) continue;
-          int x = -1, oo = -1;
-          for (int j = 0; j < I.capE(v); ++j) {
-            const int p = v * MC + j, t = I.st(p);
-            if (t == 2 && x < 0) x = p;
-            if (t == 1 && (oo < 0 || I.scost[p] < I.scost[oo])) oo = p;
+          const Summ sm{I.summ[v]};
+          if (!sm.has_in() || !sm.has_out()) continue;
+          const int x = v * MC + sm.first_in();
+          int oo = -1;
+          for (int j = 0; j < I.capv[v]; ++j) {
+            const int p = v * MC + j;
+            if (I.st(p) == ST_OUT && (oo < 0 || I.scost[p] < I.scost[oo])) oo = p;
           }
-          if (x < 0 || oo < 0) continue;
           const int32_t cdn = I.down[oo];
           I.down[x] = cdn;
           I.set_up_of(cdn, x);
@@ -185,22 +316,21 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
           changed = 1;
         }
         T.sync();
+        for (int v = T.tid; v < Sn; v += TPI) I.summ[v] = I.summarize(v);
+        T.sync();
       }
       // ---------- R0 cost to sink + advertisements ----------
       compute_costs(T, I);
       for (int v = T.tid; v < Sn; v += TPI) {
         int64_t bc = INF;
-        int bj = -1;
-        if (I.alive[v]) {
-          for (int j = 0; j < I.capE(v); ++j) {
+        if ((I.summ[v] >> 18) & 1u) {  // has an OUT slot
+          for (int j = 0; j < I.capv[v]; ++j) {
             const int p = v * MC + j;
-            if (I.st(p) == 1 && (bj < 0 || I.scost[p] < bc)) { bc = I.scost[p]; bj = j; }
+            if (I.st(p) == ST_OUT && I.scost[p] < bc) bc = I.scost[p];
           }
         }
         I.adv_cost[v] = bc;
-        I.adv_slot[v] = bj;
       }
-      // data node: lowest unpaired SRC slot, any free SNK slot
       if (T.tid == 0) { sh_i32[T.id][0] = INT_MAX; sh_i32[T.id][1] = 0; }
       T.sync();
       {
@@ -218,33 +348,35 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       // ---------- R1 requests (one per node) ----------
       for (int rr = T.tid; rr <= Sn; rr += TPI) {
         int32_t rs = kNone, tg = -2;
-        if (rr == Sn) {  // the data node
+        if (rr == Sn) {  // the data node requests for its lowest unpaired SRC slot
           if (d_rslot != INT_MAX) {
             int64_t bc = INF;
             for (int j = 0; j < n; ++j) {
-              const int64_t dj = I.d(-1, j);
-              if (!I.alive[j] || dj == INF || I.adv_cost[j] == INF) continue;
-              if (dj + I.adv_cost[j] < bc) { bc = dj + I.adv_cost[j]; tg = j; }
+              const int64_t dj = cst(I.src[j]), aj = I.adv_cost[j];
+              if (dj == INF || aj == INF || !I.alive[j]) continue;
+              if (dj + aj < bc) { bc = dj + aj; tg = j; }
             }
             if (tg != -2) rs = -2 - d_rslot;
           }
         } else if (I.alive[rr]) {
-          const SlotScan sc = scan_slots(I, rr);
+          const Summ sm{I.summ[rr]};
           int32_t x = kNone;
-          if (sc.first_in >= 0) x = sc.first_in;
-          else if (!sc.has_out && sc.first_free >= 0) x = sc.first_free;
+          if (sm.has_in()) x = rr * MC + sm.first_in();                                   // (a)
+          else if (!sm.has_out() && sm.first_free() != 63) x = rr * MC + sm.first_free();  // (b)
           if (x != kNone) {
-            const int s = rr / n;
+            const int s = I.dn.div(rr), i = rr - s * n;
             if (s == S - 1) {
-              if (I.d(rr, -1) != INF && dsink_free) tg = -1;
+              if (I.snk[i] != kAbsent && dsink_free) tg = -1;
             } else {
               int64_t bc = INF;
+              const int32_t* col = I.tile + (size_t)s * n * I.ld + i;  // C[s][v][i], v = 0..n-1
+              const int64_t* av = I.adv_cost + (s + 1) * n;
               for (int jj = 0; jj < n; ++jj) {
-                const int j = (s + 1) * n + jj;
-                if (!I.alive[j] || I.adv_cost[j] == INF) continue;
-                const int64_t dj = I.d(rr, j);
-                if (dj == INF) continue;
-                if (dj + I.adv_cost[j] < bc) { bc = dj + I.adv_cost[j]; tg = j; }
+                const int64_t aj = av[jj];
+                if (aj == INF) continue;  // dead relays advertise INF
+                const int32_t c = col[(size_t)jj * I.ld];
+                if (c == kAbsent) continue;
+                if (c + aj < bc) { bc = c + aj; tg = (s + 1) * n + jj; }
               }
             }
             if (tg != -2) rs = x;
@@ -255,7 +387,6 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       }
       T.sync();
       // ---------- R2 grants: rank among same-target requesters in ascending gid ----------
-      // (the grant is parked in prop[rr*6+5]; the data node's in sh_i32[.][2])
       for (int rr = T.tid; rr <= Sn; rr += TPI) {
         const int tg = I.req_target[rr];
         int32_t grant = kNone;
@@ -263,13 +394,13 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
           int rank = 0;
           if (rr != Sn) {
             if (I.req_target[Sn] == tg) ++rank;  // D orders before all relays
-            const int s0 = (rr / n) * n;
+            const int s0 = I.dn.div(rr) * n;
             for (int q = s0; q < rr; ++q) rank += I.req_target[q] == tg;
           }
           const int64_t ac = I.adv_cost[tg];
-          for (int j = 0; j < I.capE(tg); ++j) {
+          for (int j = 0; j < I.capv[tg]; ++j) {
             const int p = tg * MC + j;
-            if (I.st(p) == 1 && I.scost[p] == ac) { if (rank == 0) { grant = p; break; } --rank; }
+            if (I.st(p) == ST_OUT && I.scost[p] == ac) { if (rank == 0) { grant = p; break; } --rank; }
           }
         } else if (tg == -1) {
           int rank = 0;
@@ -277,13 +408,12 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
           for (int k = 0; k < M; ++k)
             if (I.snk_up[k] == kNone) { if (rank == 0) { grant = -2 - k; break; } --rank; }
         }
-        if (rr == Sn) sh_i32[T.id][2] = grant;
-        else I.prop[rr * 6 + 5] = grant;
+        I.grant[rr] = grant;
       }
       T.sync();
       // ---------- R3 commit grants ----------
       for (int rr = T.tid; rr <= Sn; rr += TPI) {
-        const int32_t grant = rr == Sn ? sh_i32[T.id][2] : I.prop[rr * 6 + 5];
+        const int32_t grant = I.grant[rr];
         if (grant == kNone) continue;
         const int32_t rs = I.req_slot[rr];
         if (rr == Sn) I.src_down[-2 - rs] = grant;
@@ -292,48 +422,52 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
         changed = 1;
       }
       T.sync();
-      // ---------- R4 proposals by idle relays (post-R3 state) ----------
+      for (int v = T.tid; v < Sn; v += TPI) I.summ[v] = I.summarize(v);
+      T.sync();
+      // ---------- R4 proposals by idle relays (post-R3 state) + R5 reservations ----------
       for (int p = T.tid; p < Sn; p += TPI) {
         int kind = K_NONE;
         int32_t x = kNone, y = kNone, z = kNone;
-        int64_t t0 = -1, t1 = -1, t2 = -1, t3 = -1;
+        int32_t t0 = -1, t1 = -1, t2 = -1, t3 = -1;
         uint64_t key = RES_NONE;
         if (I.alive[p] && I.req_target[p] == -2) {
-          const SlotScan sc = scan_slots(I, p);
-          const int s = p / n, i = p % n;
-          if (sc.first_in >= 0) {
+          const Summ sm{I.summ[p]};
+          const int s = I.dn.div(p), i = p - s * n;
+          if (sm.has_in()) {  // DENY after deny_after idle rounds holding unpaired inflow
             const int dw = I.deny[p] + 1;
             I.deny[p] = dw;
             if (dw >= P.deny_after) {
               kind = K_DENY;
-              x = sc.first_in;
+              x = p * MC + sm.first_in();
               t0 = x;
               t1 = I.res_up(I.up[x]);
               key = (uint64_t)p;  // delta = -inf
             }
           } else if (n >= 2) {
-            uint32_t qi = pick(I.h(round, p, 0), (uint32_t)(n - 1));
+            uint32_t qi = pick(I.h(p, 0), (uint32_t)(n - 1));
             if ((int)qi >= i) qi += 1;
             const int q = s * n + (int)qi;
-            const int nq = I.alive[q] ? scan_slots(I, q).npaired : 0;
+            const int nq = I.alive[q] ? Summ{I.summ[q]}.npaired() : 0;
             if (nq > 0) {
               int64_t delta = 0;
               bool ok = false;
-              if (sc.first_free >= 0 && !sc.has_out) {  // Request Redirect
-                y = nth_paired(I, q, (int)pick(I.h(round, p, 2), (uint32_t)nq));
-                const int a = I.up[y] >= 0 ? I.up[y] / MC : -1, c = I.down[y] >= 0 ? I.down[y] / MC : -1;
+              if (sm.first_free() != 63 && !sm.has_out()) {  // Request Redirect
+                y = I.nth_paired(q, (int)pick(I.h(p, 2), (uint32_t)nq));
+                const int a = I.up[y] >= 0 ? I.relay(I.up[y]) : -1;
+                const int c = I.down[y] >= 0 ? I.relay(I.down[y]) : -1;
                 const int64_t dax = I.d(a, p), dxc = I.d(p, c), dab = I.d(a, q), dbc = I.d(q, c);
                 if (dax != INF && dxc != INF && dab != INF && dbc != INF) {
                   delta = P.objective == 0 ? (dax + dxc) - (dab + dbc) : max(dax, dxc) - max(dab, dbc);
                   kind = K_REDIRECT;
-                  z = sc.first_free;
+                  z = p * MC + sm.first_free();
                   t0 = y; t1 = I.res_up(I.up[y]); t2 = I.res_dn(I.down[y]); t3 = z;
                   ok = true;
                 }
-              } else if (sc.npaired > 0) {  // Request Change
-                x = nth_paired(I, p, (int)pick(I.h(round, p, 1), (uint32_t)sc.npaired));
-                y = nth_paired(I, q, (int)pick(I.h(round, p, 2), (uint32_t)nq));
-                const int j1 = I.down[x] >= 0 ? I.down[x] / MC : -1, j2 = I.down[y] >= 0 ? I.down[y] / MC : -1;
+              } else if (sm.npaired() > 0) {  // Request Change
+                x = I.nth_paired(p, (int)pick(I.h(p, 1), (uint32_t)sm.npaired()));
+                y = I.nth_paired(q, (int)pick(I.h(p, 2), (uint32_t)nq));
+                const int j1 = I.down[x] >= 0 ? I.relay(I.down[x]) : -1;
+                const int j2 = I.down[y] >= 0 ? I.relay(I.down[y]) : -1;
                 if (j1 != j2) {
                   const int64_t a1 = I.d(p, j2), a2 = I.d(q, j1), b1 = I.d(p, j1), b2 = I.d(q, j2);
                   if (a1 != INF && a2 != INF && b1 != INF && b2 != INF) {
@@ -348,7 +482,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
                 bool accept = delta < 0;
                 if (delta > 0 && delta < P.thr_width) {  // annealing
                   const int kk = min(I.kacc[p], P.thr_K);
-                  accept = (I.h(round, p, 3) >> 32) < (uint64_t)P.thr[(size_t)kk * P.thr_width + delta];
+                  accept = (I.h(p, 3) >> 32) < (uint64_t)P.thr[(size_t)kk * P.thr_width + delta];
                 }
                 if (accept) key = ((uint64_t)(delta + (1ll << 40)) << 22) | (uint64_t)p;
                 else kind = K_NONE;
@@ -357,16 +491,15 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
           }
         }
         if (key == RES_NONE) kind = K_NONE;
-        I.prop[p * 6 + 0] = kind;
-        I.prop[p * 6 + 1] = x;
-        I.prop[p * 6 + 2] = y;
-        I.prop[p * 6 + 3] = z;
+        I.prop[p * 4 + 0] = kind;
+        I.prop[p * 4 + 1] = x;
+        I.prop[p * 4 + 2] = y;
+        I.prop[p * 4 + 3] = z;
         I.pkey[p] = key;
         I.ptouch[p * 4 + 0] = t0;
         I.ptouch[p * 4 + 1] = t1;
         I.ptouch[p * 4 + 2] = t2;
         I.ptouch[p * 4 + 3] = t3;
-        // ---------- R5 reservations ----------
         if (kind != K_NONE) {
           atomicMin((unsigned long long*)&I.res[t0], (unsigned long long)key);
           atomicMin((unsigned long long*)&I.res[t1], (unsigned long long)key);
@@ -377,16 +510,16 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       T.sync();
       // ---------- R6 commit the proposals that hold every slot they touch ----------
       for (int p = T.tid; p < Sn; p += TPI) {
-        const int kind = I.prop[p * 6 + 0];
+        const int kind = I.prop[p * 4 + 0];
         if (kind == K_NONE) continue;
         const uint64_t key = I.pkey[p];
         bool win = true;
         for (int q = 0; q < 4; ++q) {
-          const int64_t t = I.ptouch[p * 4 + q];
-          if (t >= 0) win = win && __ldcg(&I.res[t]) == key;
+          const int32_t t = I.ptouch[p * 4 + q];
+          if (t >= 0) win = win && ld_res<kSmem>(&I.res[t]) == key;
         }
         if (!win) continue;
-        const int32_t x = I.prop[p * 6 + 1], y = I.prop[p * 6 + 2], z = I.prop[p * 6 + 3];
+        const int32_t x = I.prop[p * 4 + 1], y = I.prop[p * 4 + 2], z = I.prop[p * 4 + 3];
         if (kind == K_CHANGE) {
           const int32_t dx = I.down[x], dy = I.down[y];
           I.down[x] = dy;
@@ -413,10 +546,10 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       }
       T.sync();
       for (int p = T.tid; p < Sn; p += TPI) {  // release the reservations for the next round
-        if (I.prop[p * 6 + 0] == K_NONE) continue;
+        if (I.prop[p * 4 + 0] == K_NONE) continue;
         for (int q = 0; q < 4; ++q) {
-          const int64_t t = I.ptouch[p * 4 + q];
-          if (t >= 0) __stcg(&I.res[t], RES_NONE);
+          const int32_t t = I.ptouch[p * 4 + q];
+          if (t >= 0) st_res<kSmem>(&I.res[t], RES_NONE);
         }
       }
       // ---------- R7 ----------
@@ -464,19 +597,19 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       for (int k = T.tid; k < M; k += TPI) {
         int32_t p = I.src_down[k];
         if (p == kNone) continue;
-        int64_t cc = I.d(-1, p / MC);
+        int64_t cc = cst(I.src[I.relay(p)]);
         int guard = 0;
         bool ok = true;
         while (p >= 0 && ++guard <= S + 1) {
           const int32_t nx = I.down[p];
           if (nx == kNone) { ok = false; break; }
-          cc = sadd(cc, I.d(p / MC, nx <= -2 ? -1 : nx / MC));
+          cc = sadd(cc, I.d(I.relay(p), nx <= -2 ? -1 : I.relay(nx)));
           p = nx;
         }
         if (ok && p <= -2 && cc != INF) { f += 1; c += (unsigned long long)cc; }
       }
       int dg = 0;
-      for (int p = T.tid; p < Sn * MC; p += TPI) dg += I.st(p) == 1;
+      for (int p = T.tid; p < Sn * MC; p += TPI) dg += I.st(p) == ST_OUT;
       for (int off = 16; off > 0; off >>= 1) {
         f += __shfl_xor_sync(0xffffffffu, f, off);
         c += __shfl_xor_sync(0xffffffffu, c, off);
@@ -489,6 +622,11 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       }
     }
     T.sync();
+    if constexpr (kSmem) {
+      for (int k = T.tid; k < Sn * MC; k += TPI) { g_up[k] = I.up[k]; g_down[k] = I.down[k]; }
+      for (int k = T.tid; k < M; k += TPI) { g_src_down[k] = I.src_down[k]; g_snk_up[k] = I.snk_up[k]; }
+      for (int k = T.tid; k < Sn; k += TPI) { g_kacc[k] = I.kacc[k]; g_deny[k] = I.deny[k]; }
+    }
     if (T.tid == 0) {
       if (o.rounds_run) o.rounds_run[b] = r;
       if (o.F_dec) o.F_dec[b] = (int64_t)sh_u64[T.id][0];
@@ -513,21 +651,43 @@ __global__ void init_round_state_kernel(const Problem P) {
 }
 
 template <int TPI>
-cudaError_t launch_rounds_tpi(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms) {
-  const int teams = 256 / TPI > 8 ? 8 : 256 / TPI;
-  auto k = rounds_kernel<TPI>;
+cudaError_t launch_rounds_tpi(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms, bool smem) {
+  const size_t ws = rounds_layout(P, smem).total;
+  const size_t limit = 200 * 1024;
+  int teams = TPI >= 256 ? 1 : 256 / TPI;
+  if (teams > 8) teams = 8;
+  if (smem)
+    while (teams > 1 && teams * ws > limit) --teams;
+  const size_t dyn = smem ? teams * ws : 0;
+  auto k = smem ? rounds_kernel<TPI, true> : rounds_kernel<TPI, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, teams * TPI, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, teams * TPI, dyn);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   long long grid = (long long)per_sm * num_sms;
   const long long need = (P.B + teams - 1) / teams;
   if (grid > need) grid = need;
-  k<<<(int)grid, teams * TPI, 0, st>>>(P, o);
+  if (!smem && grid * teams > P.ws_rounds_teams) grid = P.ws_rounds_teams / teams;
+  if (grid < 1) grid = 1;
+  k<<<(int)grid, teams * TPI, dyn, st>>>(P, o, ws);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+size_t rounds_ws_bytes(const Problem& P, bool smem) { return rounds_layout(P, smem).total; }
+
+int rounds_tpi(const Problem& P) {
+  const int Sn = P.S * P.n;
+  const int tpi = Sn <= 32 ? 32 : Sn <= 64 ? 64 : Sn <= 128 ? 128 : 256;  // ~one relay per thread
+  return getenv_int("GWTF_ROUNDS_TPI", tpi);
+}
+
+bool rounds_use_smem(const Problem& P) {
+  return rounds_layout(P, true).total <= 200 * 1024 && getenv_int("GWTF_ROUNDS_GLOBAL", 0) == 0;
+}
 
 cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st) {
   init_round_state_kernel<<<148 * 4, 256, 0, st>>>(P);
@@ -537,11 +697,12 @@ cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st) {
 cudaError_t launch_rounds(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms) {
   cudaError_t e = cudaMemsetAsync(P.counters + 1, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
-  const int Sn = P.S * P.n;
-  if (Sn <= 128) return launch_rounds_tpi<32>(P, o, st, num_sms);
-  if (Sn <= 512) return launch_rounds_tpi<64>(P, o, st, num_sms);
-  if (Sn <= 4096) return launch_rounds_tpi<128>(P, o, st, num_sms);
-  return launch_rounds_tpi<256>(P, o, st, num_sms);
+  const int tpi = rounds_tpi(P);
+  const bool smem = rounds_use_smem(P);
+  if (tpi <= 32) return launch_rounds_tpi<32>(P, o, st, num_sms, smem);
+  if (tpi <= 64) return launch_rounds_tpi<64>(P, o, st, num_sms, smem);
+  if (tpi <= 128) return launch_rounds_tpi<128>(P, o, st, num_sms, smem);
+  return launch_rounds_tpi<256>(P, o, st, num_sms, smem);
 }
 
 }  // namespace gwtf
