@@ -54,7 +54,7 @@ typedef enum { GWTF_OBJ_SUM = 0, GWTF_OBJ_MINIMAX = 1 } gwtf_objective;
 typedef struct {
   uint32_t abi_version;        /* must be GWTF_ABI_VERSION */
   int32_t num_instances;       /* B >= 1 */
-  int32_t num_stages;          /* S >= 1 */
+  int32_t num_stages;          /* S, 1..64 */
   int32_t clients_per_stage;   /* n, 1..4096 (absent clients: alive = 0) */
   int32_t max_cap;             /* 0..32: bound on cap, sizes the per-relay slot arrays */
   /* inputs, read during create and COPIED into the handle (caller may free afterwards): */

@@ -217,6 +217,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   if (B < 1 || S < 1 || n < 1) return fail(GWTF_E_INVALID, "num_instances, num_stages, clients_per_stage must be >= 1");
   if (MC < 0 || MC > 32) return fail(GWTF_E_INVALID, "max_cap must be in [0, 32]");
   if (n > 4096) return fail(GWTF_E_UNSUPPORTED, "clients_per_stage > 4096");
+  if (S > 64) return fail(GWTF_E_UNSUPPORTED, "num_stages > 64");
   if (S * n >= (1 << 21)) return fail(GWTF_E_UNSUPPORTED, "S*n >= 2^21");
   if (!d->cap || !d->src_cost || !d->snk_cost || !d->supply || (S > 1 && !d->link_cost))
     return fail(GWTF_E_INVALID, "NULL input array");
@@ -281,6 +282,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   AL(P.quiet, B, true);
   AL(P.round, B, true);
   AL(P.counters, 8, false);
+  AL(P.redo, B, false);
   AL(h->bad_flag, 4, false);
   uint32_t* thr_d = nullptr;
   AL(thr_d, thr.size(), false);
@@ -349,6 +351,13 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   const long double bound = (long double)(2 * S * n + 2) * (long double)maxc;
   if (bound >= (long double)(1ull << 42)) return bail(fail(GWTF_E_OVERFLOW, "(2Sn+2)*maxcost >= 2^42"));
   if (bound * (long double)Mmax >= (long double)(1ull << 62)) return bail(fail(GWTF_E_OVERFLOW, "(2Sn+2)*maxcost*M >= 2^62"));
+  // 32-bit packed keys (cost << H | hops) when the largest arc weight leaves the guard band
+  // free: (maxcost << H) + 1 < 2^29 with 2^H > 2Sn+1; else 64-bit keys
+  {
+    int H = 0;
+    while ((1ll << H) <= 2 * S * n + 1) ++H;
+    P.hbits = (H < 29 && ((maxc << H) + 1) < (1ll << 29)) ? H : 0;
+  }
   if (link_tmp) {
     cudaFree(link_tmp);
     h->allocs.erase(std::find(h->allocs.begin(), h->allocs.end(), (void*)link_tmp));

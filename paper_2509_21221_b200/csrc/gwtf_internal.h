@@ -45,8 +45,10 @@ struct Problem {
   int32_t objective, W, deny_after;
   const uint32_t* thr;         // [(K+1)][width]
   int32_t thr_width, thr_K;
-  // persistent work queue counter(s)
+  // persistent work queue counters: [0] ssp queue, [1] rounds queue, [2] redo count, [3] redo queue
   int32_t* counters;           // [8]
+  int32_t* redo;               // [B] instances re-solved with 64-bit keys (32-bit key overflow guard)
+  int32_t hbits;               // hop bits of the 32-bit packed keys; 0 = 64-bit keys only
   // global workspace for teams whose instance does not fit in shared memory
   uint8_t* ws;
   size_t ws_per_team;
