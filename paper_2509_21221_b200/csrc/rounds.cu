@@ -662,6 +662,8 @@ cudaError_t launch_rounds_tpi(const Problem& P, const RoundsOut& o, cudaStream_t
   auto k = smem ? rounds_kernel<TPI, true> : rounds_kernel<TPI, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, teams * TPI, dyn);
   if (e != cudaSuccess) return e;

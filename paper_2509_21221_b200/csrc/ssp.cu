@@ -120,7 +120,7 @@ __host__ __device__ inline SspLayout ssp_layout(const Problem& P, bool with_tile
 __device__ __forceinline__ int nid(int layer, int pos) { return (layer << 16) | pos; }
 
 template <int TPI, bool kSmem, bool k32, bool kRedo>
-__global__ void __launch_bounds__(256) ssp_kernel(const Problem P, const SspOut o, const size_t ws_bytes) {
+__global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TPI : 6) ssp_kernel(const Problem P, const SspOut o, const size_t ws_bytes) {
   using K = typename KT<k32>::K;
   constexpr K INF = KT<k32>::INF;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -565,6 +565,8 @@ cudaError_t launch_one(const Problem& P, const SspOut& o, cudaStream_t st, int n
     while (teams > 1 && teams * ws > limit) --teams;
     const size_t smem = teams * ws;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, teams * TPI, smem);
