@@ -39,6 +39,7 @@ struct Problem {
   // per-team scratch of the rounds kernel when the instance does not fit in shared memory
   uint8_t* ws_rounds;
   int32_t ws_rounds_teams;
+  int32_t rounds_cost_mode;    // R0 strategy: 0 stage-synchronous, 1 chain walk per slot, 2 per relay
   // parameters of the rounds
   uint64_t seed;
   int64_t inst_base;

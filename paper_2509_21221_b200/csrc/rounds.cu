@@ -112,6 +112,62 @@ struct Inst {
     }
     return fi | (ff << 6) | (np << 12) | (ho << 18);
   }
+  // R0 for one relay: cost to sink of each usable slot by walking its down chain (the
+  // back-to-front recursion cost(slot) = d(v, node(down)) + cost(down) unrolled; no barriers);
+  // returns adv(v) = min cost over its OUT slots
+  __device__ int64_t relay_costs(int v) const {
+    const int s0 = dn.div(v), i0 = v - s0 * n, c = capv[v];
+    int64_t best = INF;
+    for (int j = 0; j < c; ++j) {
+      const int p0 = v * MC + j;
+      int32_t p = down[p0];
+      int64_t cc = p == kNone ? INF : 0;
+      int s = s0, i = i0;
+      while (p != kNone) {
+        if (p <= -2) { cc = sadd(cc, cst(snk[i])); break; }
+        const int w = relay(p), wi = w - (s + 1) * n;
+        cc = sadd(cc, c_link(s, i, wi));
+        s += 1;
+        i = wi;
+        p = down[p];
+        if (p == kNone) cc = INF;
+      }
+      scost[p0] = cc;
+      if (up[p0] == kNone && down[p0] != kNone && cc < best) best = cc;
+    }
+    return best;
+  }
+  // chain walk of one slot (unusable slots get INF)
+  __device__ void slot_cost(int p0) const {
+    const int v = relay(p0), j = p0 - v * MC;
+    int64_t cc = INF;
+    if (j < capv[v]) {
+      int32_t p = down[p0];
+      if (p != kNone) {
+        cc = 0;
+        int s = dn.div(v), i = v - s * n;
+        while (true) {
+          if (p <= -2) { cc = sadd(cc, cst(snk[i])); break; }
+          const int w = relay(p), wi = w - (s + 1) * n;
+          cc = sadd(cc, c_link(s, i, wi));
+          s += 1;
+          i = wi;
+          p = down[p];
+          if (p == kNone) { cc = INF; break; }
+        }
+      }
+    }
+    scost[p0] = cc;
+  }
+  __device__ int64_t relay_adv(int v) const {
+    int64_t bc = INF;
+    const int c = capv[v];
+    for (int j = 0; j < c; ++j) {
+      const int p = v * MC + j;
+      if (up[p] == kNone && down[p] != kNone && scost[p] < bc) bc = scost[p];
+    }
+    return bc;
+  }
   __device__ int nth_paired(int v, int q) const {
     const int c = capv[v], base = v * MC;
     for (int j = 0; j < c; ++j)
@@ -284,24 +340,26 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
 
     for (int k = T.tid; k < nres; k += TPI) st_res<kSmem>(&I.res[k], RES_NONE);
     int quiet = 0;  // quiet = 0 at the start of every call (DESIGN.md 2.3 R7)
+    const int cost_mode = P.rounds_cost_mode;
     uint64_t round = (uint64_t)P.round[b];
     int r = 0;
     T.sync();
     while (r < o.max_rounds) {
       int changed = 0;
       I.set_round(round);
-      // ---------- slot summaries; R0a candidates (IN and OUT at one relay) ----------
+      // ---------- R0a candidates: a relay holding an IN and an OUT slot ----------
+      if (T.tid == 0) { sh_i32[T.id][0] = INT_MAX; sh_i32[T.id][1] = 0; }
       int cand = 0;
       for (int v = T.tid; v < Sn; v += TPI) {
         const uint32_t w = I.summarize(v);
-        I.summ[v] = w;
         cand |= (w & 63u) != 63u && ((w >> 18) & 1u);
       }
       if (T.sync_or(cand)) {
         // ---------- R0a self-pairing, costs of the round-start state ----------
-        compute_costs(T, I);
+        for (int v = T.tid; v < Sn; v += TPI) I.relay_costs(v);
+        T.sync();
         for (int v = T.tid; v < Sn; v += TPI) {
-          const Summ sm{I.summ[v]};
+          const Summ sm{I.summarize(v)};
           if (!sm.has_in() || !sm.has_out()) continue;
           const int x = v * MC + sm.first_in();
           int oo = -1;
@@ -316,23 +374,18 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
           changed = 1;
         }
         T.sync();
-        for (int v = T.tid; v < Sn; v += TPI) I.summ[v] = I.summarize(v);
+      }
+      // ---------- R0 cost to sink + advertisements; data-node slots ----------
+      if (cost_mode == 0) {  // stage-synchronous back-to-front recursion, then advertisements
+        compute_costs(T, I);
+        for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
+      } else if (cost_mode == 1) {  // one chain walk per slot, then advertisements
+        for (int t = T.tid; t < Sn * MC; t += TPI) I.slot_cost(t);
         T.sync();
+        for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
+      } else {  // one chain walk per relay (fused advertisement)
+        for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_costs(v);
       }
-      // ---------- R0 cost to sink + advertisements ----------
-      compute_costs(T, I);
-      for (int v = T.tid; v < Sn; v += TPI) {
-        int64_t bc = INF;
-        if ((I.summ[v] >> 18) & 1u) {  // has an OUT slot
-          for (int j = 0; j < I.capv[v]; ++j) {
-            const int p = v * MC + j;
-            if (I.st(p) == ST_OUT && I.scost[p] < bc) bc = I.scost[p];
-          }
-        }
-        I.adv_cost[v] = bc;
-      }
-      if (T.tid == 0) { sh_i32[T.id][0] = INT_MAX; sh_i32[T.id][1] = 0; }
-      T.sync();
       {
         int fs = INT_MAX, anyfree = 0;
         for (int k = T.tid; k < M; k += TPI) {
@@ -359,7 +412,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
             if (tg != -2) rs = -2 - d_rslot;
           }
         } else if (I.alive[rr]) {
-          const Summ sm{I.summ[rr]};
+          const Summ sm{I.summarize(rr)};
           int32_t x = kNone;
           if (sm.has_in()) x = rr * MC + sm.first_in();                                   // (a)
           else if (!sm.has_out() && sm.first_free() != 63) x = rr * MC + sm.first_free();  // (b)
@@ -386,43 +439,61 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
         I.req_target[rr] = tg;
       }
       T.sync();
-      // ---------- R2 grants: rank among same-target requesters in ascending gid ----------
-      for (int rr = T.tid; rr <= Sn; rr += TPI) {
-        const int tg = I.req_target[rr];
-        int32_t grant = kNone;
-        if (tg >= 0) {
-          int rank = 0;
-          if (rr != Sn) {
-            if (I.req_target[Sn] == tg) ++rank;  // D orders before all relays
-            const int s0 = I.dn.div(rr) * n;
-            for (int q = s0; q < rr; ++q) rank += I.req_target[q] == tg;
+      // ---------- R2 + R3: each target serves its requesters in ascending gid and commits ----------
+      // (a target's eligibility only reads its own OUT slots, which only it modifies; requester
+      // slots are IN/FREE slots written by exactly one target, so the fused commit equals
+      // "all grants on the pre-R3 state, then all commits")
+      for (int j = T.tid; j <= Sn; j += TPI) {
+        if (j == Sn) {  // D-sink: free SNK slots in index order to last-stage requesters in gid order
+          int k = 0;
+          for (int q = (S - 1) * n; q < Sn; ++q) {
+            if (I.req_target[q] != -1) continue;
+            while (k < M && I.snk_up[k] != kNone) ++k;
+            if (k >= M) break;
+            const int32_t rs = I.req_slot[q];
+            I.down[rs] = -2 - k;
+            I.snk_up[k] = rs;
+            I.deny[q] = 0;
+            changed = 1;
+            ++k;
           }
-          const int64_t ac = I.adv_cost[tg];
-          for (int j = 0; j < I.capv[tg]; ++j) {
-            const int p = tg * MC + j;
-            if (I.st(p) == ST_OUT && I.scost[p] == ac) { if (rank == 0) { grant = p; break; } --rank; }
-          }
-        } else if (tg == -1) {
-          int rank = 0;
-          for (int q = (S - 1) * n; q < rr; ++q) rank += I.req_target[q] == -1;
-          for (int k = 0; k < M; ++k)
-            if (I.snk_up[k] == kNone) { if (rank == 0) { grant = -2 - k; break; } --rank; }
+          continue;
         }
-        I.grant[rr] = grant;
+        const int64_t ac = I.adv_cost[j];
+        if (ac == INF) continue;  // no OUT slot: nothing to grant
+        const int s = I.dn.div(j);
+        const int c = I.capv[j];
+        int cur = 0;
+        auto next_slot = [&]() -> int {
+          while (cur < c) {
+            const int p = j * MC + cur++;
+            if (I.st(p) == ST_OUT && I.scost[p] == ac) return p;
+          }
+          return -1;
+        };
+        if (s == 0) {  // the data node is the only requester of stage-0 relays
+          if (I.req_target[Sn] == j) {
+            const int p = next_slot();
+            if (p >= 0) {
+              const int32_t rs = I.req_slot[Sn];
+              I.src_down[-2 - rs] = p;
+              I.up[p] = rs;
+              changed = 1;
+            }
+          }
+        } else {
+          for (int q = (s - 1) * n; q < s * n; ++q) {
+            if (I.req_target[q] != j) continue;
+            const int p = next_slot();
+            if (p < 0) break;
+            const int32_t rs = I.req_slot[q];
+            I.down[rs] = p;
+            I.up[p] = rs;
+            I.deny[q] = 0;
+            changed = 1;
+          }
+        }
       }
-      T.sync();
-      // ---------- R3 commit grants ----------
-      for (int rr = T.tid; rr <= Sn; rr += TPI) {
-        const int32_t grant = I.grant[rr];
-        if (grant == kNone) continue;
-        const int32_t rs = I.req_slot[rr];
-        if (rr == Sn) I.src_down[-2 - rs] = grant;
-        else { I.down[rs] = grant; I.deny[rr] = 0; }
-        I.set_up_of(grant, rs);
-        changed = 1;
-      }
-      T.sync();
-      for (int v = T.tid; v < Sn; v += TPI) I.summ[v] = I.summarize(v);
       T.sync();
       // ---------- R4 proposals by idle relays (post-R3 state) + R5 reservations ----------
       for (int p = T.tid; p < Sn; p += TPI) {
@@ -431,7 +502,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
         int32_t t0 = -1, t1 = -1, t2 = -1, t3 = -1;
         uint64_t key = RES_NONE;
         if (I.alive[p] && I.req_target[p] == -2) {
-          const Summ sm{I.summ[p]};
+          const Summ sm{I.summarize(p)};
           const int s = I.dn.div(p), i = p - s * n;
           if (sm.has_in()) {  // DENY after deny_after idle rounds holding unpaired inflow
             const int dw = I.deny[p] + 1;
@@ -447,7 +518,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
             uint32_t qi = pick(I.h(p, 0), (uint32_t)(n - 1));
             if ((int)qi >= i) qi += 1;
             const int q = s * n + (int)qi;
-            const int nq = I.alive[q] ? Summ{I.summ[q]}.npaired() : 0;
+            const int nq = I.alive[q] ? Summ{I.summarize(q)}.npaired() : 0;
             if (nq > 0) {
               int64_t delta = 0;
               bool ok = false;
@@ -492,15 +563,15 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
         }
         if (key == RES_NONE) kind = K_NONE;
         I.prop[p * 4 + 0] = kind;
-        I.prop[p * 4 + 1] = x;
-        I.prop[p * 4 + 2] = y;
-        I.prop[p * 4 + 3] = z;
-        I.pkey[p] = key;
-        I.ptouch[p * 4 + 0] = t0;
-        I.ptouch[p * 4 + 1] = t1;
-        I.ptouch[p * 4 + 2] = t2;
-        I.ptouch[p * 4 + 3] = t3;
         if (kind != K_NONE) {
+          I.prop[p * 4 + 1] = x;
+          I.prop[p * 4 + 2] = y;
+          I.prop[p * 4 + 3] = z;
+          I.pkey[p] = key;
+          I.ptouch[p * 4 + 0] = t0;
+          I.ptouch[p * 4 + 1] = t1;
+          I.ptouch[p * 4 + 2] = t2;
+          I.ptouch[p * 4 + 3] = t3;
           atomicMin((unsigned long long*)&I.res[t0], (unsigned long long)key);
           atomicMin((unsigned long long*)&I.res[t1], (unsigned long long)key);
           if (t2 >= 0) atomicMin((unsigned long long*)&I.res[t2], (unsigned long long)key);
@@ -696,7 +767,9 @@ cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_rounds(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms) {
+cudaError_t launch_rounds(const Problem& P0, const RoundsOut& o, cudaStream_t st, int num_sms) {
+  Problem P = P0;
+  P.rounds_cost_mode = getenv_int("GWTF_ROUNDS_COSTS", 0);
   cudaError_t e = cudaMemsetAsync(P.counters + 1, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
   const int tpi = rounds_tpi(P);
