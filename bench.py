@@ -32,7 +32,7 @@ import gen  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gwtf", choices=["gwtf", "reference"])
     ap.add_argument("--config", default="gpt")
@@ -67,54 +67,65 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled every 100 ms during the timed loop
+    (one `nvidia-smi -lms` stream, started before and stopped after the timed steps)."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index, self.rows, self.stop = index, [], threading.Event()
-
-    def _run(self):
-        while not self.stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([x.strip() for x in line.split(",")])
-            except Exception:
-                pass
-            self.stop.wait(0.2)
+        self.index, self.rows, self.proc = index, [], None
 
     def __enter__(self):
-        self.t = threading.Thread(target=self._run, daemon=True)
-        self.t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the first sample land before the timed region starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.stop.set()
-        self.t.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.strip().splitlines():
+            self.rows.append([x.strip() for x in line.split(",")])
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        num = lambda x: x.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(r[0]) for r in self.rows if r and num(r[0])]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and num(r[1])]
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
 
 
-def cpu_baseline(cfg, sample, inst0=0):
-    """The oracle (as it stands) on the host cores, on a bounded sample of the same workload."""
+def cpu_baseline(cfg, target_s=15.0, inst0=0):
+    """The oracle (as it stands) on the host cores, on a bounded sample of the same workload,
+    sized for about target_s seconds of CPU work (calibrated on a small first sample)."""
     from tests import harness
     threads = os.cpu_count() or 1
+    cal = max(threads * 4, 32)
     t = time.perf_counter()
-    harness.oracle_pipeline(cfg, inst0, sample, seed=0, threads=threads)
+    harness.oracle_pipeline(cfg, inst0, cal, seed=0, threads=threads)
+    rate = cal / max(time.perf_counter() - t, 1e-6)
+    sample = int(min(max(rate * target_s, cal), 200000))
+    t = time.perf_counter()
+    harness.oracle_pipeline(cfg, inst0 + cal, sample, seed=0, threads=threads)
     dt = time.perf_counter() - t
     return {"value": sample / dt, "unit": "instances/s", "cores": threads, "kind": "oracle",
-            "sample": f"{sample} instances of the same workload (full step: pre-churn rounds + churn + SSP + repair rounds), "
-                      f"{dt:.2f} s on {threads} threads"}
+            "sample": f"{sample} instances of the same workload (full step: pre-churn rounds + churn + SSP + "
+                      f"repair rounds), {dt:.1f} s on {threads} threads, one instance per thread"}
 
 
 def run_reference(args, cfg, rank, world):
@@ -262,7 +273,7 @@ def main():
     if rank == 0 and not (args.quick or args.no_e2e):
         line["e2e"] = e2e(cfg, B, inst0, dev, args)
     if rank == 0 and not (args.quick or args.no_cpu_baseline):
-        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample or max(64, (os.cpu_count() or 1) * 32))
+        line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
