@@ -36,6 +36,7 @@ extern "C" {
 #define GWTF_ABSENT INT32_MAX
 #define GWTF_HOST_PTRS (1u << 0) /* array arguments of every call on this handle are host pointers */
 #define GWTF_FORCE_GLOBAL_TIER (1u << 30) /* testing: run the exact solve through the global-memory tier */
+#define GWTF_FORCE_CLUSTER_TIER (1u << 29) /* testing: run the exact solve through the cluster tier */
 
 typedef struct gwtf_flow_s* gwtf_flow_t; /* opaque; owns all device workspace */
 
@@ -74,7 +75,7 @@ typedef struct {
   int32_t deny_after;          /* idle rounds holding unpaired inflow before DENY (default 3) */
   int32_t device;              /* CUDA device ordinal */
   void* stream;                /* cudaStream_t (NULL = legacy default stream) */
-  uint32_t flags;              /* GWTF_HOST_PTRS | GWTF_FORCE_GLOBAL_TIER */
+  uint32_t flags;              /* GWTF_HOST_PTRS | GWTF_FORCE_GLOBAL_TIER | GWTF_FORCE_CLUSTER_TIER */
 } gwtf_problem_desc;
 
 /* Eq. 1 evaluated on the device in integer half-units:
@@ -145,6 +146,11 @@ gwtf_status gwtf_flow_restore(gwtf_flow_t h);
 gwtf_status gwtf_flow_set_profiling(gwtf_flow_t h, int32_t on);
 gwtf_status gwtf_flow_kernel_times(gwtf_flow_t h, const char** names, float* ms, int32_t* launches,
                                    int32_t cap, int32_t* count);
+
+/* Work counters of the exact solve accumulated since create (host int64 out[cap], cap <= 8):
+ * [0] dense boundary relaxations, [1] backward (reverse-arc) phases, [2] augmentations,
+ * [3] Bellman-Ford passes, [4] traced path nodes (cluster tier).  Synchronizes the stream. */
+gwtf_status gwtf_flow_stats(gwtf_flow_t h, int64_t* out, int32_t cap);
 
 /* Synchronizes the stream, frees everything.  NULL is a no-op. */
 gwtf_status gwtf_flow_destroy(gwtf_flow_t h);

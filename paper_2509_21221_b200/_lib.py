@@ -13,7 +13,8 @@ LIB_PATH = os.path.join(_HERE, "libgwtf.so")
 
 GWTF_ABI_VERSION = 1
 GWTF_HOST_PTRS = 1 << 0
-GWTF_FORCE_GLOBAL_TIER = 1 << 30  # internal/testing: exact solve through the global-memory tier
+GWTF_FORCE_GLOBAL_TIER = 1 << 30  # testing: exact solve through the global-memory tier
+GWTF_FORCE_CLUSTER_TIER = 1 << 29  # testing: exact solve through the cluster tier
 OBJ_SUM, OBJ_MINIMAX = 0, 1
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NOMEM", 3: "E_CUDA", 4: "E_OVERFLOW", 5: "E_STATE", 6: "E_UNSUPPORTED"}
 
@@ -48,6 +49,7 @@ EXPORTS = {
     "gwtf_flow_restore": ([P], I32),
     "gwtf_flow_set_profiling": ([P, I32], I32),
     "gwtf_flow_kernel_times": ([P, ctypes.POINTER(ctypes.c_char_p), P, P, I32, P], I32),
+    "gwtf_flow_stats": ([P, P, I32], I32),
     "gwtf_flow_destroy": ([P], I32),
     "gwtf_last_error": ([], ctypes.c_char_p),
     "gwtf_abi_version": ([], I32),

@@ -76,6 +76,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---- distributed shared memory (thread-block clusters) ----------------------------------
+// shared::cluster address of `local_ptr`'s counterpart in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local_ptr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local_ptr)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint64_t dsmem_ld_u64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
+// 64-bit unsigned atomic min on another CTA's shared memory.  A plain atomicMin on a
+// map_shared_rank() pointer (and atom.shared::cluster.min.u64) compiles to a generic 64-bit
+// ATOM with a CAS-loop fallback that loses updates across SMs on sm_100a (measured: a
+// 16-CTA min returned 998 instead of 985); the CAS itself is a native remote operation.
+__device__ __forceinline__ uint64_t dsmem_atomic_min_u64(uint32_t addr, uint64_t v) {
+  uint64_t cur = dsmem_ld_u64(addr);
+  while (v < cur) {
+    uint64_t prev;
+    asm volatile("atom.shared::cluster.cas.b64 %0, [%1], %2, %3;" : "=l"(prev) : "r"(addr), "l"(cur), "l"(v) : "memory");
+    if (prev == cur) return cur;
+    cur = prev;
+  }
+  return cur;
+}
+
 // ---- packed lexicographic keys: key = cost << 20 | hops -------------
 __device__ __forceinline__ uint64_t key_fwd(uint64_t k, int32_t c) {  // k + (c, 1)
   return k + ((uint64_t)(uint32_t)c << kHopBits) + 1ull;

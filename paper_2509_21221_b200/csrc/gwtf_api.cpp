@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -283,6 +284,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   AL(P.round, B, true);
   AL(P.counters, 8, false);
   AL(P.redo, B, false);
+  AL(P.stats, 2048, false);
   AL(h->bad_flag, 4, false);
   uint32_t* thr_d = nullptr;
   AL(thr_d, thr.size(), false);
@@ -297,9 +299,24 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   P.objective = d->objective;
   P.W = d->steady_window;
   P.deny_after = d->deny_after;
+  if (const char* dbg = getenv("GWTF_DEBUG_FLAGS")) P.debug = atoi(dbg);
 
-  // global workspace for the shared-memory-overflow tier of the exact solve
-  if (ssp_smem_bytes(P) > 227 * 1024 || (h->flags & GWTF_FORCE_GLOBAL_TIER)) {
+  // exact-solve tiers for instances that do not fit in shared memory: the cluster tier (one
+  // thread-block cluster per instance, tiles streamed from HBM) when the device can host it,
+  // else the global-memory team tier
+  const bool big = ssp_smem_bytes(P) > 227 * 1024;
+  if (big || (h->flags & GWTF_FORCE_CLUSTER_TIER)) {
+    P.cluster_size = ssp_cluster_size(P);
+    if (P.cluster_size > 0) {
+      P.ws_cluster_slots = (int32_t)std::min<int64_t>(h->num_sms / P.cluster_size, B);
+      uint8_t* wc = nullptr;
+      if ((s = alloc(h, &wc, (size_t)P.ws_cluster_slots * (2 * Sn + 4) * 4)) != GWTF_OK) return bail(s);
+      P.ws_cluster = wc;
+    } else if (h->flags & GWTF_FORCE_CLUSTER_TIER) {
+      return bail(fail(GWTF_E_UNSUPPORTED, "cluster tier unavailable for this shape"));
+    }
+  }
+  if ((big && P.cluster_size == 0) || (h->flags & GWTF_FORCE_GLOBAL_TIER)) {
     P.ws_teams = (int32_t)std::min<int64_t>(h->num_sms, B);
     P.ws_per_team = ssp_global_ws_bytes(P);
     uint8_t* ws = nullptr;
@@ -363,6 +380,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     h->allocs.erase(std::find(h->allocs.begin(), h->allocs.end(), (void*)link_tmp));
   }
   CK(h, launch_init_round_state(P, h->stream));
+  CK(h, cudaMemsetAsync(P.stats, 0, 2048 * sizeof(unsigned long long), h->stream));
   CK(h, cudaMemsetAsync(P.arc_cnt, 0, B * std::max<size_t>(nb, 1) * 4, h->stream));
   *out = h;
   return GWTF_OK;
@@ -382,7 +400,8 @@ gwtf_status gwtf_flow_solve_batch(gwtf_flow_t h, int64_t* flow_value, int64_t* t
   if ((s = map_out(h, inst_status, B, 3, &o.status, maps)) != GWTF_OK) return s;
   Timer t;
   prof_begin(h, "ssp_kernel", &t);
-  CK(h, launch_ssp(h->P, o, h->stream, h->num_sms, (h->flags & GWTF_FORCE_GLOBAL_TIER) != 0));
+  const int tier = (h->flags & GWTF_FORCE_GLOBAL_TIER) ? 1 : (h->flags & GWTF_FORCE_CLUSTER_TIER) ? 2 : 0;
+  CK(h, launch_ssp(h->P, o, h->stream, h->num_sms, tier));
   prof_end(h, &t);
   h->has_assignment = true;
   return finish_out(h, maps);
@@ -555,6 +574,17 @@ gwtf_status gwtf_flow_kernel_times(gwtf_flow_t h, const char** names, float* ms,
     if (ms) ms[i] = h->ms[i];
     if (launches) launches[i] = h->launches[i];
   }
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_stats(gwtf_flow_t h, int64_t* out, int32_t cap) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!out || cap < 0) return fail(GWTF_E_INVALID, "stats: NULL out");
+  std::vector<unsigned long long> v(2048);
+  CK(h, cudaMemcpyAsync(v.data(), h->P.stats, 2048 * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < std::min(cap, 2048); ++i) out[i] = (int64_t)v[i];
   return GWTF_OK;
 }
 

@@ -49,7 +49,15 @@ struct Problem {
   // persistent work queue counters: [0] ssp queue, [1] rounds queue, [2] redo count, [3] redo queue
   int32_t* counters;           // [8]
   int32_t* redo;               // [B] instances re-solved with 64-bit keys (32-bit key overflow guard)
+  // work counters of the exact solve (gwtf_flow_stats): relax steps, backward phases,
+  // augmentations, Bellman-Ford passes, traced path nodes
+  unsigned long long* stats;   // [8]
   int32_t hbits;               // hop bits of the 32-bit packed keys; 0 = 64-bit keys only
+  // cluster tier (instances too large for shared memory): cluster size and per-cluster path scratch
+  int32_t cluster_size;        // 0 = cluster tier unavailable
+  uint8_t* ws_cluster;
+  int32_t ws_cluster_slots;
+  int32_t debug;               // GWTF_DEBUG_FLAGS (testing)
   // global workspace for teams whose instance does not fit in shared memory
   uint8_t* ws;
   size_t ws_per_team;
@@ -71,7 +79,11 @@ size_t ssp_global_ws_bytes(const Problem& P);
 size_t rounds_ws_bytes(const Problem& P, bool smem);
 int rounds_tpi(const Problem& P);
 bool rounds_use_smem(const Problem& P);
-cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, bool force_global);
+// tier: 0 automatic (shared memory, else cluster, else global), 1 force global, 2 force cluster
+cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, int force_tier);
+size_t ssp_cluster_smem_bytes(const Problem& P, int C);
+int ssp_cluster_size(const Problem& P);
+cudaError_t launch_ssp_cluster(const Problem& P, const SspOut& o, cudaStream_t st, int C);
 cudaError_t launch_rounds(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms);
 cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st);
 cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32_t* upd, int64_t k,

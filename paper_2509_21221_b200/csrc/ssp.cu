@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
   const size_t tile_elems = (size_t)(S - 1) * n * ld;
   const uint32_t tile_bytes = (uint32_t)(tile_elems * 4);
   uint32_t phase = 0;
+  unsigned long long n_relax = 0, n_back = 0, n_pass = 0;
 
   if (kSmem && T.tid == 0) {
     mbar_init(mbar, 1);
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
         for (int s = 0; s + 1 < S; ++s) {
           if (!((fwd >> s) & 1ull)) continue;
           fwd &= ~(1ull << s);
+          ++n_relax;
           const int32_t* Ts = tile + (size_t)s * n * ld;
           const K* ko = kout + (size_t)s * ld;
           int ch = 0;
@@ -316,6 +318,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
         for (int s = S - 1; s >= 0; --s) {
           if (!((bwd >> s) & 1ull)) continue;
           bwd &= ~(1ull << s);
+          ++n_back;
           for (int vb = 0; vb < n; vb += NG) {
             const int v = vb + gi;
             if (li == 0 && v < n) {
@@ -347,6 +350,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
             bwd |= 1ull << (s - 1);
           }
         }
+        ++n_pass;
         if (!(fwd | bwd) && !tdirty && !trev) break;
       }
       if (tkey == INF) break;  // t* unreachable: F is the maximum flow
@@ -528,6 +532,13 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
 
     // ---- results and the canonical assignment ----
     T.sync();
+    if (T.tid == 0) {
+      atomicAdd(&P.stats[0], n_relax);
+      atomicAdd(&P.stats[1], n_back);
+      atomicAdd(&P.stats[2], (unsigned long long)*A_p);
+      atomicAdd(&P.stats[3], n_pass);
+    }
+    n_relax = n_back = n_pass = 0;
     const int st = *status_p;
     if (k32 && st == 3) {  // key overflow: queue the instance for the 64-bit kernel
       if (T.tid == 0) {
@@ -600,11 +611,14 @@ cudaError_t launch_tpi(const Problem& P, const SspOut& o, cudaStream_t st, int n
 size_t ssp_smem_bytes(const Problem& P) { return ssp_layout(P, true, 8).total; }
 size_t ssp_global_ws_bytes(const Problem& P) { return ssp_layout(P, false, 8).total; }
 
-cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, bool force_global) {
+cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, int force_tier) {
   cudaError_t e = cudaMemsetAsync(P.counters, 0, 4 * sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
-  const bool smem_tier = !force_global && ssp_smem_bytes(P) <= 227 * 1024;
-  if (!smem_tier) return launch_tpi<256>(P, o, st, num_sms, false);
+  const bool smem_tier = force_tier == 0 && ssp_smem_bytes(P) <= 227 * 1024;
+  if (!smem_tier) {
+    if (force_tier != 1 && P.cluster_size > 0) return launch_ssp_cluster(P, o, st, P.cluster_size);
+    return launch_tpi<256>(P, o, st, num_sms, false);
+  }
   if (P.n <= 32) return launch_tpi<32>(P, o, st, num_sms, true);
   if (P.n <= 64) return launch_tpi<64>(P, o, st, num_sms, true);
   if (P.n <= 128) return launch_tpi<128>(P, o, st, num_sms, true);

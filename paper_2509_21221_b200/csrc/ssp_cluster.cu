@@ -1,0 +1,596 @@
+// Exact solve, cluster tier: one thread-block cluster (up to 16 CTAs, one per SM) per instance,
+// for instances whose tiles cannot live in shared memory (e.g. the stress shape: 64 stages x
+// 1,024 clients = 252 MB of int32 tiles).  Same canonical SSP as ssp.cu with
+// 64-bit (cost, hops) keys; only the data placement differs:
+//   * CTA r of the cluster owns destination rows v in [r*R, r*R+R) of every stage: their in/out
+//     keys, node flows and capacities live in its shared memory;
+//   * the dense min-plus relaxation of boundary s streams the CTA's R rows of tile s from HBM
+//     by TMA bulk copies (cp.async.bulk, TR rows per copy, NB copies in flight on an mbarrier
+//     ring) while the out_s key vector is gathered from the owner CTAs through DSMEM;
+//   * one cluster barrier per boundary step; reverse arcs are relaxed with a DSMEM 64-bit
+//     compare-and-swap min into the owner's keys (common.cuh: the generic 64-bit atomicMin is
+//     not atomic on remote shared memory); phase votes and the t* minimum are reduced from
+//     per-CTA slots read by every CTA (no remote atomics, no resets);
+//   * the forward relaxation also records the lowest arg-min source of every row, so the
+//     canonical predecessor of an in-node is one lookup (the row was last relaxed after the last
+//     change of its sources, dirty-stage tracking guarantees it);
+//   * the leader CTA traces the canonical path and augments; the arc lists stay in global memory
+//     and are only accessed through L2 (ld/st.global.cg): they are written by the leader's SM and
+//     read by the other SMs of the cluster, whose L1 would otherwise serve stale lines.
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gwtf {
+
+namespace {
+
+constexpr int CT = 256;  // threads per CTA
+constexpr int TR = 8;    // tile rows per bulk copy
+constexpr int NB = 3;    // copies in flight
+constexpr uint64_t INF = ~0ull;
+
+__host__ __device__ inline size_t al16c(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct Misc {  // per-CTA control block; the leader's copy is authoritative
+  int64_t F, cost;
+  uint64_t tpart[2], red64;
+  int32_t inst, A, status, pathlen;
+  uint32_t votes[2];  // alternating slots: a CTA is at most one phase ahead of the slowest
+  int32_t red32, pred;
+};
+
+struct ClLayout {
+  size_t misc, kin, kout, amin, g, capE, srcf, snkf, kbuf, ring, mbar, total;
+};
+__host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
+  ClLayout L;
+  const size_t R = (P.n + C - 1) / C, SR = (size_t)P.S * R;
+  size_t o = 0;
+  L.misc = o; o += al16c(sizeof(Misc));
+  L.mbar = o; o += al16c(NB * 8);
+  L.kin = o; o += al16c(SR * 8);
+  L.kout = o; o += al16c(SR * 8);
+  L.amin = o; o += al16c(SR * 2);
+  L.g = o; o += al16c(SR * 2);
+  L.capE = o; o += al16c(SR * 2);
+  L.srcf = o; o += al16c(R * 4);
+  L.snkf = o; o += al16c(R * 4);
+  L.kbuf = o; o += al16c((size_t)P.ld * 8);
+  L.ring = o; o += al16c((size_t)NB * TR * P.ld * 4);
+  L.total = o;
+  return L;
+}
+
+template <int C>
+__global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, const SspOut o) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int r = (int)cl.block_rank(), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cid = blockIdx.x / C;
+  const int S = P.S, n = P.n, ld = P.ld, Lt = 2 * S + 1, Lcap = P.Lcap;
+  const int R = (n + C - 1) / C, v0 = r * R, nr = max(0, min(R, n - v0));
+  const ClLayout L = cl_layout(P, C);
+  Misc* misc = (Misc*)(sm + L.misc);
+  uint64_t* mbar = (uint64_t*)(sm + L.mbar);
+  uint64_t* kin = (uint64_t*)(sm + L.kin);
+  uint64_t* kout = (uint64_t*)(sm + L.kout);
+  int16_t* amin = (int16_t*)(sm + L.amin);
+  int16_t* g = (int16_t*)(sm + L.g);
+  int16_t* capE = (int16_t*)(sm + L.capE);
+  int32_t* srcf = (int32_t*)(sm + L.srcf);
+  int32_t* snkf = (int32_t*)(sm + L.snkf);
+  uint64_t* kbuf = (uint64_t*)(sm + L.kbuf);
+  int32_t* ring = (int32_t*)(sm + L.ring);
+  Misc* M0 = cl.map_shared_rank(misc, 0);
+  uint32_t* path = (uint32_t*)(P.ws_cluster) + (size_t)cid * (2 * S * n + 4);
+  // remote views of the owners' arrays
+  auto own = [&](int v) { return v / R; };
+  auto rkin = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kin, q) + s * R + (v - q * R); };
+  auto rkout = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kout, q) + s * R + (v - q * R); };
+  auto rg = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
+  auto rcap = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(capE, q) + s * R + (v - q * R); };
+  auto ramin = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(amin, q) + s * R + (v - q * R); };
+  auto rsrcf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(srcf, q) + (v - q * R); };
+  auto rsnkf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(snkf, q) + (v - q * R); };
+
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], 1);
+    fence_barrier_init();
+  }
+  uint32_t ph = 0;        // parity bit per ring buffer (uniform over the CTA)
+  uint32_t vote_id = 0;   // phase counter of the votes (uniform over the cluster)
+  uint32_t tphase = 0;    // phase counter of the t* reductions
+  __syncthreads();
+
+  for (;;) {
+    if (r == 0 && tid == 0) misc->inst = atomicAdd(&P.counters[4], 1);
+    cl.sync();
+    const int inst = M0->inst;
+    cl.sync();  // every CTA has read the leader's value before any CTA exits or it is rewritten
+    if (inst >= P.B) break;
+    const int64_t M = P.supply[inst];
+    const int32_t* tile = P.tile + (size_t)inst * (S - 1) * n * ld;
+    const int32_t* src = P.src + (size_t)inst * n;
+    const int32_t* snk = P.snk + (size_t)inst * n;
+    uint32_t* arcs = P.arcs + (size_t)inst * (S - 1) * Lcap;
+    int32_t* cnt = P.arc_cnt + (size_t)inst * (S - 1);
+    for (int k = tid; k < S * R; k += CT) {
+      const int s = k / R, v = v0 + k % R;
+      g[k] = 0;
+      capE[k] = (v < n && P.alive[((size_t)inst * S + s) * n + v]) ? (int16_t)P.cap[((size_t)inst * S + s) * n + v] : 0;
+    }
+    for (int k = tid; k < R; k += CT) { srcf[k] = 0; snkf[k] = 0; }
+    if (r == 0) {
+      if (tid == 0) { misc->F = 0; misc->cost = 0; misc->A = 0; misc->status = 0; misc->votes[0] = 0; misc->votes[1] = 0; }
+      for (int k = tid; k < S - 1; k += CT) __stcg(&cnt[k], 0);
+    }
+    vote_id = 0;
+    cl.sync();
+
+    // vote: did any CTA of the cluster change something in this phase?  (cluster barrier)
+    auto vote = [&](int ch) -> bool {
+      const int any = __syncthreads_or(ch);
+      ++vote_id;
+      if (tid == 0) misc->votes[vote_id & 1] = any ? vote_id : 0u;  // own slot, double-buffered
+      cl.sync();
+      bool res = false;
+      for (int q = 0; q < C; ++q) res |= cl.map_shared_rank(misc, q)->votes[vote_id & 1] == vote_id;
+      return res;
+    };
+
+    for (;;) {  // successive shortest paths
+      const int64_t F = M0->F;
+      if (F >= M || M0->status) break;
+      for (int k = tid; k < S * R; k += CT) { kin[k] = INF; kout[k] = INF; amin[k] = -1; }
+      __syncthreads();
+      for (int lv = tid; lv < nr; lv += CT) {  // s* -> in_0, in_0 -> out_0
+        const int v = v0 + lv;
+        if (src[v] != kAbsent) {
+          const uint64_t c = ((uint64_t)(uint32_t)src[v] << kHopBits) | 1ull;
+          kin[lv] = c;
+          if (g[lv] < capE[lv]) kout[lv] = c + 1;
+        }
+      }
+      uint64_t tkey = INF;
+      uint64_t fwd = S > 1 ? 1ull : 0ull, bwd = 1ull;
+      bool tdirty = S == 1, trev = false;
+      cl.sync();
+      for (;;) {
+        // ---- forward: dense min-plus relaxation of the dirty boundaries (streamed tiles) ----
+        for (int s = 0; s + 1 < S; ++s) {
+          if (!((fwd >> s) & 1ull)) continue;
+          fwd &= ~(1ull << s);
+          if (r == 0 && tid == 0) atomicAdd(&P.stats[0], 1ull);
+          const int32_t* rows = tile + ((size_t)s * n + v0) * ld;
+          const int nch = (nr + TR - 1) / TR;
+          auto issue = [&](int k) {
+            const int b = k % NB;
+            const int rws = min(TR, nr - k * TR);
+            const uint32_t bytes = (uint32_t)rws * ld * 4;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&mbar[b], bytes);
+            bulk_g2s(ring + (size_t)b * TR * ld, rows + (size_t)k * TR * ld, bytes, &mbar[b]);
+          };
+          if (tid == 0)
+            for (int k = 0; k < min(NB, nch); ++k) issue(k);
+          for (int u = tid; u < ld; u += CT) kbuf[u] = u < n ? *rkout(s, u) : INF;  // gather out_s over DSMEM
+          __syncthreads();
+          int ch = 0;
+          for (int k = 0; k < nch; ++k) {
+            const int b = k % NB;
+            mbar_wait(&mbar[b], (ph >> b) & 1u);
+            ph ^= 1u << b;
+            const int rws = min(TR, nr - k * TR);
+            for (int lr = warp; lr < rws; lr += CT / 32) {
+              const int4* row = (const int4*)(ring + ((size_t)b * TR + lr) * ld);
+              uint64_t acc = INF;
+              int idx = -1;
+              for (int c = lane; c < ld / 4; c += 32) {
+                const int4 w = row[c];
+                const ulonglong2 k01 = *(const ulonglong2*)(kbuf + 4 * c);
+                const ulonglong2 k23 = *(const ulonglong2*)(kbuf + 4 * c + 2);
+                const int32_t ws[4] = {w.x, w.y, w.z, w.w};
+                const uint64_t ks[4] = {k01.x, k01.y, k23.x, k23.y};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  if (ws[q] == kAbsent || ks[q] == INF) continue;
+                  const uint64_t cand = ks[q] + ((uint64_t)(uint32_t)ws[q] << kHopBits) + 1ull;
+                  if (cand < acc) { acc = cand; idx = 4 * c + q; }
+                }
+              }
+              for (int off = 16; off > 0; off >>= 1) {  // lexicographic (value, lowest index) min
+                const uint64_t oa = __shfl_xor_sync(0xffffffffu, acc, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
+                if (oa < acc || (oa == acc && (unsigned)oi < (unsigned)idx)) { acc = oa; idx = oi; }
+              }
+              if (lane == 0) {
+                const int lv = k * TR + lr, e = (s + 1) * R + lv;
+                amin[e] = (int16_t)(acc == INF ? -1 : idx);
+                uint64_t kv = kin[e];
+                if (acc < kv) { kin[e] = acc; kv = acc; ch = 1; }
+                if (kv != INF && g[e] < capE[e] && kv + 1 < kout[e]) { kout[e] = kv + 1; ch = 1; }
+              }
+            }
+            __syncthreads();  // buffer b consumed
+            if (tid == 0 && k + NB < nch) issue(k + NB);
+          }
+          if (vote(ch)) {
+            if (s + 1 < S - 1) fwd |= 1ull << (s + 1);
+            else tdirty = true;
+            bwd |= 1ull << (s + 1);
+          }
+        }
+        // ---- out_{S-1} -> t* ----
+        if (tdirty) {
+          tdirty = false;
+          // every CTA publishes its partial minimum in its own slot (double-buffered by the
+          // phase parity), then every CTA reduces all C slots: no remote atomics, no resets
+          const int slot = (int)(++tphase & 1u);
+          if (tid == 0) misc->red64 = INF;
+          __syncthreads();
+          uint64_t tc = INF;
+          for (int lv = tid; lv < nr; lv += CT) {
+            const int v = v0 + lv;
+            const uint64_t k = kout[(S - 1) * R + lv];
+            if (snk[v] != kAbsent && k != INF) tc = umin64(tc, k + ((uint64_t)(uint32_t)snk[v] << kHopBits) + 1ull);
+          }
+          for (int off = 16; off > 0; off >>= 1)
+            tc = umin64(tc, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)tc, off));
+          if (lane == 0 && tc != INF) atomicMin((unsigned long long*)&misc->red64, (unsigned long long)tc);
+          __syncthreads();
+          if (tid == 0) misc->tpart[slot] = misc->red64;
+          cl.sync();
+          uint64_t tn = INF;
+          for (int q = 0; q < C; ++q) tn = umin64(tn, cl.map_shared_rank(misc, q)->tpart[slot]);
+          if (tn < tkey) { tkey = tn; trev = true; }
+        }
+        // ---- t* -> out_{S-1} (reverse sink arcs) ----
+        if (trev) {
+          trev = false;
+          int ch = 0;
+          if (tkey != INF)
+            for (int lv = tid; lv < nr; lv += CT) {
+              if (snkf[lv] <= 0) continue;
+              const int e = (S - 1) * R + lv;
+              const uint64_t c = tkey - ((uint64_t)(uint32_t)snk[v0 + lv] << kHopBits) + 1ull;
+              if (c < kout[e]) { kout[e] = c; ch = 1; }
+            }
+          if (vote(ch)) bwd |= 1ull << (S - 1);
+        }
+        // ---- backward: reverse node arcs (owners) + reverse inter-stage arcs (DSMEM atomicMin) ----
+        for (int s = S - 1; s >= 0; --s) {
+          if (!((bwd >> s) & 1ull)) continue;
+          bwd &= ~(1ull << s);
+          if (r == 0 && tid == 0) atomicAdd(&P.stats[1], 1ull);
+          for (int lv = tid; lv < nr; lv += CT) {
+            const int e = s * R + lv;
+            if (g[e] > 0 && kout[e] != INF && kout[e] + 1 < kin[e]) kin[e] = kout[e] + 1;
+          }
+          if (s == 0) { cl.sync(); break; }
+          const uint32_t* al = arcs + (size_t)(s - 1) * Lcap;
+          const int c = __ldcg(&cnt[s - 1]);
+          int ch = 0;
+          for (int e = r * CT + tid; e < c; e += C * CT) {
+            const uint32_t ent = __ldcg(&al[e]);
+            const int u = (int)(ent >> 20), v = (int)((ent >> 8) & 0xFFFu);
+            uint64_t ki = *rkin(s, v);
+            const uint64_t kov = *rkout(s, v);
+            if (*rg(s, v) > 0 && kov != INF && kov + 1 < ki) ki = kov + 1;
+            if (ki == INF) continue;
+            const int32_t w = tile[((size_t)(s - 1) * n + v) * ld + u];
+            const uint64_t cand = ki - ((uint64_t)(uint32_t)w << kHopBits) + 1ull;
+            const int q = own(u);
+            const uint64_t old = dsmem_atomic_min_u64(dsmem_addr(kout + (s - 1) * R + (u - q * R), (uint32_t)q), cand);
+            if (cand < old) ch = 1;
+          }
+          if (vote(ch)) {
+            fwd |= 1ull << (s - 1);
+            bwd |= 1ull << (s - 1);
+          }
+        }
+        if (r == 0 && tid == 0) atomicAdd(&P.stats[3], 1ull);
+        if (!(fwd | bwd) && !tdirty && !trev) break;
+      }
+      if (tkey == INF) break;  // t* unreachable: F is maximal
+      if ((P.debug & 8) && r == 0 && tid == 0) {  // testing: record the key of every augmenting path
+        const unsigned long long a = atomicAdd(&P.stats[10], 1ull);
+        if (a < 1000) P.stats[1000 + a] = tkey;
+      }
+      if ((P.debug & 4) && r == 0 && M0->A == (P.debug >> 8)) {  // testing: dump the converged keys
+        if (tid == 0) {
+          P.stats[8] = tkey;
+          for (int s2 = 0; s2 < S && 2 * S * n + 16 < 2000; ++s2)
+            for (int i = 0; i < n; ++i) {
+              P.stats[16 + (s2 * n + i) * 3 + 0] = *rkin(s2, i);
+              P.stats[16 + (s2 * n + i) * 3 + 1] = *rkout(s2, i);
+              P.stats[16 + (s2 * n + i) * 3 + 2] = (unsigned long long)*ramin(s2, i);
+            }
+          misc->status = 9;
+        }
+      }
+      if ((P.debug & 4) && M0->A == (P.debug >> 8)) { cl.sync(); break; }
+
+      // ---- trace the canonical augmenting path and augment (leader CTA) ----
+      if (r == 0) {
+        auto key_of = [&](int id) -> uint64_t {
+          const int l = id >> 16, p = id & 0xFFFF;
+          if (l == 0) return 0ull;
+          if (l == Lt) return tkey;
+          if (l & 1) return *rkin((l - 1) >> 1, p);
+          return *rkout((l >> 1) - 1, p);
+        };
+        int x = Lt << 16, len = 1, err = 0;
+        if (tid == 0) path[0] = (uint32_t)x;
+        while (x != 0) {
+          const int l = x >> 16, p = x & 0xFFFF;
+          const uint64_t kx = key_of(x);
+          if (tid == 0) misc->red32 = INT_MAX;
+          __syncthreads();
+          int pred = -1;
+          if (l == Lt) {  // lowest i with out_{S-1,i} + (snk_i, 1) == key(t*)
+            for (int i = tid; i < n; i += CT) {
+              if (snk[i] == kAbsent) continue;
+              const uint64_t k = *rkout(S - 1, i);
+              if (k != INF && k + ((uint64_t)(uint32_t)snk[i] << kHopBits) + 1ull == kx) { atomicMin(&misc->red32, i); break; }
+            }
+            __syncthreads();
+            if (misc->red32 != INT_MAX) pred = ((2 * S) << 16) | misc->red32;
+          } else if (l & 1) {  // in_{s,i}: s* / lowest tight out_{s-1,u} (recorded arg-min), then out_{s,i}
+            const int s = (l - 1) >> 1, i = p;
+            if (s == 0) {
+              if (src[i] != kAbsent && ((((uint64_t)(uint32_t)src[i]) << kHopBits) | 1ull) == kx) pred = 0;
+            } else {
+              const int u = *ramin(s, i);
+              if (u >= 0) {
+                const uint64_t k = *rkout(s - 1, u);
+                const int32_t w = tile[((size_t)(s - 1) * n + i) * ld + u];
+                if (k != INF && w != kAbsent && k + ((uint64_t)(uint32_t)w << kHopBits) + 1ull == kx)
+                  pred = ((2 * s) << 16) | u;
+              }
+            }
+            if (pred < 0) {
+              const uint64_t ko = *rkout(s, i);
+              if (*rg(s, i) > 0 && ko != INF && ko + 1 == kx) pred = ((2 * s + 2) << 16) | i;
+            }
+          } else {  // out_{s,i}: in_{s,i}, then lowest tight reverse in_{s+1,v}, then t*
+            const int s = (l >> 1) - 1, i = p;
+            const uint64_t ki = *rkin(s, i);
+            if (*rg(s, i) < *rcap(s, i) && ki != INF && ki + 1 == kx) {
+              pred = ((2 * s + 1) << 16) | i;
+            } else if (s < S - 1) {
+              const uint32_t* al = arcs + (size_t)s * Lcap;
+              const int c = __ldcg(&cnt[s]);
+              for (int e = tid; e < c; e += CT) {
+                const uint32_t ent = __ldcg(&al[e]);
+                if ((int)(ent >> 20) != i) continue;
+                const int v = (int)((ent >> 8) & 0xFFFu);
+                const uint64_t k = *rkin(s + 1, v);
+                const int32_t w = tile[((size_t)s * n + v) * ld + i];
+                if (k != INF && k + 1ull == kx + ((uint64_t)(uint32_t)w << kHopBits)) atomicMin(&misc->red32, v);
+              }
+              __syncthreads();
+              if (misc->red32 != INT_MAX) pred = ((2 * s + 3) << 16) | misc->red32;
+            } else if (*rsnkf(i) > 0 && tkey + 1ull == kx + ((uint64_t)(uint32_t)snk[i] << kHopBits)) {
+              pred = Lt << 16;
+            }
+          }
+          __syncthreads();
+          if (pred < 0 || len >= 2 * S * n + 2) {
+            if (tid == 0 && atomicCAS(&P.stats[9], 0ull, (unsigned long long)inst + 1) == 0ull) {
+              P.stats[5] = (unsigned long long)x; P.stats[6] = kx; P.stats[7] = (unsigned long long)len;
+              P.stats[8] = tkey;
+              for (int s2 = 0; s2 < S && 2 * S * n + 16 < 2000; ++s2)
+                for (int i = 0; i < n; ++i) {
+                  P.stats[16 + (s2 * n + i) * 3 + 0] = *rkin(s2, i);
+                  P.stats[16 + (s2 * n + i) * 3 + 1] = *rkout(s2, i);
+                  P.stats[16 + (s2 * n + i) * 3 + 2] = (unsigned long long)*rg(s2, i);
+                }
+            }
+            err = 1;
+            break;
+          }
+          if (tid == 0) path[len] = (uint32_t)pred;
+          ++len;
+          x = pred;
+        }
+        __syncthreads();
+        // bottleneck delta = min(M - F, residual capacities); arc e: path[len-1-e] -> path[len-2-e]
+        if (tid == 0) misc->red64 = err ? 0ull : (uint64_t)(M - F);
+        __syncthreads();
+        if (!err) {
+          for (int e = tid; e < len - 1; e += CT) {
+            const int u = (int)path[len - 1 - e], v = (int)path[len - 2 - e];
+            const int lu = u >> 16, lv = v >> 16, pu = u & 0xFFFF;
+            uint64_t rc = INF;
+            if (u == 0 || lv == Lt) {
+            } else if ((lu & 1) && lv == lu + 1) {
+              const int s = (lu - 1) >> 1;
+              rc = (uint64_t)(*rcap(s, pu) - *rg(s, pu));
+            } else if (!(lu & 1) && lv == lu - 1) {
+              rc = (uint64_t)*rg((lu >> 1) - 1, pu);
+            } else if ((lu & 1) && lv == lu - 1) {
+              rc = 1ull << 62;  // reverse inter-stage arc: looked up below
+            }
+            if (rc != INF && rc < (1ull << 62)) atomicMin((unsigned long long*)&misc->red64, (unsigned long long)rc);
+          }
+          __syncthreads();
+          for (int e = 0; e < len - 1; ++e) {  // reverse inter-stage arcs: f(u, v) from the list
+            const int u = (int)path[len - 1 - e], v = (int)path[len - 2 - e];
+            const int lu = u >> 16, lv = v >> 16;
+            if (!((lu & 1) && lv == lu - 1)) continue;
+            const int s = (lv >> 1) - 1;
+            const uint32_t key = ((uint32_t)(v & 0xFFFF) << 12) | (uint32_t)(u & 0xFFFF);
+            const uint32_t* al = arcs + (size_t)s * Lcap;
+            for (int q = tid; q < __ldcg(&cnt[s]); q += CT)
+              { const uint32_t ent = __ldcg(&al[q]); if ((ent >> 8) == key) atomicMin((unsigned long long*)&misc->red64, (unsigned long long)(ent & 0xFFu)); }
+            __syncthreads();
+          }
+        }
+        const long long d = (long long)misc->red64;
+        __syncthreads();
+        if (err || d <= 0) {
+          if (tid == 0) misc->status = err ? 1 : 4;
+        } else {
+          for (int e = 0; e < len - 1; ++e) {
+            const int u = (int)path[len - 1 - e], v = (int)path[len - 2 - e];
+            const int lu = u >> 16, lv = v >> 16, pu = u & 0xFFFF, pv = v & 0xFFFF;
+            if (u == 0) {
+              if (tid == 0) *rsrcf(pv) += (int32_t)d;
+            } else if (lv == Lt) {
+              if (tid == 0) *rsnkf(pu) += (int32_t)d;
+            } else if ((lu & 1) && lv == lu + 1) {
+              if (tid == 0) *rg((lu - 1) >> 1, pu) += (int16_t)d;
+            } else if (!(lu & 1) && lv == lu - 1) {
+              if (tid == 0) *rg((lu >> 1) - 1, pu) -= (int16_t)d;
+            } else {
+              const bool fwdarc = !(lu & 1);
+              const int s = fwdarc ? (lu >> 1) - 1 : (lv >> 1) - 1;
+              const uint32_t uu = fwdarc ? pu : pv, vv = fwdarc ? pv : pu;
+              const uint32_t key = (uu << 12) | vv;
+              uint32_t* al = arcs + (size_t)s * Lcap;
+              const int c = __ldcg(&cnt[s]);
+              if (tid == 0) misc->red32 = INT_MAX;
+              __syncthreads();
+              for (int q = tid; q < c; q += CT)
+                if ((__ldcg(&al[q]) >> 8) == key) atomicMin(&misc->red32, q);
+              __syncthreads();
+              if (tid == 0) {
+                const int found = misc->red32;
+                if (found != INT_MAX) {
+                  const int f = (int)(__ldcg(&al[found]) & 0xFFu) + (fwdarc ? (int)d : -(int)d);
+                  if (f > 0) {
+                    __stcg(&al[found], (uu << 20) | (vv << 8) | (uint32_t)f);
+                  } else {
+                    __stcg(&al[found], __ldcg(&al[c - 1]));
+                    __stcg(&cnt[s], c - 1);
+                  }
+                } else if (fwdarc && c < Lcap) {
+                  __stcg(&al[c], (uu << 20) | (vv << 8) | (uint32_t)d);
+                  __stcg(&cnt[s], c + 1);
+                } else {
+                  misc->status = 2;
+                }
+              }
+              __syncthreads();
+            }
+          }
+          if (tid == 0) {
+            misc->F = F + d;
+            misc->cost += (int64_t)d * (int64_t)(tkey >> kHopBits);
+            misc->A += 1;
+            atomicAdd(&P.stats[2], 1ull);
+            atomicAdd(&P.stats[4], (unsigned long long)len);
+          }
+        }
+      }
+      cl.sync();
+    }
+
+    // ---- results and the canonical assignment ----
+    if (r == 0 && tid == 0) {
+      o.F[inst] = misc->F;
+      o.cost[inst] = misc->cost;
+      if (o.A) o.A[inst] = misc->A;
+      if (o.status) o.status[inst] = misc->status;
+    }
+    for (int k = tid; k < S * R; k += CT) {
+      const int s = k / R, v = v0 + k % R;
+      if (v < n) P.g[((size_t)inst * S + s) * n + v] = g[k];
+    }
+    for (int lv = tid; lv < nr; lv += CT) {
+      P.src_f[(size_t)inst * n + v0 + lv] = srcf[lv];
+      P.snk_f[(size_t)inst * n + v0 + lv] = snkf[lv];
+    }
+    cl.sync();
+  }
+}
+
+template <int C>
+cudaError_t launch_c(const Problem& P, const SspOut& o, cudaStream_t st, int* nclusters_out, bool query) {
+  const size_t smem = cl_layout(P, C).total;
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  auto k = ssp_cluster_kernel<C>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (C > 8) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(CT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(C);
+  int ncl = 0;
+  e = cudaOccupancyMaxActiveClusters(&ncl, (void*)k, &cfg);
+  if (e != cudaSuccess) return e;
+  if (getenv("GWTF_DEBUG")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)k);
+    fprintf(stderr, "[gwtf] C=%d regs %d static smem %zu max dyn %d ptx %d -> clusters %d\n", C, fa.numRegs,
+            fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.ptxVersion, ncl);
+    for (size_t kb : {0, 64, 128, 160, 192, 200}) {
+      cudaLaunchConfig_t c2 = cfg;
+      c2.dynamicSmemBytes = kb * 1024;
+      int m = -1;
+      cudaError_t e2 = cudaOccupancyMaxActiveClusters(&m, (void*)k, &c2);
+      fprintf(stderr, "[gwtf]   dyn %zu KB -> %d (%s)\n", kb, m, cudaGetErrorString(e2));
+    }
+  }
+  if (ncl < 1) return cudaErrorInvalidConfiguration;
+  if (ncl > P.B) ncl = P.B;
+  if (nclusters_out) *nclusters_out = ncl;
+  if (query) return cudaSuccess;
+  if (ncl > P.ws_cluster_slots) ncl = P.ws_cluster_slots;  // path scratch slots
+  cfg.gridDim = dim3(ncl * C);
+  return cudaLaunchKernelEx(&cfg, k, P, o);
+}
+
+}  // namespace
+
+size_t ssp_cluster_smem_bytes(const Problem& P, int C) { return cl_layout(P, C).total; }
+
+// Largest cluster size (16, 8, 4, 2) whose per-CTA layout fits and that the device can host.
+int ssp_cluster_size(const Problem& P) {
+  for (int C : {16, 8, 4, 2}) {
+    if (P.n < C || cl_layout(P, C).total > 227 * 1024) continue;
+    int ncl = 0;
+    cudaError_t e;
+    if (C == 16) e = launch_c<16>(P, SspOut{}, nullptr, &ncl, true);
+    else if (C == 8) e = launch_c<8>(P, SspOut{}, nullptr, &ncl, true);
+    else if (C == 4) e = launch_c<4>(P, SspOut{}, nullptr, &ncl, true);
+    else e = launch_c<2>(P, SspOut{}, nullptr, &ncl, true);
+    if (getenv("GWTF_DEBUG"))
+      fprintf(stderr, "[gwtf] cluster size %d: smem %zu B, query %s, max active clusters %d\n", C,
+              cl_layout(P, C).total, cudaGetErrorString(e), ncl);
+    if (e == cudaSuccess && ncl >= 1) return C;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+cudaError_t launch_ssp_cluster(const Problem& P, const SspOut& o, cudaStream_t st, int C) {
+  cudaError_t e = cudaMemsetAsync(P.counters + 4, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
+  switch (C) {
+    case 16: return launch_c<16>(P, o, st, nullptr, false);
+    case 8: return launch_c<8>(P, o, st, nullptr, false);
+    case 4: return launch_c<4>(P, o, st, nullptr, false);
+    case 2: return launch_c<2>(P, o, st, nullptr, false);
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
+
+}  // namespace gwtf

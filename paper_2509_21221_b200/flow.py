@@ -76,7 +76,7 @@ class Flow:
 
     def __init__(self, cap, src_cost, snk_cost, link_cost, supply, *, max_cap, alive=None, seed=0, inst_base=0,
                  T0=1.7, alpha=0.95, objective=_lib.OBJ_SUM, steady_window=5, deny_after=3, stream=None,
-                 host=False, force_global_tier=False):
+                 host=False, force_global_tier=False, force_cluster_tier=False):
         B, S, n = cap.shape
         self.B, self.S, self.n, self.max_cap = B, S, n, max_cap
         self.host = host
@@ -106,7 +106,8 @@ class Flow:
         d.objective, d.steady_window, d.deny_after = objective, steady_window, deny_after
         d.device = self.device.index if self.device.index is not None else torch.cuda.current_device()
         d.stream = self.stream.cuda_stream
-        d.flags = (_lib.GWTF_HOST_PTRS if host else 0) | (_lib.GWTF_FORCE_GLOBAL_TIER if force_global_tier else 0)
+        d.flags = ((_lib.GWTF_HOST_PTRS if host else 0) | (_lib.GWTF_FORCE_GLOBAL_TIER if force_global_tier else 0)
+                   | (_lib.GWTF_FORCE_CLUSTER_TIER if force_cluster_tier else 0))
         h = ctypes.c_void_p()
         check("gwtf_flow_create", lib().gwtf_flow_create(ctypes.byref(d), ctypes.byref(h)))
         self.h = h
@@ -193,3 +194,13 @@ class Flow:
             self.h, names, ctypes.cast(ms, ctypes.c_void_p), ctypes.cast(nl, ctypes.c_void_p), cap,
             ctypes.cast(ctypes.byref(cnt), ctypes.c_void_p)))
         return {names[i].decode(): (ms[i], nl[i]) for i in range(min(cnt.value, cap))}
+
+    def stats(self, raw: bool = False):
+        """Exact-solve work counters since create (gwtf_flow_stats)."""
+        import numpy as np
+        out = np.zeros(2048, np.int64)
+        check("gwtf_flow_stats", lib().gwtf_flow_stats(self.h, out.ctypes.data, 2048))
+        if raw:
+            return out
+        keys = ("relax_steps", "backward_phases", "augmentations", "bf_passes", "path_nodes")
+        return {k: int(out[i]) for i, k in enumerate(keys)}

@@ -251,3 +251,33 @@ def test_full_size_bench_config_sampled():
         assert (int(rr.dec_flow[b]), int(rr.dec_cost[b]), int(rr.rounds_run[b])) == (
             int(o["F_dec"][0]), int(o["cost_dec"][0]), int(o["rounds"][0])), b
     assert (sol.status == 0).all()
+
+
+@pytest.mark.parametrize("name,B", [("gpt", 24), ("llama", 6), ("churn", 4), ("flow3", 16)])
+def test_cluster_tier_parity_forced(name, B):
+    """Instances forced through the thread-block-cluster tier (HBM-streamed tiles, DSMEM keys)."""
+    cfg = gen.CONFIGS[name]
+    fl, *_ = _gpu_flow(cfg, 0, B, force_cluster_tier=True)
+    sol = fl.solve_batch()
+    nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    for b in range(B):
+        r = _oracle_ssp(cfg, bt, src, snk, link, b)
+        assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), (name, b)
+        assert np.array_equal(nf[b], r.node_flow) and np.array_equal(af[b], r.arc_flow), (name, b)
+        assert np.array_equal(sf[b], r.src_flow) and np.array_equal(kf[b], r.snk_flow), (name, b)
+    assert (sol.status == 0).all()
+
+
+def test_cluster_tier_stress_scaled():
+    """The stress distributions at 8 x 256 (1.8 MB of tiles per instance): the cluster tier by size."""
+    cfg = gen.CONFIGS["stress_s"]
+    B = 4
+    fl, *_ = _gpu_flow(cfg, 0, B)
+    sol = fl.solve_batch()
+    nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    for b in range(B):
+        r = _oracle_ssp(cfg, bt, src, snk, link, b)
+        assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
+        assert np.array_equal(af[b], r.arc_flow) and np.array_equal(nf[b], r.node_flow), b
