@@ -11,15 +11,14 @@
 //     compare-and-swap min into the owner's keys (common.cuh: the generic 64-bit atomicMin is
 //     not atomic on remote shared memory); phase votes and the t* minimum are reduced from
 //     per-CTA slots read by every CTA (no remote atomics, no resets);
-//   * the forward relaxation also records the lowest arg-min source of every row, so the
-//     canonical predecessor of an in-node is one lookup (the row was last relaxed after the last
-//     change of its sources, dirty-stage tracking guarantees it);
 //   * the leader CTA traces the canonical path and augments; the arc lists stay in global memory
 //     and are only accessed through L2 (ld/st.global.cg): they are written by the leader's SM and
 //     read by the other SMs of the cluster, whose L1 would otherwise serve stale lines.
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -33,6 +32,7 @@ constexpr int CT = 256;  // threads per CTA
 constexpr int TR = 8;    // tile rows per bulk copy
 constexpr int NB = 3;    // copies in flight
 constexpr uint64_t INF = ~0ull;
+constexpr uint64_t kBig = 1ull << 62;  // INF inside the branch-free relaxation
 
 __host__ __device__ inline size_t al16c(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -45,7 +45,7 @@ struct Misc {  // per-CTA control block; the leader's copy is authoritative
 };
 
 struct ClLayout {
-  size_t misc, kin, kout, amin, g, capE, srcf, snkf, kbuf, ring, mbar, total;
+  size_t misc, kin, kout, g, capE, srcf, snkf, kbuf, ring, mbar, total;
 };
 __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   ClLayout L;
@@ -55,7 +55,6 @@ __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   L.mbar = o; o += al16c(NB * 8);
   L.kin = o; o += al16c(SR * 8);
   L.kout = o; o += al16c(SR * 8);
-  L.amin = o; o += al16c(SR * 2);
   L.g = o; o += al16c(SR * 2);
   L.capE = o; o += al16c(SR * 2);
   L.srcf = o; o += al16c(R * 4);
@@ -79,7 +78,6 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   uint64_t* mbar = (uint64_t*)(sm + L.mbar);
   uint64_t* kin = (uint64_t*)(sm + L.kin);
   uint64_t* kout = (uint64_t*)(sm + L.kout);
-  int16_t* amin = (int16_t*)(sm + L.amin);
   int16_t* g = (int16_t*)(sm + L.g);
   int16_t* capE = (int16_t*)(sm + L.capE);
   int32_t* srcf = (int32_t*)(sm + L.srcf);
@@ -94,7 +92,6 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   auto rkout = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kout, q) + s * R + (v - q * R); };
   auto rg = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
   auto rcap = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(capE, q) + s * R + (v - q * R); };
-  auto ramin = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(amin, q) + s * R + (v - q * R); };
   auto rsrcf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(srcf, q) + (v - q * R); };
   auto rsnkf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(snkf, q) + (v - q * R); };
 
@@ -146,7 +143,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
     for (;;) {  // successive shortest paths
       const int64_t F = M0->F;
       if (F >= M || M0->status) break;
-      for (int k = tid; k < S * R; k += CT) { kin[k] = INF; kout[k] = INF; amin[k] = -1; }
+      for (int k = tid; k < S * R; k += CT) { kin[k] = INF; kout[k] = INF; }
       __syncthreads();
       for (int lv = tid; lv < nr; lv += CT) {  // s* -> in_0, in_0 -> out_0
         const int v = v0 + lv;
@@ -178,7 +175,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           };
           if (tid == 0)
             for (int k = 0; k < min(NB, nch); ++k) issue(k);
-          for (int u = tid; u < ld; u += CT) kbuf[u] = u < n ? *rkout(s, u) : INF;  // gather out_s over DSMEM
+          for (int u = tid; u < ld; u += CT) {  // gather out_s over DSMEM (INF as kBig)
+            const uint64_t kk = u < n ? *rkout(s, u) : INF;
+            kbuf[u] = kk == INF ? kBig : kk;
+          }
           __syncthreads();
           int ch = 0;
           for (int k = 0; k < nch; ++k) {
@@ -187,30 +187,25 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             ph ^= 1u << b;
             const int rws = min(TR, nr - k * TR);
             for (int lr = warp; lr < rws; lr += CT / 32) {
+              // branch-free: keys are < 2^62 when finite (DESIGN.md 2.2 bound) and kBig = 2^62 stands
+              // for INF in kbuf, absent weights are INT32_MAX; no candidate can overflow 64 bits
               const int4* row = (const int4*)(ring + ((size_t)b * TR + lr) * ld);
-              uint64_t acc = INF;
-              int idx = -1;
+              uint64_t acc = kBig;
+#pragma unroll 2
               for (int c = lane; c < ld / 4; c += 32) {
                 const int4 w = row[c];
                 const ulonglong2 k01 = *(const ulonglong2*)(kbuf + 4 * c);
                 const ulonglong2 k23 = *(const ulonglong2*)(kbuf + 4 * c + 2);
-                const int32_t ws[4] = {w.x, w.y, w.z, w.w};
-                const uint64_t ks[4] = {k01.x, k01.y, k23.x, k23.y};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  if (ws[q] == kAbsent || ks[q] == INF) continue;
-                  const uint64_t cand = ks[q] + ((uint64_t)(uint32_t)ws[q] << kHopBits) + 1ull;
-                  if (cand < acc) { acc = cand; idx = 4 * c + q; }
-                }
+                acc = umin64(acc, k01.x + ((uint64_t)(uint32_t)w.x << kHopBits) + 1ull);
+                acc = umin64(acc, k01.y + ((uint64_t)(uint32_t)w.y << kHopBits) + 1ull);
+                acc = umin64(acc, k23.x + ((uint64_t)(uint32_t)w.z << kHopBits) + 1ull);
+                acc = umin64(acc, k23.y + ((uint64_t)(uint32_t)w.w << kHopBits) + 1ull);
               }
-              for (int off = 16; off > 0; off >>= 1) {  // lexicographic (value, lowest index) min
-                const uint64_t oa = __shfl_xor_sync(0xffffffffu, acc, off);
-                const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
-                if (oa < acc || (oa == acc && (unsigned)oi < (unsigned)idx)) { acc = oa; idx = oi; }
-              }
+              for (int off = 16; off > 0; off >>= 1)
+                acc = umin64(acc, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)acc, off));
               if (lane == 0) {
+                if (acc >= kBig) acc = INF;
                 const int lv = k * TR + lr, e = (s + 1) * R + lv;
-                amin[e] = (int16_t)(acc == INF ? -1 : idx);
                 uint64_t kv = kin[e];
                 if (acc < kv) { kin[e] = acc; kv = acc; ch = 1; }
                 if (kv != INF && g[e] < capE[e] && kv + 1 < kout[e]) { kout[e] = kv + 1; ch = 1; }
@@ -308,7 +303,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             for (int i = 0; i < n; ++i) {
               P.stats[16 + (s2 * n + i) * 3 + 0] = *rkin(s2, i);
               P.stats[16 + (s2 * n + i) * 3 + 1] = *rkout(s2, i);
-              P.stats[16 + (s2 * n + i) * 3 + 2] = (unsigned long long)*ramin(s2, i);
+              P.stats[16 + (s2 * n + i) * 3 + 2] = (unsigned long long)*rg(s2, i);
             }
           misc->status = 9;
         }
@@ -344,14 +339,16 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             const int s = (l - 1) >> 1, i = p;
             if (s == 0) {
               if (src[i] != kAbsent && ((((uint64_t)(uint32_t)src[i]) << kHopBits) | 1ull) == kx) pred = 0;
-            } else {
-              const int u = *ramin(s, i);
-              if (u >= 0) {
+            } else {  // lowest tight u of row i of boundary s-1 (block-parallel scan)
+              const int32_t* row = tile + ((size_t)(s - 1) * n + i) * ld;
+              for (int u = tid; u < n; u += CT) {
+                const int32_t w = row[u];
+                if (w == kAbsent) continue;
                 const uint64_t k = *rkout(s - 1, u);
-                const int32_t w = tile[((size_t)(s - 1) * n + i) * ld + u];
-                if (k != INF && w != kAbsent && k + ((uint64_t)(uint32_t)w << kHopBits) + 1ull == kx)
-                  pred = ((2 * s) << 16) | u;
+                if (k != INF && k + ((uint64_t)(uint32_t)w << kHopBits) + 1ull == kx) { atomicMin(&misc->red32, u); break; }
               }
+              __syncthreads();
+              if (misc->red32 != INT_MAX) pred = ((2 * s) << 16) | misc->red32;
             }
             if (pred < 0) {
               const uint64_t ko = *rkout(s, i);
@@ -562,23 +559,34 @@ cudaError_t launch_c(const Problem& P, const SspOut& o, cudaStream_t st, int* nc
 
 size_t ssp_cluster_smem_bytes(const Problem& P, int C) { return cl_layout(P, C).total; }
 
-// Largest cluster size (16, 8, 4, 2) whose per-CTA layout fits and that the device can host.
+// Cluster size: the largest number of SMs working at once, min(B, clusters the device can
+// host) x C, over the sizes whose per-CTA layout fits (ties -> larger C).  E.g. 8 stress
+// instances: 8 clusters of 14 CTAs run all instances at once, 7 clusters of 16 would need a
+// second wave for the 8th.
 int ssp_cluster_size(const Problem& P) {
-  for (int C : {16, 8, 4, 2}) {
+  int best = 0;
+  long long best_sms = 0;
+  for (int C : {16, 14, 12, 8, 4, 2}) {
     if (P.n < C || cl_layout(P, C).total > 227 * 1024) continue;
     int ncl = 0;
     cudaError_t e;
-    if (C == 16) e = launch_c<16>(P, SspOut{}, nullptr, &ncl, true);
-    else if (C == 8) e = launch_c<8>(P, SspOut{}, nullptr, &ncl, true);
-    else if (C == 4) e = launch_c<4>(P, SspOut{}, nullptr, &ncl, true);
-    else e = launch_c<2>(P, SspOut{}, nullptr, &ncl, true);
+    switch (C) {
+      case 16: e = launch_c<16>(P, SspOut{}, nullptr, &ncl, true); break;
+      case 14: e = launch_c<14>(P, SspOut{}, nullptr, &ncl, true); break;
+      case 12: e = launch_c<12>(P, SspOut{}, nullptr, &ncl, true); break;
+      case 8: e = launch_c<8>(P, SspOut{}, nullptr, &ncl, true); break;
+      case 4: e = launch_c<4>(P, SspOut{}, nullptr, &ncl, true); break;
+      default: e = launch_c<2>(P, SspOut{}, nullptr, &ncl, true); break;
+    }
     if (getenv("GWTF_DEBUG"))
       fprintf(stderr, "[gwtf] cluster size %d: smem %zu B, query %s, max active clusters %d\n", C,
               cl_layout(P, C).total, cudaGetErrorString(e), ncl);
-    if (e == cudaSuccess && ncl >= 1) return C;
-    cudaGetLastError();
+    if (e != cudaSuccess) { cudaGetLastError(); continue; }
+    const long long sms = (long long)std::min<long long>(ncl, P.B) * C;
+    if (ncl >= 1 && sms > best_sms) { best_sms = sms; best = C; }
   }
-  return 0;
+  if (const char* f = getenv("GWTF_CLUSTER_SIZE")) best = atoi(f);  // testing override
+  return best;
 }
 
 cudaError_t launch_ssp_cluster(const Problem& P, const SspOut& o, cudaStream_t st, int C) {
@@ -586,6 +594,8 @@ cudaError_t launch_ssp_cluster(const Problem& P, const SspOut& o, cudaStream_t s
   if (e != cudaSuccess) return e;
   switch (C) {
     case 16: return launch_c<16>(P, o, st, nullptr, false);
+    case 14: return launch_c<14>(P, o, st, nullptr, false);
+    case 12: return launch_c<12>(P, o, st, nullptr, false);
     case 8: return launch_c<8>(P, o, st, nullptr, false);
     case 4: return launch_c<4>(P, o, st, nullptr, false);
     case 2: return launch_c<2>(P, o, st, nullptr, false);
