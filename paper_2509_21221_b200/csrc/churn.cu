@@ -48,6 +48,7 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
     const int b = u[0], s = u[1], v = u[2], w = u[3], c = u[4];
     const bool cost_ok = c == kAbsent || (c >= 0 && c < (1 << 30));
     if (b < 0 || b >= P.B || !cost_ok) { atomicOr(bad, 1); continue; }
+    if (c != kAbsent) atomicMax(&P.counters[6], c);  // weight bound of the cluster tier's 32-bit keys
     if (s == -1) {
       if (v < 0 || v >= P.n) { atomicOr(bad, 1); continue; }
       P.src[(size_t)b * P.n + v] = c;

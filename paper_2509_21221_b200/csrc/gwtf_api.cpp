@@ -310,7 +310,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     if (P.cluster_size > 0) {
       P.ws_cluster_slots = (int32_t)std::min<int64_t>(h->num_sms / P.cluster_size, B);
       uint8_t* wc = nullptr;
-      if ((s = alloc(h, &wc, (size_t)P.ws_cluster_slots * (2 * Sn + 4) * 4)) != GWTF_OK) return bail(s);
+      if ((s = alloc(h, &wc, (size_t)P.ws_cluster_slots * 2 * (2 * Sn + 4) * 4)) != GWTF_OK) return bail(s);
       P.ws_cluster = wc;
     } else if (h->flags & GWTF_FORCE_CLUSTER_TIER) {
       return bail(fail(GWTF_E_UNSUPPORTED, "cluster tier unavailable for this shape"));
@@ -378,6 +378,10 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   if (link_tmp) {
     cudaFree(link_tmp);
     h->allocs.erase(std::find(h->allocs.begin(), h->allocs.end(), (void*)link_tmp));
+  }
+  {  // counters[6]: bound on the largest finite arc weight (raised by apply_churn's edge updates)
+    const int32_t mw = (int32_t)maxc;
+    CK(h, cudaMemcpyAsync(P.counters + 6, &mw, 4, cudaMemcpyHostToDevice, h->stream));
   }
   CK(h, launch_init_round_state(P, h->stream));
   CK(h, cudaMemsetAsync(P.stats, 0, 2048 * sizeof(unsigned long long), h->stream));

@@ -5,8 +5,9 @@
 //   * CTA r of the cluster owns destination rows v in [r*R, r*R+R) of every stage: their in/out
 //     keys, node flows and capacities live in its shared memory;
 //   * the dense min-plus relaxation of boundary s streams the CTA's R rows of tile s from HBM
-//     by TMA bulk copies (cp.async.bulk, TR rows per copy, NB copies in flight on an mbarrier
-//     ring) while the out_s key vector is gathered from the owner CTAs through DSMEM;
+//     by TMA bulk copies (cp.async.bulk, one row per copy, up to 32 rows in flight on an
+//     mbarrier ring; 32-bit DPX keys when the costs allow) while the out_s key vector is
+//     gathered from the owner CTAs through DSMEM;
 //   * one cluster barrier per boundary step; reverse arcs are relaxed with a DSMEM 64-bit
 //     compare-and-swap min into the owner's keys (common.cuh: the generic 64-bit atomicMin is
 //     not atomic on remote shared memory); phase votes and the t* minimum are reduced from
@@ -28,9 +29,10 @@ namespace gwtf {
 
 namespace {
 
-constexpr int CT = 256;  // threads per CTA
-constexpr int TR = 8;    // tile rows per bulk copy
-constexpr int NB = 3;    // copies in flight
+constexpr int CT = 256;      // threads per CTA
+constexpr int NW = CT / 32;  // warps per CTA: warp w relaxes rows w, w + NW, ... of a boundary
+constexpr int NBMAX = 32;    // row slots of the TMA ring (one 4*ld-byte row per bulk copy)
+constexpr size_t kSmemMax = 227 * 1024;
 constexpr uint64_t INF = ~0ull;
 constexpr uint64_t kBig = 1ull << 62;  // INF inside the branch-free relaxation
 
@@ -41,18 +43,19 @@ struct Misc {  // per-CTA control block; the leader's copy is authoritative
   uint64_t tpart[2], red64;
   int32_t inst, A, status, pathlen;
   uint32_t votes[2];  // alternating slots: a CTA is at most one phase ahead of the slowest
-  int32_t red32, pred;
+  int32_t red32, pred, nrem;
 };
 
 struct ClLayout {
-  size_t misc, kin, kout, g, capE, srcf, snkf, kbuf, ring, mbar, total;
+  size_t misc, kin, kout, g, capE, srcf, snkf, kbuf, kb32, aq, ring, mbar, total;
+  int nbr;  // row slots of the ring (power of two, >= NW)
 };
 __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   ClLayout L;
   const size_t R = (P.n + C - 1) / C, SR = (size_t)P.S * R;
   size_t o = 0;
   L.misc = o; o += al16c(sizeof(Misc));
-  L.mbar = o; o += al16c(NB * 8);
+  L.mbar = o; o += al16c(NBMAX * 8);
   L.kin = o; o += al16c(SR * 8);
   L.kout = o; o += al16c(SR * 8);
   L.g = o; o += al16c(SR * 2);
@@ -60,7 +63,12 @@ __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   L.srcf = o; o += al16c(R * 4);
   L.snkf = o; o += al16c(R * 4);
   L.kbuf = o; o += al16c((size_t)P.ld * 8);
-  L.ring = o; o += al16c((size_t)NB * TR * P.ld * 4);
+  L.kb32 = o; o += al16c((size_t)P.ld * 4);
+  L.aq = o; o += al16c((size_t)CT * 12);
+  // as many row slots in flight as fit (more bytes in flight per SM = closer to its HBM share)
+  L.nbr = NBMAX;
+  while (L.nbr > NW && o + (size_t)L.nbr * P.ld * 4 > kSmemMax) L.nbr >>= 1;
+  L.ring = o; o += al16c((size_t)L.nbr * P.ld * 4);
   L.total = o;
   return L;
 }
@@ -83,11 +91,22 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   int32_t* srcf = (int32_t*)(sm + L.srcf);
   int32_t* snkf = (int32_t*)(sm + L.snkf);
   uint64_t* kbuf = (uint64_t*)(sm + L.kbuf);
+  uint32_t* kb32 = (uint32_t*)(sm + L.kb32);
+  uint32_t* aq = (uint32_t*)(sm + L.aq);  // staged path arcs: list key, boundary, list length
   int32_t* ring = (int32_t*)(sm + L.ring);
+  const int nbr = L.nbr;
   Misc* M0 = cl.map_shared_rank(misc, 0);
-  uint32_t* path = (uint32_t*)(P.ws_cluster) + (size_t)cid * (2 * S * n + 4);
+  uint32_t* path = (uint32_t*)(P.ws_cluster) + (size_t)cid * 2 * (2 * S * n + 4);  // nodes t* -> s*
+  int32_t* found = (int32_t*)(path + (2 * S * n + 4));  // list index of path arc e (INT_MAX: none)
   // remote views of the owners' arrays
-  auto own = [&](int v) { return v / R; };
+  const uint64_t rmag = ((1ull << 32) + R - 1) / R;  // v / R == (v * rmag) >> 32 for v < 2^32 / R
+  auto own = [&](int v) { return (int)(((uint64_t)(uint32_t)v * rmag) >> 32); };
+  // 32-bit relaxation keys: (cost << H32) + hops + 1 with 2^H32 > 2Sn+2 hops; a
+  // boundary step uses them when every finite out-key cost plus the largest arc weight stays
+  // below T32, and absent weights / INF keys are clamped to T32 (never a minimum).
+  const int H32 = 32 - __clz(2 * S * n + 2);
+  const int CB32 = 32 - H32;
+  const uint32_t T32 = CB32 >= 4 ? (1u << (CB32 - 1)) - 1u : 0u;
   auto rkin = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kin, q) + s * R + (v - q * R); };
   auto rkout = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kout, q) + s * R + (v - q * R); };
   auto rg = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
@@ -96,10 +115,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   auto rsnkf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(snkf, q) + (v - q * R); };
 
   if (tid == 0) {
-    for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], 1);
+    for (int b = 0; b < nbr; ++b) mbar_init(&mbar[b], 1);
     fence_barrier_init();
   }
-  uint32_t ph = 0;        // parity bit per ring buffer (uniform over the CTA)
+  uint32_t seq = 0;       // rows streamed so far: row j of a step is ring use seq + j (uniform)
   uint32_t vote_id = 0;   // phase counter of the votes (uniform over the cluster)
   uint32_t tphase = 0;    // phase counter of the t* reductions
   __syncthreads();
@@ -111,6 +130,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
     cl.sync();  // every CTA has read the leader's value before any CTA exits or it is rewritten
     if (inst >= P.B) break;
     const int64_t M = P.supply[inst];
+    const int32_t maxw = *(volatile int32_t*)&P.counters[6];  // largest finite arc weight (bound)
     const int32_t* tile = P.tile + (size_t)inst * (S - 1) * n * ld;
     const int32_t* src = P.src + (size_t)inst * n;
     const int32_t* snk = P.snk + (size_t)inst * n;
@@ -164,32 +184,57 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           fwd &= ~(1ull << s);
           if (r == 0 && tid == 0) atomicAdd(&P.stats[0], 1ull);
           const int32_t* rows = tile + ((size_t)s * n + v0) * ld;
-          const int nch = (nr + TR - 1) / TR;
-          auto issue = [&](int k) {
-            const int b = k % NB;
-            const int rws = min(TR, nr - k * TR);
-            const uint32_t bytes = (uint32_t)rws * ld * 4;
+          const uint32_t rowbytes = (uint32_t)ld * 4;
+          // row j goes to slot (seq + j) % nbr; the warp that consumes row j refills its slot with
+          // row j + nbr, so nbr rows are always in flight and no CTA-wide barrier sits in the loop
+          auto issue = [&](int j) {
+            const int b = (int)((seq + (uint32_t)j) & (uint32_t)(nbr - 1));
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&mbar[b], bytes);
-            bulk_g2s(ring + (size_t)b * TR * ld, rows + (size_t)k * TR * ld, bytes, &mbar[b]);
+            mbar_arrive_expect_tx(&mbar[b], rowbytes);
+            bulk_g2s(ring + (size_t)b * ld, rows + (size_t)j * ld, rowbytes, &mbar[b]);
           };
           if (tid == 0)
-            for (int k = 0; k < min(NB, nch); ++k) issue(k);
-          for (int u = tid; u < ld; u += CT) {  // gather out_s over DSMEM (INF as kBig)
+            for (int j = 0; j < min(nbr, nr); ++j) issue(j);
+          const uint32_t lim = T32 > (uint32_t)maxw ? T32 - (uint32_t)maxw : 0u;
+          int wide = lim == 0u;
+          for (int u = tid; u < ld; u += CT) {  // gather out_s over DSMEM
             const uint64_t kk = u < n ? *rkout(s, u) : INF;
             kbuf[u] = kk == INF ? kBig : kk;
+            uint32_t k32 = T32 << H32;
+            if (kk != INF) {
+              const uint64_t c = kk >> kHopBits, hops = kk & ((1ull << kHopBits) - 1);
+              if (c >= lim || hops + 1 >= (1ull << H32)) wide = 1;
+              k32 = ((uint32_t)c << H32) + (uint32_t)hops + 1u;
+            }
+            kb32[u] = k32;
           }
-          __syncthreads();
+          wide = __syncthreads_or(wide);
           int ch = 0;
-          for (int k = 0; k < nch; ++k) {
-            const int b = k % NB;
-            mbar_wait(&mbar[b], (ph >> b) & 1u);
-            ph ^= 1u << b;
-            const int rws = min(TR, nr - k * TR);
-            for (int lr = warp; lr < rws; lr += CT / 32) {
-              // branch-free: keys are < 2^62 when finite (DESIGN.md 2.2 bound) and kBig = 2^62 stands
-              // for INF in kbuf, absent weights are INT32_MAX; no candidate can overflow 64 bits
-              const int4* row = (const int4*)(ring + ((size_t)b * TR + lr) * ld);
+          for (int j = warp; j < nr; j += NW) {
+            const uint32_t q = seq + (uint32_t)j;
+            const int b = (int)(q & (uint32_t)(nbr - 1));
+            mbar_wait(&mbar[b], (q / (uint32_t)nbr) & 1u);
+            const int4* row = (const int4*)(ring + (size_t)b * ld);
+            uint64_t best;
+            if (!wide) {
+              // 32-bit: per weight one clamp, one shift and one DPX add-min (VIADDMNMX)
+              const uint4* kv4 = (const uint4*)kb32;
+              uint32_t acc = 0xFFFFFFFFu;
+#pragma unroll 4
+              for (int c = lane; c < ld / 4; c += 32) {
+                const int4 w = row[c];
+                const uint4 kq = kv4[c];
+                acc = __viaddmin_u32(kq.x, min((uint32_t)w.x, T32) << H32, acc);
+                acc = __viaddmin_u32(kq.y, min((uint32_t)w.y, T32) << H32, acc);
+                acc = __viaddmin_u32(kq.z, min((uint32_t)w.z, T32) << H32, acc);
+                acc = __viaddmin_u32(kq.w, min((uint32_t)w.w, T32) << H32, acc);
+              }
+              acc = __reduce_min_sync(0xffffffffu, acc);
+              best = (acc >> H32) >= T32 ? INF
+                                         : ((uint64_t)(acc >> H32) << kHopBits) | (uint64_t)(acc & ((1u << H32) - 1u));
+            } else {
+              // 64-bit branch-free: keys are < 2^62 when finite (DESIGN.md 2.2 bound) and kBig =
+              // 2^62 stands for INF in kbuf, absent weights are INT32_MAX; nothing overflows
               uint64_t acc = kBig;
 #pragma unroll 2
               for (int c = lane; c < ld / 4; c += 32) {
@@ -203,17 +248,18 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               }
               for (int off = 16; off > 0; off >>= 1)
                 acc = umin64(acc, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)acc, off));
-              if (lane == 0) {
-                if (acc >= kBig) acc = INF;
-                const int lv = k * TR + lr, e = (s + 1) * R + lv;
-                uint64_t kv = kin[e];
-                if (acc < kv) { kin[e] = acc; kv = acc; ch = 1; }
-                if (kv != INF && g[e] < capE[e] && kv + 1 < kout[e]) { kout[e] = kv + 1; ch = 1; }
-              }
+              best = acc >= kBig ? INF : acc;
             }
-            __syncthreads();  // buffer b consumed
-            if (tid == 0 && k + NB < nch) issue(k + NB);
+            __syncwarp();  // every lane is done with slot b
+            if (lane == 0) {
+              if (j + nbr < nr) issue(j + nbr);
+              const int e = (s + 1) * R + j;
+              uint64_t kv = kin[e];
+              if (best < kv) { kin[e] = best; kv = best; ch = 1; }
+              if (kv != INF && g[e] < capE[e] && kv + 1 < kout[e]) { kout[e] = kv + 1; ch = 1; }
+            }
           }
+          seq += (uint32_t)nr;
           if (vote(ch)) {
             if (s + 1 < S - 1) fwd |= 1ull << (s + 1);
             else tdirty = true;
@@ -339,13 +385,20 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             const int s = (l - 1) >> 1, i = p;
             if (s == 0) {
               if (src[i] != kAbsent && ((((uint64_t)(uint32_t)src[i]) << kHopBits) | 1ull) == kx) pred = 0;
-            } else {  // lowest tight u of row i of boundary s-1 (block-parallel scan)
-              const int32_t* row = tile + ((size_t)(s - 1) * n + i) * ld;
-              for (int u = tid; u < n; u += CT) {
-                const int32_t w = row[u];
-                if (w == kAbsent) continue;
-                const uint64_t k = *rkout(s - 1, u);
-                if (k != INF && k + ((uint64_t)(uint32_t)w << kHopBits) + 1ull == kx) { atomicMin(&misc->red32, u); break; }
+            } else {  // lowest tight u of row i of boundary s-1: 4 weights and 4 out-keys per thread
+              const int4* row4 = (const int4*)(tile + ((size_t)(s - 1) * n + i) * ld);
+              for (int c = tid; c < ld / 4; c += CT) {
+                const int4 w4 = row4[c];
+                const int32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+                uint64_t k4[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) k4[j] = (ws[j] != kAbsent && 4 * c + j < n) ? *rkout(s - 1, 4 * c + j) : INF;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  if (k4[j] != INF && k4[j] + ((uint64_t)(uint32_t)ws[j] << kHopBits) + 1ull == kx) {
+                    atomicMin(&misc->red32, 4 * c + j);
+                    break;
+                  }
               }
               __syncthreads();
               if (misc->red32 != INT_MAX) pred = ((2 * s) << 16) | misc->red32;
@@ -396,7 +449,48 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           x = pred;
         }
         __syncthreads();
-        // bottleneck delta = min(M - F, residual capacities); arc e: path[len-1-e] -> path[len-2-e]
+        if (tid == 0) misc->pathlen = err ? -1 : len;
+        for (int e = tid; e < len - 1; e += CT) found[e] = INT_MAX;
+      }
+      cl.sync();
+
+      // ---- locate the path's inter-stage arcs in the positive-arc lists (whole cluster) ----
+      // arc e of the path is path[len-1-e] -> path[len-2-e]; the lists are scanned in parallel by
+      // all C * CT threads of the cluster, chunk by chunk of CT path arcs staged in shared memory
+      const int plen = M0->pathlen;
+      for (int e0 = 0; e0 < plen - 1; e0 += CT) {
+        const int ne = min(CT, plen - 1 - e0);
+        if (tid < ne) {
+          const int e = e0 + tid;
+          const int u = (int)__ldcg(&path[plen - 1 - e]), v = (int)__ldcg(&path[plen - 2 - e]);
+          const int lu = u >> 16, lv = v >> 16, pu = u & 0xFFFF, pv = v & 0xFFFF;
+          uint32_t key = 0xFFFFFFFFu;
+          int sb = 0, c = 0;
+          if (u != 0 && lv != Lt && ((!(lu & 1) && lv == lu + 1) || ((lu & 1) && lv == lu - 1))) {
+            const bool fwdarc = !(lu & 1);
+            sb = fwdarc ? (lu >> 1) - 1 : (lv >> 1) - 1;
+            key = fwdarc ? (((uint32_t)pu << 12) | (uint32_t)pv) : (((uint32_t)pv << 12) | (uint32_t)pu);
+            c = __ldcg(&cnt[sb]);
+          }
+          aq[3 * tid] = key; aq[3 * tid + 1] = (uint32_t)sb; aq[3 * tid + 2] = (uint32_t)c;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int t = 0; t < ne; ++t) {
+          const uint32_t key = aq[3 * t];
+          const int c = (int)aq[3 * t + 2];
+          const uint32_t* al = arcs + (size_t)aq[3 * t + 1] * Lcap;
+          for (int q = r * CT + tid; q < c; q += C * CT)
+            if ((__ldcg(&al[q]) >> 8) == key) atomicMin(&found[e0 + t], q);
+        }
+        __syncthreads();
+      }
+      cl.sync();
+
+      // ---- bottleneck and augmentation (leader CTA; a simple path touches every g, f_src,
+      // f_snk and list entry at most once, so all in-place updates run in parallel) ----
+      if (r == 0) {
+        const int len = plen, err = plen < 0;
         if (tid == 0) misc->red64 = err ? 0ull : (uint64_t)(M - F);
         __syncthreads();
         if (!err) {
@@ -410,72 +504,89 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               rc = (uint64_t)(*rcap(s, pu) - *rg(s, pu));
             } else if (!(lu & 1) && lv == lu - 1) {
               rc = (uint64_t)*rg((lu >> 1) - 1, pu);
-            } else if ((lu & 1) && lv == lu - 1) {
-              rc = 1ull << 62;  // reverse inter-stage arc: looked up below
+            } else if ((lu & 1) && lv == lu - 1) {  // reverse inter-stage arc: its flow
+              const int q = __ldcg(&found[e]);
+              rc = q == INT_MAX ? 0ull : (uint64_t)(__ldcg(&arcs[(size_t)((lv >> 1) - 1) * Lcap + q]) & 0xFFu);
             }
-            if (rc != INF && rc < (1ull << 62)) atomicMin((unsigned long long*)&misc->red64, (unsigned long long)rc);
-          }
-          __syncthreads();
-          for (int e = 0; e < len - 1; ++e) {  // reverse inter-stage arcs: f(u, v) from the list
-            const int u = (int)path[len - 1 - e], v = (int)path[len - 2 - e];
-            const int lu = u >> 16, lv = v >> 16;
-            if (!((lu & 1) && lv == lu - 1)) continue;
-            const int s = (lv >> 1) - 1;
-            const uint32_t key = ((uint32_t)(v & 0xFFFF) << 12) | (uint32_t)(u & 0xFFFF);
-            const uint32_t* al = arcs + (size_t)s * Lcap;
-            for (int q = tid; q < __ldcg(&cnt[s]); q += CT)
-              { const uint32_t ent = __ldcg(&al[q]); if ((ent >> 8) == key) atomicMin((unsigned long long*)&misc->red64, (unsigned long long)(ent & 0xFFu)); }
-            __syncthreads();
+            if (rc != INF) atomicMin((unsigned long long*)&misc->red64, (unsigned long long)rc);
           }
         }
+        __syncthreads();
         const long long d = (long long)misc->red64;
         __syncthreads();
         if (err || d <= 0) {
           if (tid == 0) misc->status = err ? 1 : 4;
         } else {
-          for (int e = 0; e < len - 1; ++e) {
-            const int u = (int)path[len - 1 - e], v = (int)path[len - 2 - e];
-            const int lu = u >> 16, lv = v >> 16, pu = u & 0xFFFF, pv = v & 0xFFFF;
-            if (u == 0) {
-              if (tid == 0) *rsrcf(pv) += (int32_t)d;
-            } else if (lv == Lt) {
-              if (tid == 0) *rsnkf(pu) += (int32_t)d;
-            } else if ((lu & 1) && lv == lu + 1) {
-              if (tid == 0) *rg((lu - 1) >> 1, pu) += (int16_t)d;
-            } else if (!(lu & 1) && lv == lu - 1) {
-              if (tid == 0) *rg((lu >> 1) - 1, pu) -= (int16_t)d;
-            } else {
-              const bool fwdarc = !(lu & 1);
-              const int s = fwdarc ? (lu >> 1) - 1 : (lv >> 1) - 1;
-              const uint32_t uu = fwdarc ? pu : pv, vv = fwdarc ? pv : pu;
-              const uint32_t key = (uu << 12) | vv;
-              uint32_t* al = arcs + (size_t)s * Lcap;
-              const int c = __ldcg(&cnt[s]);
-              if (tid == 0) misc->red32 = INT_MAX;
-              __syncthreads();
-              for (int q = tid; q < c; q += CT)
-                if ((__ldcg(&al[q]) >> 8) == key) atomicMin(&misc->red32, q);
-              __syncthreads();
-              if (tid == 0) {
-                const int found = misc->red32;
-                if (found != INT_MAX) {
-                  const int f = (int)(__ldcg(&al[found]) & 0xFFu) + (fwdarc ? (int)d : -(int)d);
+          // (1) node arcs, source/sink arcs and list entries whose flow stays positive; entries
+          // whose flow drops to zero are collected and (2) leave their list one by one (swap with
+          // the last entry).  A removal moves another entry, so every index is re-checked.
+          auto locate = [&](const uint32_t* al, int sb, int q, uint32_t key) -> int {
+            const int c = __ldcg(&cnt[sb]);
+            if (q < c && (__ldcg(&al[q]) >> 8) == key) return q;
+            for (int k = 0; k < c; ++k)
+              if ((__ldcg(&al[k]) >> 8) == key) return k;
+            return -1;
+          };
+          for (int e0 = 0; e0 < len - 1; e0 += CT) {
+            if (tid == 0) misc->nrem = 0;
+            __syncthreads();
+            const int e = e0 + tid;
+            if (e < len - 1) {
+              const int u = (int)path[len - 1 - e], v = (int)path[len - 2 - e];
+              const int lu = u >> 16, lv = v >> 16, pu = u & 0xFFFF, pv = v & 0xFFFF;
+              if (u == 0) {
+                *rsrcf(pv) += (int32_t)d;
+              } else if (lv == Lt) {
+                *rsnkf(pu) += (int32_t)d;
+              } else if ((lu & 1) && lv == lu + 1) {
+                *rg((lu - 1) >> 1, pu) += (int16_t)d;
+              } else if (!(lu & 1) && lv == lu - 1) {
+                *rg((lu >> 1) - 1, pu) -= (int16_t)d;
+              } else {
+                const bool fwdarc = !(lu & 1);
+                const int sb = fwdarc ? (lu >> 1) - 1 : (lv >> 1) - 1;
+                const uint32_t key = fwdarc ? (((uint32_t)pu << 12) | (uint32_t)pv) : (((uint32_t)pv << 12) | (uint32_t)pu);
+                uint32_t* al = arcs + (size_t)sb * Lcap;
+                int q = __ldcg(&found[e]);
+                if (q != INT_MAX) q = locate(al, sb, q, key);
+                if (q >= 0 && q != INT_MAX) {
+                  const uint32_t ent = __ldcg(&al[q]);
+                  const int f = (int)(ent & 0xFFu) + (fwdarc ? (int)d : -(int)d);
                   if (f > 0) {
-                    __stcg(&al[found], (uu << 20) | (vv << 8) | (uint32_t)f);
+                    __stcg(&al[q], (ent & ~0xFFu) | (uint32_t)f);
                   } else {
-                    __stcg(&al[found], __ldcg(&al[c - 1]));
-                    __stcg(&cnt[s], c - 1);
+                    const int k = atomicAdd(&misc->nrem, 1);
+                    aq[3 * k] = key; aq[3 * k + 1] = (uint32_t)sb; aq[3 * k + 2] = (uint32_t)q;
                   }
-                } else if (fwdarc && c < Lcap) {
-                  __stcg(&al[c], (uu << 20) | (vv << 8) | (uint32_t)d);
-                  __stcg(&cnt[s], c + 1);
-                } else {
+                } else if (!fwdarc || q < 0) {
                   misc->status = 2;
                 }
               }
-              __syncthreads();
             }
+            __syncthreads();
+            if (tid == 0)
+              for (int k = 0; k < misc->nrem; ++k) {
+                const int sb = (int)aq[3 * k + 1];
+                uint32_t* al = arcs + (size_t)sb * Lcap;
+                const int q = locate(al, sb, (int)aq[3 * k + 2], aq[3 * k]);
+                if (q < 0) { misc->status = 2; continue; }
+                const int c = __ldcg(&cnt[sb]);
+                __stcg(&al[q], __ldcg(&al[c - 1]));
+                __stcg(&cnt[sb], c - 1);
+              }
+            __syncthreads();
           }
+          // (3) new positive arcs are appended (parallel, one atomic slot each)
+          for (int e = tid; e < len - 1; e += CT) {
+            const int u = (int)path[len - 1 - e], v = (int)path[len - 2 - e];
+            const int lu = u >> 16, lv = v >> 16, pu = u & 0xFFFF, pv = v & 0xFFFF;
+            if (u == 0 || lv == Lt || !(!(lu & 1) && lv == lu + 1) || __ldcg(&found[e]) != INT_MAX) continue;
+            const int sb = (lu >> 1) - 1;
+            const int q = atomicAdd(&cnt[sb], 1);
+            if (q < Lcap) __stcg(&arcs[(size_t)sb * Lcap + q], ((uint32_t)pu << 20) | ((uint32_t)pv << 8) | (uint32_t)d);
+            else misc->status = 2;
+          }
+          __syncthreads();
           if (tid == 0) {
             misc->F = F + d;
             misc->cost += (int64_t)d * (int64_t)(tkey >> kHopBits);
@@ -510,7 +621,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
 template <int C>
 cudaError_t launch_c(const Problem& P, const SspOut& o, cudaStream_t st, int* nclusters_out, bool query) {
   const size_t smem = cl_layout(P, C).total;
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  if (smem > kSmemMax) return cudaErrorInvalidConfiguration;
   auto k = ssp_cluster_kernel<C>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -538,13 +649,6 @@ cudaError_t launch_c(const Problem& P, const SspOut& o, cudaStream_t st, int* nc
     cudaFuncGetAttributes(&fa, (const void*)k);
     fprintf(stderr, "[gwtf] C=%d regs %d static smem %zu max dyn %d ptx %d -> clusters %d\n", C, fa.numRegs,
             fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.ptxVersion, ncl);
-    for (size_t kb : {0, 64, 128, 160, 192, 200}) {
-      cudaLaunchConfig_t c2 = cfg;
-      c2.dynamicSmemBytes = kb * 1024;
-      int m = -1;
-      cudaError_t e2 = cudaOccupancyMaxActiveClusters(&m, (void*)k, &c2);
-      fprintf(stderr, "[gwtf]   dyn %zu KB -> %d (%s)\n", kb, m, cudaGetErrorString(e2));
-    }
   }
   if (ncl < 1) return cudaErrorInvalidConfiguration;
   if (ncl > P.B) ncl = P.B;
@@ -559,31 +663,32 @@ cudaError_t launch_c(const Problem& P, const SspOut& o, cudaStream_t st, int* nc
 
 size_t ssp_cluster_smem_bytes(const Problem& P, int C) { return cl_layout(P, C).total; }
 
-// Cluster size: the largest number of SMs working at once, min(B, clusters the device can
-// host) x C, over the sizes whose per-CTA layout fits (ties -> larger C).  E.g. 8 stress
-// instances: 8 clusters of 14 CTAs run all instances at once, 7 clusters of 16 would need a
-// second wave for the 8th.
+// Cluster size: the smallest estimated makespan, waves x per-CTA rows, where waves =
+// ceil(B / clusters the device hosts at once) and a CTA's step time grows with its R = n / C
+// destination rows plus a fixed barrier/gather overhead (~16 rows).  E.g. 8 stress instances:
+// clusters of 16 CTAs fit 7 at a time (2 waves), clusters of 10 fit all 8 (1 wave).
 int ssp_cluster_size(const Problem& P) {
   int best = 0;
-  long long best_sms = 0;
-  for (int C : {16, 14, 12, 8, 4, 2}) {
-    if (P.n < C || cl_layout(P, C).total > 227 * 1024) continue;
+  long long best_cost = 0;
+  for (int C : {16, 12, 10, 8, 4, 2}) {
+    if (P.n < C || cl_layout(P, C).total > kSmemMax) continue;
     int ncl = 0;
     cudaError_t e;
     switch (C) {
       case 16: e = launch_c<16>(P, SspOut{}, nullptr, &ncl, true); break;
-      case 14: e = launch_c<14>(P, SspOut{}, nullptr, &ncl, true); break;
       case 12: e = launch_c<12>(P, SspOut{}, nullptr, &ncl, true); break;
+      case 10: e = launch_c<10>(P, SspOut{}, nullptr, &ncl, true); break;
       case 8: e = launch_c<8>(P, SspOut{}, nullptr, &ncl, true); break;
       case 4: e = launch_c<4>(P, SspOut{}, nullptr, &ncl, true); break;
       default: e = launch_c<2>(P, SspOut{}, nullptr, &ncl, true); break;
     }
     if (getenv("GWTF_DEBUG"))
-      fprintf(stderr, "[gwtf] cluster size %d: smem %zu B, query %s, max active clusters %d\n", C,
-              cl_layout(P, C).total, cudaGetErrorString(e), ncl);
-    if (e != cudaSuccess) { cudaGetLastError(); continue; }
-    const long long sms = (long long)std::min<long long>(ncl, P.B) * C;
-    if (ncl >= 1 && sms > best_sms) { best_sms = sms; best = C; }
+      fprintf(stderr, "[gwtf] cluster size %d: smem %zu B, ring %d rows, query %s, max active clusters %d\n", C,
+              cl_layout(P, C).total, cl_layout(P, C).nbr, cudaGetErrorString(e), ncl);
+    if (e != cudaSuccess || ncl < 1) { cudaGetLastError(); continue; }
+    const long long waves = (P.B + ncl - 1) / ncl;
+    const long long cost = waves * ((P.n + C - 1) / C + 16);
+    if (best == 0 || cost < best_cost) { best_cost = cost; best = C; }
   }
   if (const char* f = getenv("GWTF_CLUSTER_SIZE")) best = atoi(f);  // testing override
   return best;
@@ -594,8 +699,8 @@ cudaError_t launch_ssp_cluster(const Problem& P, const SspOut& o, cudaStream_t s
   if (e != cudaSuccess) return e;
   switch (C) {
     case 16: return launch_c<16>(P, o, st, nullptr, false);
-    case 14: return launch_c<14>(P, o, st, nullptr, false);
     case 12: return launch_c<12>(P, o, st, nullptr, false);
+    case 10: return launch_c<10>(P, o, st, nullptr, false);
     case 8: return launch_c<8>(P, o, st, nullptr, false);
     case 4: return launch_c<4>(P, o, st, nullptr, false);
     case 2: return launch_c<2>(P, o, st, nullptr, false);

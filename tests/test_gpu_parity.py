@@ -253,9 +253,13 @@ def test_full_size_bench_config_sampled():
     assert (sol.status == 0).all()
 
 
-@pytest.mark.parametrize("name,B", [("gpt", 24), ("llama", 6), ("churn", 4), ("flow3", 16)])
-def test_cluster_tier_parity_forced(name, B):
-    """Instances forced through the thread-block-cluster tier (HBM-streamed tiles, DSMEM keys)."""
+@pytest.mark.parametrize("name,B,C", [("gpt", 24, None), ("gpt", 24, 16), ("gpt", 24, 8), ("llama", 6, None),
+                                      ("churn", 4, None), ("churn", 4, 16), ("flow3", 16, None)])
+def test_cluster_tier_parity_forced(name, B, C, monkeypatch):
+    """Instances forced through the thread-block-cluster tier (HBM-streamed tiles, DSMEM keys), with
+    the automatic cluster size and with pinned ones (R = n / C destination rows per CTA)."""
+    if C is not None:
+        monkeypatch.setenv("GWTF_CLUSTER_SIZE", str(C))
     cfg = gen.CONFIGS[name]
     fl, *_ = _gpu_flow(cfg, 0, B, force_cluster_tier=True)
     sol = fl.solve_batch()
@@ -266,6 +270,26 @@ def test_cluster_tier_parity_forced(name, B):
         assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), (name, b)
         assert np.array_equal(nf[b], r.node_flow) and np.array_equal(af[b], r.arc_flow), (name, b)
         assert np.array_equal(sf[b], r.src_flow) and np.array_equal(kf[b], r.snk_flow), (name, b)
+    assert (sol.status == 0).all()
+
+
+def test_cluster_tier_wide_keys():
+    """Arc weights too large for the cluster tier's 32-bit relaxation keys (every boundary step
+    takes the 64-bit path): link costs scaled by 2^16, still exact."""
+    from paper_2509_21221_b200 import Flow
+    cfg = gen.CONFIGS["churn"]
+    B = 4
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    big = np.where(link == gen.ABSENT, link, link.astype(np.int64) * 65536).astype(np.int32)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    fl = Flow(dev(bt.cap), dev(src), dev(snk), dev(big), dev(bt.supply), max_cap=cfg.max_cap,
+              alive=dev(bt.alive), force_cluster_tier=True)
+    sol = fl.solve_batch()
+    nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+    for b in range(B):
+        r = _oracle_ssp(cfg, bt, src, snk, big, b)
+        assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
+        assert np.array_equal(nf[b], r.node_flow) and np.array_equal(af[b], r.arc_flow), b
     assert (sol.status == 0).all()
 
 
