@@ -27,6 +27,18 @@ __global__ void pad_tiles_kernel(const Problem P, const int32_t* __restrict__ li
   }
 }
 
+// 16-bit copy of the padded tiles for the cluster tier's streamed relaxation (half the HBM bytes)
+__global__ void pack_tile16_kernel(const Problem P) {
+  const size_t rows = (size_t)P.B * (P.S - 1) * P.n;
+  const size_t total = rows * P.ld16;
+  for (size_t t = gtid(); t < total; t += gstride()) {
+    const size_t row = t / P.ld16;
+    const int c = (int)(t % P.ld16);
+    const int32_t v = c < P.n ? P.tile[row * P.ld + c] : kAbsent;
+    P.tile16[t] = v == kAbsent || v >= 0xFFFF ? (uint16_t)0xFFFFu : (uint16_t)v;
+  }
+}
+
 // max finite value and min value of an int32 array (validation of costs / capacities)
 __global__ void scan_kernel(const int32_t* __restrict__ v, int64_t count, int32_t* out_max, int32_t* out_min) {
   int mx = INT_MIN, mn = INT_MAX;
@@ -57,6 +69,10 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
       P.snk[(size_t)b * P.n + w] = c;
     } else if (s >= 0 && s < P.S - 1 && v >= 0 && v < P.n && w >= 0 && w < P.n) {
       P.tile[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld + w] = c;
+      if (P.tile16) {  // the cluster tier's 16-bit copy; a finite cost >= 0xFFFF retires it (bit 2)
+        if (c != kAbsent && c >= 0xFFFF) atomicOr(bad, 2);
+        P.tile16[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld16 + w] = c == kAbsent || c >= 0xFFFF ? 0xFFFFu : (uint16_t)c;
+      }
     } else {
       atomicOr(bad, 1);
     }
@@ -176,6 +192,12 @@ __global__ void eq1_kernel(int32_t B, int32_t S, int32_t n, int32_t L, const int
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st) {
   const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld;
   if (total) pad_tiles_kernel<<<grid_for(total), 256, 0, st>>>(P, link);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_tile16(const Problem& P, cudaStream_t st) {
+  const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld16;
+  if (total && P.tile16) pack_tile16_kernel<<<grid_for(total), 256, 0, st>>>(P);
   return cudaGetLastError();
 }
 

@@ -379,6 +379,11 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     cudaFree(link_tmp);
     h->allocs.erase(std::find(h->allocs.begin(), h->allocs.end(), (void*)link_tmp));
   }
+  if (P.cluster_size > 0 && nb && maxc < 0xFFFF && !getenv("GWTF_NO_TILE16")) {  // 16-bit tile copy streamed by the cluster tier
+    P.ld16 = (int32_t)((n + 7) / 8 * 8);
+    if ((s = alloc(h, &P.tile16, B * nb * n * P.ld16, true)) != GWTF_OK) return bail(s);
+    CK(h, launch_pack_tile16(P, h->stream));
+  }
   {  // counters[6]: bound on the largest finite arc weight (raised by apply_churn's edge updates)
     const int32_t mw = (int32_t)maxc;
     CK(h, cudaMemcpyAsync(P.counters + 6, &mw, 4, cudaMemcpyHostToDevice, h->stream));
@@ -463,7 +468,8 @@ gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const
     int32_t bad = 0;
     CK(h, cudaMemcpyAsync(&bad, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
-    if (bad) return fail(GWTF_E_INVALID, "edge update out of range (valid updates were applied)");
+    if (bad & 2) h->P.tile16 = nullptr;  // a cost no longer fits 16 bits: stream the int32 tiles
+    if (bad & 1) return fail(GWTF_E_INVALID, "edge update out of range (valid updates were applied)");
   }
   return GWTF_OK;
 }

@@ -16,6 +16,9 @@ struct Problem {
   int64_t Mmax;                // max supply over the batch (SRC/SNK slot arrays)
   int32_t Lcap;                // positive-arc list capacity per boundary
   int32_t* tile;               // [B][S-1][n][ld] dest-major, padding = kAbsent
+  uint16_t* tile16;            // cluster tier: [B][S-1][n][ld16] copy of tile, 0xFFFF = absent/padding
+                               // (nullptr when some cost >= 0xFFFF or the tier is unused)
+  int32_t ld16;                // n rounded up to 8
   int32_t* src;                // [B][n]
   int32_t* snk;                // [B][n]
   int32_t* cap;                // [B][S][n]
@@ -89,6 +92,7 @@ cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st);
 cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32_t* upd, int64_t k,
                          int32_t* bad_flag, cudaStream_t st);
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st);
+cudaError_t launch_pack_tile16(const Problem& P, cudaStream_t st);
 cudaError_t launch_dense_arcs(const Problem& P, int32_t* dense, cudaStream_t st);
 cudaError_t launch_eq1(int32_t B, int32_t S, int32_t n, int32_t L, const int32_t* comp, const int32_t* loc,
                        const int32_t* dloc, const int32_t* lat, const int32_t* bw, int64_t size_kbit,

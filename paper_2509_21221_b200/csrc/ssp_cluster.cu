@@ -29,9 +29,9 @@ namespace gwtf {
 
 namespace {
 
-constexpr int CT = 256;      // threads per CTA
+constexpr int CT = 512;      // threads per CTA
 constexpr int NW = CT / 32;  // warps per CTA: warp w relaxes rows w, w + NW, ... of a boundary
-constexpr int NBMAX = 32;    // row slots of the TMA ring (one 4*ld-byte row per bulk copy)
+constexpr int NBMAX = 64;    // row slots of the TMA ring (one row per bulk copy)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr uint64_t INF = ~0ull;
 constexpr uint64_t kBig = 1ull << 62;  // INF inside the branch-free relaxation
@@ -62,13 +62,15 @@ __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   L.capE = o; o += al16c(SR * 2);
   L.srcf = o; o += al16c(R * 4);
   L.snkf = o; o += al16c(R * 4);
-  L.kbuf = o; o += al16c((size_t)P.ld * 8);
-  L.kb32 = o; o += al16c((size_t)P.ld * 4);
+  const size_t ldk = P.tile16 ? P.ld16 : P.ld;                     // key-vector length
+  const size_t slot = P.tile16 ? (size_t)P.ld16 * 2 : (size_t)P.ld * 4;  // bytes per streamed row
+  L.kbuf = o; o += al16c(ldk * 8);
+  L.kb32 = o; o += al16c(ldk * 4);
   L.aq = o; o += al16c((size_t)CT * 12);
   // as many row slots in flight as fit (more bytes in flight per SM = closer to its HBM share)
   L.nbr = NBMAX;
-  while (L.nbr > NW && o + (size_t)L.nbr * P.ld * 4 > kSmemMax) L.nbr >>= 1;
-  L.ring = o; o += al16c((size_t)L.nbr * P.ld * 4);
+  while (L.nbr > NW && o + (size_t)L.nbr * slot > kSmemMax) L.nbr >>= 1;
+  L.ring = o; o += al16c((size_t)L.nbr * slot);
   L.total = o;
   return L;
 }
@@ -93,8 +95,12 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   uint64_t* kbuf = (uint64_t*)(sm + L.kbuf);
   uint32_t* kb32 = (uint32_t*)(sm + L.kb32);
   uint32_t* aq = (uint32_t*)(sm + L.aq);  // staged path arcs: list key, boundary, list length
-  int32_t* ring = (int32_t*)(sm + L.ring);
+  uint8_t* ring = sm + L.ring;
   const int nbr = L.nbr;
+  // streamed rows: the 16-bit tile copy when present (half the bytes), else the int32 tiles
+  const bool t16 = P.tile16 != nullptr;
+  const int ldk = t16 ? P.ld16 : ld;  // weights per streamed row
+  const uint32_t rowbytes = t16 ? (uint32_t)P.ld16 * 2 : (uint32_t)ld * 4;
   Misc* M0 = cl.map_shared_rank(misc, 0);
   uint32_t* path = (uint32_t*)(P.ws_cluster) + (size_t)cid * 2 * (2 * S * n + 4);  // nodes t* -> s*
   int32_t* found = (int32_t*)(path + (2 * S * n + 4));  // list index of path arc e (INT_MAX: none)
@@ -106,7 +112,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   // below T32, and absent weights / INF keys are clamped to T32 (never a minimum).
   const int H32 = 32 - __clz(2 * S * n + 2);
   const int CB32 = 32 - H32;
-  const uint32_t T32 = CB32 >= 4 ? (1u << (CB32 - 1)) - 1u : 0u;
+  const uint32_t T32 = CB32 >= 4 ? min((1u << (CB32 - 1)) - 1u, t16 ? 0xFFFFu : 0xFFFFFFFFu) : 0u;
+  const uint32_t T2 = T32 | (T32 << 16);  // per-halfword clamp of the 16-bit rows
   auto rkin = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kin, q) + s * R + (v - q * R); };
   auto rkout = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kout, q) + s * R + (v - q * R); };
   auto rg = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
@@ -118,6 +125,16 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
     for (int b = 0; b < nbr; ++b) mbar_init(&mbar[b], 1);
     fence_barrier_init();
   }
+  // testing (GWTF_DEBUG_FLAGS & 16): leader-thread cycle counts per phase into stats[1100 + k]
+  unsigned long long tlast = clock64();
+#define TMARK(k)                                                                       \
+  do {                                                                                 \
+    if ((P.debug & 16) && r == 0 && tid == 0) {                                        \
+      const unsigned long long t_ = clock64();                                         \
+      atomicAdd(&P.stats[1100 + (k)], t_ - tlast);                                     \
+      tlast = t_;                                                                      \
+    }                                                                                  \
+  } while (0)
   uint32_t seq = 0;       // rows streamed so far: row j of a step is ring use seq + j (uniform)
   uint32_t vote_id = 0;   // phase counter of the votes (uniform over the cluster)
   uint32_t tphase = 0;    // phase counter of the t* reductions
@@ -183,76 +200,130 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           if (!((fwd >> s) & 1ull)) continue;
           fwd &= ~(1ull << s);
           if (r == 0 && tid == 0) atomicAdd(&P.stats[0], 1ull);
-          const int32_t* rows = tile + ((size_t)s * n + v0) * ld;
-          const uint32_t rowbytes = (uint32_t)ld * 4;
+          TMARK(9);
+          const uint8_t* rows = t16 ? (const uint8_t*)(P.tile16 + (((size_t)inst * (S - 1) + s) * n + v0) * P.ld16)
+                                    : (const uint8_t*)(tile + ((size_t)s * n + v0) * ld);
           // row j goes to slot (seq + j) % nbr; the warp that consumes row j refills its slot with
           // row j + nbr, so nbr rows are always in flight and no CTA-wide barrier sits in the loop
           auto issue = [&](int j) {
             const int b = (int)((seq + (uint32_t)j) & (uint32_t)(nbr - 1));
-            fence_proxy_async_smem();
             mbar_arrive_expect_tx(&mbar[b], rowbytes);
-            bulk_g2s(ring + (size_t)b * ld, rows + (size_t)j * ld, rowbytes, &mbar[b]);
+            bulk_g2s(ring + (size_t)b * rowbytes, rows + (size_t)j * rowbytes, rowbytes, &mbar[b]);
           };
-          if (tid == 0)
-            for (int j = 0; j < min(nbr, nr); ++j) issue(j);
+          if (lane == 0) {  // each warp fills the slots of its own first rows
+            fence_proxy_async_smem();
+            for (int j = warp; j < min(nbr, nr); j += NW) issue(j);
+          }
           const uint32_t lim = T32 > (uint32_t)maxw ? T32 - (uint32_t)maxw : 0u;
-          int wide = lim == 0u;
-          for (int u = tid; u < ld; u += CT) {  // gather out_s over DSMEM
-            const uint64_t kk = u < n ? *rkout(s, u) : INF;
-            kbuf[u] = kk == INF ? kBig : kk;
-            uint32_t k32 = T32 << H32;
-            if (kk != INF) {
-              const uint64_t c = kk >> kHopBits, hops = kk & ((1ull << kHopBits) - 1);
-              if (c >= lim || hops + 1 >= (1ull << H32)) wide = 1;
-              k32 = ((uint32_t)c << H32) + (uint32_t)hops + 1u;
+          int wide = lim == 0u || (P.debug & 32);  // testing: force the 64-bit path
+          for (int u0 = 0; u0 < ldk; u0 += 4 * CT) {  // gather out_s over DSMEM (4 loads in flight)
+            uint64_t kk[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int u = u0 + j * CT + tid;
+              kk[j] = u < n ? dsmem_ld_u64(dsmem_addr(kout + s * R + (u - own(u) * R), (uint32_t)own(u))) : INF;
             }
-            kb32[u] = k32;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int u = u0 + j * CT + tid;
+              if (u >= ldk) break;
+              kbuf[u] = kk[j] == INF ? kBig : kk[j];
+              uint32_t k32 = T32 << H32;
+              if (kk[j] != INF) {
+                const uint64_t c = kk[j] >> kHopBits, hops = kk[j] & ((1ull << kHopBits) - 1);
+                if (c >= lim || hops + 1 >= (1ull << H32)) wide = 1;
+                k32 = ((uint32_t)c << H32) + (uint32_t)hops + 1u;
+              }
+              kb32[u] = k32;
+            }
           }
           wide = __syncthreads_or(wide);
+          TMARK(0);
           int ch = 0;
           for (int j = warp; j < nr; j += NW) {
             const uint32_t q = seq + (uint32_t)j;
             const int b = (int)(q & (uint32_t)(nbr - 1));
             mbar_wait(&mbar[b], (q / (uint32_t)nbr) & 1u);
-            const int4* row = (const int4*)(ring + (size_t)b * ld);
+            const uint8_t* rowb = ring + (size_t)b * rowbytes;
             uint64_t best;
             if (!wide) {
-              // 32-bit: per weight one clamp, one shift and one DPX add-min (VIADDMNMX)
+              // 32-bit: per weight one clamp, one shift and one DPX add-min (VIADDMNMX); four
+              // independent accumulators keep the add-min chains short
               const uint4* kv4 = (const uint4*)kb32;
-              uint32_t acc = 0xFFFFFFFFu;
+              uint32_t a0 = 0xFFFFFFFFu, a1 = a0, a2 = a0, a3 = a0;
+              if (t16) {
+                const uint4* row = (const uint4*)rowb;
+#pragma unroll 2
+                for (int c = lane; c < ldk / 8; c += 32) {
+                  const uint4 w = row[c];  // 8 weights, two per word
+                  const uint4 ka = kv4[2 * c], kc = kv4[2 * c + 1];
+                  uint32_t x = __vminu2(w.x, T2);
+                  a0 = __viaddmin_u32(ka.x, (x & 0xFFFFu) << H32, a0);
+                  a1 = __viaddmin_u32(ka.y, (x >> 16) << H32, a1);
+                  x = __vminu2(w.y, T2);
+                  a2 = __viaddmin_u32(ka.z, (x & 0xFFFFu) << H32, a2);
+                  a3 = __viaddmin_u32(ka.w, (x >> 16) << H32, a3);
+                  x = __vminu2(w.z, T2);
+                  a0 = __viaddmin_u32(kc.x, (x & 0xFFFFu) << H32, a0);
+                  a1 = __viaddmin_u32(kc.y, (x >> 16) << H32, a1);
+                  x = __vminu2(w.w, T2);
+                  a2 = __viaddmin_u32(kc.z, (x & 0xFFFFu) << H32, a2);
+                  a3 = __viaddmin_u32(kc.w, (x >> 16) << H32, a3);
+                }
+              } else {
+                const int4* row = (const int4*)rowb;
 #pragma unroll 4
-              for (int c = lane; c < ld / 4; c += 32) {
-                const int4 w = row[c];
-                const uint4 kq = kv4[c];
-                acc = __viaddmin_u32(kq.x, min((uint32_t)w.x, T32) << H32, acc);
-                acc = __viaddmin_u32(kq.y, min((uint32_t)w.y, T32) << H32, acc);
-                acc = __viaddmin_u32(kq.z, min((uint32_t)w.z, T32) << H32, acc);
-                acc = __viaddmin_u32(kq.w, min((uint32_t)w.w, T32) << H32, acc);
+                for (int c = lane; c < ld / 4; c += 32) {
+                  const int4 w = row[c];
+                  const uint4 kq = kv4[c];
+                  a0 = __viaddmin_u32(kq.x, min((uint32_t)w.x, T32) << H32, a0);
+                  a1 = __viaddmin_u32(kq.y, min((uint32_t)w.y, T32) << H32, a1);
+                  a2 = __viaddmin_u32(kq.z, min((uint32_t)w.z, T32) << H32, a2);
+                  a3 = __viaddmin_u32(kq.w, min((uint32_t)w.w, T32) << H32, a3);
+                }
               }
-              acc = __reduce_min_sync(0xffffffffu, acc);
+              const uint32_t acc = __reduce_min_sync(0xffffffffu, min(min(a0, a1), min(a2, a3)));
               best = (acc >> H32) >= T32 ? INF
                                          : ((uint64_t)(acc >> H32) << kHopBits) | (uint64_t)(acc & ((1u << H32) - 1u));
             } else {
               // 64-bit branch-free: keys are < 2^62 when finite (DESIGN.md 2.2 bound) and kBig =
-              // 2^62 stands for INF in kbuf, absent weights are INT32_MAX; nothing overflows
-              uint64_t acc = kBig;
+              // 2^62 stands for INF in kbuf; absent weights (INT32_MAX, or 0xFFFF -> 2^42 in the
+              // 16-bit rows) push a candidate to >= 2^62; nothing overflows 64 bits
+              uint64_t acc = kBig, acc2 = kBig;
+              if (t16) {
+                const uint2* row = (const uint2*)rowb;
+                auto w64 = [](uint32_t h) -> uint64_t { return h == 0xFFFFu ? (1ull << 42) : (uint64_t)h; };
 #pragma unroll 2
-              for (int c = lane; c < ld / 4; c += 32) {
-                const int4 w = row[c];
-                const ulonglong2 k01 = *(const ulonglong2*)(kbuf + 4 * c);
-                const ulonglong2 k23 = *(const ulonglong2*)(kbuf + 4 * c + 2);
-                acc = umin64(acc, k01.x + ((uint64_t)(uint32_t)w.x << kHopBits) + 1ull);
-                acc = umin64(acc, k01.y + ((uint64_t)(uint32_t)w.y << kHopBits) + 1ull);
-                acc = umin64(acc, k23.x + ((uint64_t)(uint32_t)w.z << kHopBits) + 1ull);
-                acc = umin64(acc, k23.y + ((uint64_t)(uint32_t)w.w << kHopBits) + 1ull);
+                for (int c = lane; c < ldk / 4; c += 32) {
+                  const uint2 w = row[c];  // 4 weights
+                  const ulonglong2 k01 = *(const ulonglong2*)(kbuf + 4 * c);
+                  const ulonglong2 k23 = *(const ulonglong2*)(kbuf + 4 * c + 2);
+                  acc = umin64(acc, k01.x + (w64(w.x & 0xFFFFu) << kHopBits) + 1ull);
+                  acc2 = umin64(acc2, k01.y + (w64(w.x >> 16) << kHopBits) + 1ull);
+                  acc = umin64(acc, k23.x + (w64(w.y & 0xFFFFu) << kHopBits) + 1ull);
+                  acc2 = umin64(acc2, k23.y + (w64(w.y >> 16) << kHopBits) + 1ull);
+                }
+              } else {
+                const int4* row = (const int4*)rowb;
+#pragma unroll 2
+                for (int c = lane; c < ld / 4; c += 32) {
+                  const int4 w = row[c];
+                  const ulonglong2 k01 = *(const ulonglong2*)(kbuf + 4 * c);
+                  const ulonglong2 k23 = *(const ulonglong2*)(kbuf + 4 * c + 2);
+                  acc = umin64(acc, k01.x + ((uint64_t)(uint32_t)w.x << kHopBits) + 1ull);
+                  acc2 = umin64(acc2, k01.y + ((uint64_t)(uint32_t)w.y << kHopBits) + 1ull);
+                  acc = umin64(acc, k23.x + ((uint64_t)(uint32_t)w.z << kHopBits) + 1ull);
+                  acc2 = umin64(acc2, k23.y + ((uint64_t)(uint32_t)w.w << kHopBits) + 1ull);
+                }
               }
+              acc = umin64(acc, acc2);
               for (int off = 16; off > 0; off >>= 1)
                 acc = umin64(acc, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)acc, off));
               best = acc >= kBig ? INF : acc;
             }
             __syncwarp();  // every lane is done with slot b
             if (lane == 0) {
-              if (j + nbr < nr) issue(j + nbr);
+              if (j + nbr < nr) { fence_proxy_async_smem(); issue(j + nbr); }
               const int e = (s + 1) * R + j;
               uint64_t kv = kin[e];
               if (best < kv) { kin[e] = best; kv = best; ch = 1; }
@@ -260,7 +331,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             }
           }
           seq += (uint32_t)nr;
-          if (vote(ch)) {
+          TMARK(1);
+          const bool vf = vote(ch);
+          TMARK(2);
+          if (vf) {
             if (s + 1 < S - 1) fwd |= 1ull << (s + 1);
             else tdirty = true;
             bwd |= 1ull << (s + 1);
@@ -290,6 +364,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           for (int q = 0; q < C; ++q) tn = umin64(tn, cl.map_shared_rank(misc, q)->tpart[slot]);
           if (tn < tkey) { tkey = tn; trev = true; }
         }
+        TMARK(3);
         // ---- t* -> out_{S-1} (reverse sink arcs) ----
         if (trev) {
           trev = false;
@@ -303,6 +378,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             }
           if (vote(ch)) bwd |= 1ull << (S - 1);
         }
+        TMARK(4);
         // ---- backward: reverse node arcs (owners) + reverse inter-stage arcs (DSMEM atomicMin) ----
         for (int s = S - 1; s >= 0; --s) {
           if (!((bwd >> s) & 1ull)) continue;
@@ -334,6 +410,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             bwd |= 1ull << (s - 1);
           }
         }
+        TMARK(5);
         if (r == 0 && tid == 0) atomicAdd(&P.stats[3], 1ull);
         if (!(fwd | bwd) && !tdirty && !trev) break;
       }
@@ -356,6 +433,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
       }
       if ((P.debug & 4) && M0->A == (P.debug >> 8)) { cl.sync(); break; }
 
+      TMARK(9);
       // ---- trace the canonical augmenting path and augment (leader CTA) ----
       if (r == 0) {
         auto key_of = [&](int id) -> uint64_t {
@@ -454,6 +532,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
       }
       cl.sync();
 
+      TMARK(6);
       // ---- locate the path's inter-stage arcs in the positive-arc lists (whole cluster) ----
       // arc e of the path is path[len-1-e] -> path[len-2-e]; the lists are scanned in parallel by
       // all C * CT threads of the cluster, chunk by chunk of CT path arcs staged in shared memory
@@ -487,6 +566,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
       }
       cl.sync();
 
+      TMARK(7);
       // ---- bottleneck and augmentation (leader CTA; a simple path touches every g, f_src,
       // f_snk and list entry at most once, so all in-place updates run in parallel) ----
       if (r == 0) {
@@ -596,6 +676,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           }
         }
       }
+      TMARK(8);
       cl.sync();
     }
 

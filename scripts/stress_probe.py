@@ -43,3 +43,11 @@ print(json.dumps({"config": "stress", "B": a.batch, "supply": a.supply, "ms": mi
                   "F": sol.flow_value.tolist(), "cost": sol.total_cost.tolist(), "status": sol.status.tolist(),
                   "ms_per_aug_per_instance": min(ms) / max(A / a.batch, 1),
                   "algorithmic_GBps": alg / t / 1e9, "stats": fl.stats()}))
+if os.environ.get("GWTF_DEBUG_FLAGS", "0") != "0" and int(os.environ["GWTF_DEBUG_FLAGS"]) & 16:
+    raw = fl.stats(raw=True)
+    names = ["gather", "relax", "relax_vote", "tstar", "trev", "backward", "trace", "lookup", "augment", "other"]
+    cyc = raw[1100:1110].astype(float)
+    tot = cyc.sum()
+    print("phase cycles (leader thread, all solves, summed over clusters):")
+    for nm, c in zip(names, cyc):
+        print(f"  {nm:10s} {c:14.0f}  {100 * c / tot:5.1f}%")
