@@ -111,6 +111,10 @@ CONFIGS = {
     # stress shape scaled down (same distributions) for oracle parity of the cluster tier
     "stress_s": Config("stress_s", 5, S=8, n=256, M=512, max_cap=20, cap=(1, 20), B=8, cost=(1, 100),
                        max_rounds=120 + 2 * 512),
+    # stress distributions at 64 x 512: 2Sn+2 >= 2^16 hop values, so the cluster tier's 32-bit keys
+    # carry >= 17 hop bits (its shift-and-mask weight path), with a small supply for the oracle
+    "stress_h": Config("stress_h", 6, S=64, n=512, M=16, max_cap=20, cap=(1, 20), B=2, cost=(1, 100),
+                       max_rounds=120 + 2 * 16),
     # flow-test settings 1-4: 1 source, 40 relays, 8 or 10 stages
     "flow1": Config("flow1", 11, S=8, n=5, M=128, max_cap=3, cap=(1, 3), B=64, cost=(1, 20), max_rounds=120 + 256),
     "flow2": Config("flow2", 12, S=10, n=4, M=128, max_cap=3, cap=(1, 3), B=64, cost=(1, 20), max_rounds=120 + 256),

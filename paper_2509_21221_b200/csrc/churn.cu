@@ -27,7 +27,8 @@ __global__ void pad_tiles_kernel(const Problem P, const int32_t* __restrict__ li
   }
 }
 
-// 16-bit copy of the padded tiles for the cluster tier's streamed relaxation (half the HBM bytes)
+// 16-bit copy of the padded tiles for the cluster tier's streamed relaxation (half the HBM bytes);
+// absent arcs and padding carry the clamp value t16code, so the kernel needs no per-weight clamp
 __global__ void pack_tile16_kernel(const Problem P) {
   const size_t rows = (size_t)P.B * (P.S - 1) * P.n;
   const size_t total = rows * P.ld16;
@@ -35,7 +36,7 @@ __global__ void pack_tile16_kernel(const Problem P) {
     const size_t row = t / P.ld16;
     const int c = (int)(t % P.ld16);
     const int32_t v = c < P.n ? P.tile[row * P.ld + c] : kAbsent;
-    P.tile16[t] = v == kAbsent || v >= 0xFFFF ? (uint16_t)0xFFFFu : (uint16_t)v;
+    P.tile16[t] = v == kAbsent || v >= P.t16code ? (uint16_t)P.t16code : (uint16_t)v;
   }
 }
 
@@ -69,9 +70,10 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
       P.snk[(size_t)b * P.n + w] = c;
     } else if (s >= 0 && s < P.S - 1 && v >= 0 && v < P.n && w >= 0 && w < P.n) {
       P.tile[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld + w] = c;
-      if (P.tile16) {  // the cluster tier's 16-bit copy; a finite cost >= 0xFFFF retires it (bit 2)
-        if (c != kAbsent && c >= 0xFFFF) atomicOr(bad, 2);
-        P.tile16[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld16 + w] = c == kAbsent || c >= 0xFFFF ? 0xFFFFu : (uint16_t)c;
+      if (P.tile16) {  // the cluster tier's 16-bit copy; a finite cost >= t16code retires it (bit 2)
+        if (c != kAbsent && c >= P.t16code) atomicOr(bad, 2);
+        P.tile16[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld16 + w] =
+            c == kAbsent || c >= P.t16code ? (uint16_t)P.t16code : (uint16_t)c;
       }
     } else {
       atomicOr(bad, 1);

@@ -379,7 +379,13 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     cudaFree(link_tmp);
     h->allocs.erase(std::find(h->allocs.begin(), h->allocs.end(), (void*)link_tmp));
   }
-  if (P.cluster_size > 0 && nb && maxc < 0xFFFF && !getenv("GWTF_NO_TILE16")) {  // 16-bit tile copy streamed by the cluster tier
+  {  // absent code of the 16-bit tiles = the cluster tier's 32-bit key clamp T32 (ssp_cluster.cu)
+    int H = 0;
+    while ((1ll << H) <= 2 * S * n + 2) ++H;
+    const int CB = 32 - H;
+    P.t16code = CB >= 4 ? (int32_t)std::min<int64_t>((1ll << (CB - 1)) - 1, 0xFFFF) : 0;
+  }
+  if (P.cluster_size > 0 && nb && maxc < P.t16code && !getenv("GWTF_NO_TILE16")) {  // 16-bit tile copy streamed by the cluster tier
     P.ld16 = (int32_t)((n + 7) / 8 * 8);
     if ((s = alloc(h, &P.tile16, B * nb * n * P.ld16, true)) != GWTF_OK) return bail(s);
     CK(h, launch_pack_tile16(P, h->stream));

@@ -16,9 +16,10 @@ struct Problem {
   int64_t Mmax;                // max supply over the batch (SRC/SNK slot arrays)
   int32_t Lcap;                // positive-arc list capacity per boundary
   int32_t* tile;               // [B][S-1][n][ld] dest-major, padding = kAbsent
-  uint16_t* tile16;            // cluster tier: [B][S-1][n][ld16] copy of tile, 0xFFFF = absent/padding
-                               // (nullptr when some cost >= 0xFFFF or the tier is unused)
+  uint16_t* tile16;            // cluster tier: [B][S-1][n][ld16] copy of tile, t16code = absent/padding
+                               // (nullptr when some cost >= t16code or the tier is unused)
   int32_t ld16;                // n rounded up to 8
+  int32_t t16code;             // T32 of the cluster tier's 32-bit keys (ssp_cluster.cu), < 2^16
   int32_t* src;                // [B][n]
   int32_t* snk;                // [B][n]
   int32_t* cap;                // [B][S][n]

@@ -3,18 +3,20 @@
 // 1,024 clients = 252 MB of int32 tiles).  Same canonical SSP as ssp.cu with
 // 64-bit (cost, hops) keys; only the data placement differs:
 //   * CTA r of the cluster owns destination rows v in [r*R, r*R+R) of every stage: their in/out
-//     keys, node flows and capacities live in its shared memory;
+//     keys, node flows and capacities live in its shared memory (read remotely through DSMEM;
+//     reverse arcs relax into the owner's keys with a DSMEM 64-bit compare-and-swap min,
+//     common.cuh: the generic 64-bit atomicMin is not atomic on remote shared memory);
 //   * the dense min-plus relaxation of boundary s streams the CTA's R rows of tile s from HBM
-//     by TMA bulk copies (cp.async.bulk, one row per copy, up to 32 rows in flight on an
-//     mbarrier ring; 32-bit DPX keys when the costs allow) while the out_s key vector is
-//     gathered from the owner CTAs through DSMEM;
-//   * one cluster barrier per boundary step; reverse arcs are relaxed with a DSMEM 64-bit
-//     compare-and-swap min into the owner's keys (common.cuh: the generic 64-bit atomicMin is
-//     not atomic on remote shared memory); phase votes and the t* minimum are reduced from
+//     in chunks of NW rows (one cp.async.bulk per chunk, one mbarrier per ring slot; the last
+//     warp to finish a chunk refills its slot), from a 16-bit copy of the tiles when the costs
+//     fit (half the bytes), with 32-bit DPX keys (VIADDMNMX) held in registers when the costs
+//     allow, while the out_s key vector is gathered from the owner CTAs through DSMEM;
+//   * one cluster barrier per boundary step; phase votes and the t* minimum are reduced from
 //     per-CTA slots read by every CTA (no remote atomics, no resets);
-//   * the leader CTA traces the canonical path and augments; the arc lists stay in global memory
-//     and are only accessed through L2 (ld/st.global.cg): they are written by the leader's SM and
-//     read by the other SMs of the cluster, whose L1 would otherwise serve stale lines.
+//   * the leader CTA traces the canonical path; the whole cluster locates the path's arcs in the
+//     positive-arc lists; the leader augments.  The lists stay in global memory and are only
+//     accessed through L2: written by the leader's SM, read by the other SMs of the cluster,
+//     whose L1 would otherwise serve stale lines.
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
@@ -31,7 +33,8 @@ namespace {
 
 constexpr int CT = 512;      // threads per CTA
 constexpr int NW = CT / 32;  // warps per CTA: warp w relaxes rows w, w + NW, ... of a boundary
-constexpr int NBMAX = 64;    // row slots of the TMA ring (one row per bulk copy)
+constexpr int NBMAX = 64;    // chunk slots of the TMA ring (one chunk of NW rows per bulk copy)
+constexpr int KQ = 4;        // register-resident key chunks per lane (16-bit rows up to 1,024 weights)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr uint64_t INF = ~0ull;
 constexpr uint64_t kBig = 1ull << 62;  // INF inside the branch-free relaxation
@@ -48,14 +51,14 @@ struct Misc {  // per-CTA control block; the leader's copy is authoritative
 
 struct ClLayout {
   size_t misc, kin, kout, g, capE, srcf, snkf, kbuf, kb32, aq, ring, mbar, total;
-  int nbr;  // row slots of the ring (power of two, >= NW)
+  int nbc;  // chunk slots of the ring (chunk = NW consecutive rows = one bulk copy)
 };
 __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   ClLayout L;
   const size_t R = (P.n + C - 1) / C, SR = (size_t)P.S * R;
   size_t o = 0;
   L.misc = o; o += al16c(sizeof(Misc));
-  L.mbar = o; o += al16c(NBMAX * 8);
+  L.mbar = o; o += al16c(NBMAX * 8 + NBMAX * 4);  // full barriers + consumed-row counters
   L.kin = o; o += al16c(SR * 8);
   L.kout = o; o += al16c(SR * 8);
   L.g = o; o += al16c(SR * 2);
@@ -67,10 +70,14 @@ __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   L.kbuf = o; o += al16c(ldk * 8);
   L.kb32 = o; o += al16c(ldk * 4);
   L.aq = o; o += al16c((size_t)CT * 12);
-  // as many row slots in flight as fit (more bytes in flight per SM = closer to its HBM share)
-  L.nbr = NBMAX;
-  while (L.nbr > NW && o + (size_t)L.nbr * slot > kSmemMax) L.nbr >>= 1;
-  L.ring = o; o += al16c((size_t)L.nbr * slot);
+  // as many chunk slots in flight as fit, up to the ceil(R / NW) chunks a CTA streams per
+  // boundary.  Chunks, not rows: a bulk copy costs the TMA unit a fixed ~46 cycles, so 2 KB
+  // rows would cap an SM at ~44 B/cycle (scratch probe), 32-64 KB chunks run at ~80 B/cycle.
+  const size_t cbytes = slot * NW;
+  const size_t fit = o < kSmemMax ? (kSmemMax - o - 16) / cbytes : 0;
+  L.nbc = (int)std::min<size_t>(std::min<size_t>(fit, (size_t)NBMAX), (R + NW - 1) / NW);
+  if (L.nbc < 1) L.nbc = 1;  // layout too large: total > kSmemMax rejects it
+  L.ring = o; o += al16c((size_t)L.nbc * cbytes);
   L.total = o;
   return L;
 }
@@ -86,8 +93,6 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const ClLayout L = cl_layout(P, C);
   Misc* misc = (Misc*)(sm + L.misc);
   uint64_t* mbar = (uint64_t*)(sm + L.mbar);
-  uint64_t* kin = (uint64_t*)(sm + L.kin);
-  uint64_t* kout = (uint64_t*)(sm + L.kout);
   int16_t* g = (int16_t*)(sm + L.g);
   int16_t* capE = (int16_t*)(sm + L.capE);
   int32_t* srcf = (int32_t*)(sm + L.srcf);
@@ -96,14 +101,19 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   uint32_t* kb32 = (uint32_t*)(sm + L.kb32);
   uint32_t* aq = (uint32_t*)(sm + L.aq);  // staged path arcs: list key, boundary, list length
   uint8_t* ring = sm + L.ring;
-  const int nbr = L.nbr;
+  const int nbc = L.nbc;
+  uint32_t* ecnt = (uint32_t*)(mbar + NBMAX);  // per chunk slot: rows consumed (monotonic)
   // streamed rows: the 16-bit tile copy when present (half the bytes), else the int32 tiles
   const bool t16 = P.tile16 != nullptr;
   const int ldk = t16 ? P.ld16 : ld;  // weights per streamed row
   const uint32_t rowbytes = t16 ? (uint32_t)P.ld16 * 2 : (uint32_t)ld * 4;
   Misc* M0 = cl.map_shared_rank(misc, 0);
-  uint32_t* path = (uint32_t*)(P.ws_cluster) + (size_t)cid * 2 * (2 * S * n + 4);  // nodes t* -> s*
+  // per-cluster global scratch: path (t* -> s*) and found (gwtf_api.cpp sizes it)
+  uint32_t* path = (uint32_t*)(P.ws_cluster + (size_t)cid * 2 * (2 * (size_t)S * n + 4) * 4);
   int32_t* found = (int32_t*)(path + (2 * S * n + 4));  // list index of path arc e (INT_MAX: none)
+  // keys of the owned rows: kin[s * R + lv] / kout[s * R + lv] in shared memory (remote: DSMEM)
+  uint64_t* kin = (uint64_t*)(sm + L.kin);
+  uint64_t* kout = (uint64_t*)(sm + L.kout);
   // remote views of the owners' arrays
   const uint64_t rmag = ((1ull << 32) + R - 1) / R;  // v / R == (v * rmag) >> 32 for v < 2^32 / R
   auto own = [&](int v) { return (int)(((uint64_t)(uint32_t)v * rmag) >> 32); };
@@ -114,15 +124,15 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const int CB32 = 32 - H32;
   const uint32_t T32 = CB32 >= 4 ? min((1u << (CB32 - 1)) - 1u, t16 ? 0xFFFFu : 0xFFFFFFFFu) : 0u;
   const uint32_t T2 = T32 | (T32 << 16);  // per-halfword clamp of the 16-bit rows
-  auto rkin = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kin, q) + s * R + (v - q * R); };
-  auto rkout = [&](int s, int v) -> uint64_t* { const int q = own(v); return cl.map_shared_rank(kout, q) + s * R + (v - q * R); };
+  auto ldk_in = [&](int s, int v) -> uint64_t { const int q = own(v); return *(cl.map_shared_rank(kin, q) + s * R + (v - q * R)); };
+  auto ldk_out = [&](int s, int v) -> uint64_t { const int q = own(v); return *(cl.map_shared_rank(kout, q) + s * R + (v - q * R)); };
   auto rg = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
   auto rcap = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(capE, q) + s * R + (v - q * R); };
   auto rsrcf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(srcf, q) + (v - q * R); };
   auto rsnkf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(snkf, q) + (v - q * R); };
 
   if (tid == 0) {
-    for (int b = 0; b < nbr; ++b) mbar_init(&mbar[b], 1);
+    for (int b = 0; b < nbc; ++b) { mbar_init(&mbar[b], 1); ecnt[b] = 0; }
     fence_barrier_init();
   }
   // testing (GWTF_DEBUG_FLAGS & 16): leader-thread cycle counts per phase into stats[1100 + k]
@@ -135,7 +145,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
       tlast = t_;                                                                      \
     }                                                                                  \
   } while (0)
-  uint32_t seq = 0;       // rows streamed so far: row j of a step is ring use seq + j (uniform)
+  int slot0 = 0;          // ring slot of the next chunk (uniform over the CTA)
+  uint64_t php = 0;       // per-slot mbarrier phase parity (uniform over the CTA)
   uint32_t vote_id = 0;   // phase counter of the votes (uniform over the cluster)
   uint32_t tphase = 0;    // phase counter of the t* reductions
   __syncthreads();
@@ -180,15 +191,16 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
     for (;;) {  // successive shortest paths
       const int64_t F = M0->F;
       if (F >= M || M0->status) break;
-      for (int k = tid; k < S * R; k += CT) { kin[k] = INF; kout[k] = INF; }
-      __syncthreads();
-      for (int lv = tid; lv < nr; lv += CT) {  // s* -> in_0, in_0 -> out_0
-        const int v = v0 + lv;
-        if (src[v] != kAbsent) {
-          const uint64_t c = ((uint64_t)(uint32_t)src[v] << kHopBits) | 1ull;
-          kin[lv] = c;
-          if (g[lv] < capE[lv]) kout[lv] = c + 1;
+      for (int k = tid; k < S * R; k += CT) {  // own rows: INF, then s* -> in_0, in_0 -> out_0
+        const int s = k / R, lv = k - s * R, v = v0 + lv;
+        if (lv >= nr) continue;
+        uint64_t ki = INF, ko = INF;
+        if (s == 0 && src[v] != kAbsent) {
+          ki = ((uint64_t)(uint32_t)src[v] << kHopBits) | 1ull;
+          if (g[lv] < capE[lv]) ko = ki + 1;
         }
+        kin[k] = ki;
+        kout[k] = ko;
       }
       uint64_t tkey = INF;
       uint64_t fwd = S > 1 ? 1ull : 0ull, bwd = 1ull;
@@ -203,20 +215,33 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           TMARK(9);
           const uint8_t* rows = t16 ? (const uint8_t*)(P.tile16 + (((size_t)inst * (S - 1) + s) * n + v0) * P.ld16)
                                     : (const uint8_t*)(tile + ((size_t)s * n + v0) * ld);
-          // row j goes to slot (seq + j) % nbr; the warp that consumes row j refills its slot with
-          // row j + nbr, so nbr rows are always in flight and no CTA-wide barrier sits in the loop
-          auto issue = [&](int j) {
-            const int b = (int)((seq + (uint32_t)j) & (uint32_t)(nbr - 1));
-            mbar_arrive_expect_tx(&mbar[b], rowbytes);
-            bulk_g2s(ring + (size_t)b * rowbytes, rows + (size_t)j * rowbytes, rowbytes, &mbar[b]);
+          // chunk k (rows k*NW .. k*NW+NW-1, one per warp) goes to slot (slot0 + k) % nbc; the last
+          // warp to finish a chunk refills its slot with chunk k + nbc
+          const int nch = (nr + NW - 1) / NW;
+          const uint32_t cbytes = (uint32_t)NW * rowbytes;
+          auto issue = [&](int k, int b) {  // chunk k into slot b
+            const uint32_t bytes = (uint32_t)min(NW, nr - k * NW) * rowbytes;
+            mbar_arrive_expect_tx(&mbar[b], bytes);
+            bulk_g2s(ring + (size_t)b * cbytes, rows + (size_t)k * cbytes, bytes, &mbar[b]);
           };
-          if (lane == 0) {  // each warp fills the slots of its own first rows
+          const bool nostream = P.debug & 64;  // testing: time the compute without the stream
+          if (tid == 0 && !nostream) {
             fence_proxy_async_smem();
-            for (int j = warp; j < min(nbr, nr); j += NW) issue(j);
+            for (int k = 0; k < min(nbc, nch); ++k) issue(k, slot0 + k < nbc ? slot0 + k : slot0 + k - nbc);
+          }
+          // lane k of warp w prefetches the keys of the warp's row j = k * NW + w of in/out_{s+1}
+          // (consumed by lane k after the row's minimum; rows beyond 32 per warp load late)
+          uint64_t pkv = INF, pko = INF;
+          int pres = 0;  // in -> out residual of that row
+          if (lane < nch && lane * NW + warp < nr) {
+            const int jr = lane * NW + warp;
+            pkv = kin[(s + 1) * R + jr];
+            pko = kout[(s + 1) * R + jr];
+            pres = g[(s + 1) * R + jr] < capE[(s + 1) * R + jr];
           }
           const uint32_t lim = T32 > (uint32_t)maxw ? T32 - (uint32_t)maxw : 0u;
           int wide = lim == 0u || (P.debug & 32);  // testing: force the 64-bit path
-          for (int u0 = 0; u0 < ldk; u0 += 4 * CT) {  // gather out_s over DSMEM (4 loads in flight)
+          for (int u0 = 0; u0 < ldk; u0 += 4 * CT) {  // gather out_s from L2 (4 loads in flight)
             uint64_t kk[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -237,14 +262,27 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               kb32[u] = k32;
             }
           }
-          wide = __syncthreads_or(wide);
+          wide = __syncthreads_or(wide) && !nostream;
+          // 16-bit rows of up to 1,024 weights: every lane keeps the 32-bit keys of its own
+          // columns (chunks c = lane + 32q, 8 weights each) in registers for the whole step
+          const bool kreg = t16 && ldk <= 8 * 32 * KQ;
+          uint4 kr[2 * KQ];
+          if (kreg && !wide) {
+            const uint4* kv4 = (const uint4*)kb32;
+#pragma unroll
+            for (int q = 0; q < KQ; ++q) {
+              const int c = lane + 32 * q;
+              kr[2 * q] = c < ldk / 8 ? kv4[2 * c] : make_uint4(0u, 0u, 0u, 0u);
+              kr[2 * q + 1] = c < ldk / 8 ? kv4[2 * c + 1] : make_uint4(0u, 0u, 0u, 0u);
+            }
+          }
           TMARK(0);
           int ch = 0;
-          for (int j = warp; j < nr; j += NW) {
-            const uint32_t q = seq + (uint32_t)j;
-            const int b = (int)(q & (uint32_t)(nbr - 1));
-            mbar_wait(&mbar[b], (q / (uint32_t)nbr) & 1u);
-            const uint8_t* rowb = ring + (size_t)b * rowbytes;
+          for (int k = 0, b = slot0; k < nch; ++k, b = b + 1 == nbc ? 0 : b + 1) {
+            const int j = k * NW + warp;
+            if (j < nr) {
+            if (!nostream) mbar_wait(&mbar[b], (uint32_t)(php >> b) & 1u);
+            const uint8_t* rowb = ring + (size_t)b * cbytes + (size_t)warp * rowbytes;
             uint64_t best;
             if (!wide) {
               // 32-bit: per weight one clamp, one shift and one DPX add-min (VIADDMNMX); four
@@ -252,23 +290,40 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               const uint4* kv4 = (const uint4*)kb32;
               uint32_t a0 = 0xFFFFFFFFu, a1 = a0, a2 = a0, a3 = a0;
               if (t16) {
+                // 16-bit rows, pre-clamped (absent = T32): two weights per word, shifted into the
+                // cost field; with H32 >= 16 the low weight is one shift, the high one shift + mask
                 const uint4* row = (const uint4*)rowb;
+                const uint32_t hm = ~((1u << H32) - 1u);
+                if (kreg && H32 >= 16) {
+                  const int hs = H32 - 16;
+#pragma unroll
+                  for (int q = 0; q < KQ; ++q) {
+                    if (lane + 32 * q < ldk / 8) {
+                      const uint4 w = row[lane + 32 * q];
+                      a0 = __viaddmin_u32(kr[2 * q].x, w.x << H32, a0);
+                      a1 = __viaddmin_u32(kr[2 * q].y, (w.x << hs) & hm, a1);
+                      a2 = __viaddmin_u32(kr[2 * q].z, w.y << H32, a2);
+                      a3 = __viaddmin_u32(kr[2 * q].w, (w.y << hs) & hm, a3);
+                      a0 = __viaddmin_u32(kr[2 * q + 1].x, w.z << H32, a0);
+                      a1 = __viaddmin_u32(kr[2 * q + 1].y, (w.z << hs) & hm, a1);
+                      a2 = __viaddmin_u32(kr[2 * q + 1].z, w.w << H32, a2);
+                      a3 = __viaddmin_u32(kr[2 * q + 1].w, (w.w << hs) & hm, a3);
+                    }
+                  }
+                } else {
 #pragma unroll 2
-                for (int c = lane; c < ldk / 8; c += 32) {
-                  const uint4 w = row[c];  // 8 weights, two per word
-                  const uint4 ka = kv4[2 * c], kc = kv4[2 * c + 1];
-                  uint32_t x = __vminu2(w.x, T2);
-                  a0 = __viaddmin_u32(ka.x, (x & 0xFFFFu) << H32, a0);
-                  a1 = __viaddmin_u32(ka.y, (x >> 16) << H32, a1);
-                  x = __vminu2(w.y, T2);
-                  a2 = __viaddmin_u32(ka.z, (x & 0xFFFFu) << H32, a2);
-                  a3 = __viaddmin_u32(ka.w, (x >> 16) << H32, a3);
-                  x = __vminu2(w.z, T2);
-                  a0 = __viaddmin_u32(kc.x, (x & 0xFFFFu) << H32, a0);
-                  a1 = __viaddmin_u32(kc.y, (x >> 16) << H32, a1);
-                  x = __vminu2(w.w, T2);
-                  a2 = __viaddmin_u32(kc.z, (x & 0xFFFFu) << H32, a2);
-                  a3 = __viaddmin_u32(kc.w, (x >> 16) << H32, a3);
+                  for (int c = lane; c < ldk / 8; c += 32) {
+                    const uint4 w = row[c];
+                    const uint4 ka = kv4[2 * c], kc = kv4[2 * c + 1];
+                    a0 = __viaddmin_u32(ka.x, (w.x & 0xFFFFu) << H32, a0);
+                    a1 = __viaddmin_u32(ka.y, (w.x >> 16) << H32, a1);
+                    a2 = __viaddmin_u32(ka.z, (w.y & 0xFFFFu) << H32, a2);
+                    a3 = __viaddmin_u32(ka.w, (w.y >> 16) << H32, a3);
+                    a0 = __viaddmin_u32(kc.x, (w.z & 0xFFFFu) << H32, a0);
+                    a1 = __viaddmin_u32(kc.y, (w.z >> 16) << H32, a1);
+                    a2 = __viaddmin_u32(kc.z, (w.w & 0xFFFFu) << H32, a2);
+                    a3 = __viaddmin_u32(kc.w, (w.w >> 16) << H32, a3);
+                  }
                 }
               } else {
                 const int4* row = (const int4*)rowb;
@@ -292,7 +347,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               uint64_t acc = kBig, acc2 = kBig;
               if (t16) {
                 const uint2* row = (const uint2*)rowb;
-                auto w64 = [](uint32_t h) -> uint64_t { return h == 0xFFFFu ? (1ull << 42) : (uint64_t)h; };
+                auto w64 = [&](uint32_t h) -> uint64_t { return h == T32 ? (1ull << 42) : (uint64_t)h; };
 #pragma unroll 2
                 for (int c = lane; c < ldk / 4; c += 32) {
                   const uint2 w = row[c];  // 4 weights
@@ -321,16 +376,27 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 acc = umin64(acc, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)acc, off));
               best = acc >= kBig ? INF : acc;
             }
-            __syncwarp();  // every lane is done with slot b
-            if (lane == 0) {
-              if (j + nbr < nr) { fence_proxy_async_smem(); issue(j + nbr); }
+            if (lane == (k & 31)) {  // the lane holding the row's prefetched keys
               const int e = (s + 1) * R + j;
-              uint64_t kv = kin[e];
+              uint64_t kv = pkv, ko = pko;
+              int res = pres;
+              if (k >= 32) { kv = kin[e]; ko = kout[e]; res = g[e] < capE[e]; }
               if (best < kv) { kin[e] = best; kv = best; ch = 1; }
-              if (kv != INF && g[e] < capE[e] && kv + 1 < kout[e]) { kout[e] = kv + 1; ch = 1; }
+              if (kv != INF && res && kv + 1 < ko) { kout[e] = kv + 1; ch = 1; }
+            }
+            }
+            // every lane is done with its row of slot b (its values fed the warp minimum); the
+            // last warp to finish the chunk refills the slot through the async proxy
+            php ^= 1ull << b;  // slot b's phase advanced (every thread tracks every chunk)
+            if (lane == 0 && k + nbc < nch && !nostream) {
+              if (atomicAdd(&ecnt[b], 1u) % NW == NW - 1) {  // last reader of the chunk
+                __threadfence_block();
+                fence_proxy_async_smem();
+                issue(k + nbc, b);
+              }
             }
           }
-          seq += (uint32_t)nr;
+          slot0 = (slot0 + nch) % nbc;
           TMARK(1);
           const bool vf = vote(ch);
           TMARK(2);
@@ -372,9 +438,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           if (tkey != INF)
             for (int lv = tid; lv < nr; lv += CT) {
               if (snkf[lv] <= 0) continue;
-              const int e = (S - 1) * R + lv;
               const uint64_t c = tkey - ((uint64_t)(uint32_t)snk[v0 + lv] << kHopBits) + 1ull;
-              if (c < kout[e]) { kout[e] = c; ch = 1; }
+              if (c < kout[(S - 1) * R + lv]) { kout[(S - 1) * R + lv] = c; ch = 1; }
             }
           if (vote(ch)) bwd |= 1ull << (S - 1);
         }
@@ -385,8 +450,9 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           bwd &= ~(1ull << s);
           if (r == 0 && tid == 0) atomicAdd(&P.stats[1], 1ull);
           for (int lv = tid; lv < nr; lv += CT) {
-            const int e = s * R + lv;
-            if (g[e] > 0 && kout[e] != INF && kout[e] + 1 < kin[e]) kin[e] = kout[e] + 1;
+            if (g[s * R + lv] <= 0) continue;
+            const uint64_t ko = kout[s * R + lv];
+            if (ko != INF && ko + 1 < kin[s * R + lv]) kin[s * R + lv] = ko + 1;
           }
           if (s == 0) { cl.sync(); break; }
           const uint32_t* al = arcs + (size_t)(s - 1) * Lcap;
@@ -395,8 +461,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           for (int e = r * CT + tid; e < c; e += C * CT) {
             const uint32_t ent = __ldcg(&al[e]);
             const int u = (int)(ent >> 20), v = (int)((ent >> 8) & 0xFFFu);
-            uint64_t ki = *rkin(s, v);
-            const uint64_t kov = *rkout(s, v);
+            uint64_t ki = ldk_in(s, v);
+            const uint64_t kov = ldk_out(s, v);
             if (*rg(s, v) > 0 && kov != INF && kov + 1 < ki) ki = kov + 1;
             if (ki == INF) continue;
             const int32_t w = tile[((size_t)(s - 1) * n + v) * ld + u];
@@ -424,8 +490,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           P.stats[8] = tkey;
           for (int s2 = 0; s2 < S && 2 * S * n + 16 < 2000; ++s2)
             for (int i = 0; i < n; ++i) {
-              P.stats[16 + (s2 * n + i) * 3 + 0] = *rkin(s2, i);
-              P.stats[16 + (s2 * n + i) * 3 + 1] = *rkout(s2, i);
+              P.stats[16 + (s2 * n + i) * 3 + 0] = ldk_in(s2, i);
+              P.stats[16 + (s2 * n + i) * 3 + 1] = ldk_out(s2, i);
               P.stats[16 + (s2 * n + i) * 3 + 2] = (unsigned long long)*rg(s2, i);
             }
           misc->status = 9;
@@ -440,8 +506,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           const int l = id >> 16, p = id & 0xFFFF;
           if (l == 0) return 0ull;
           if (l == Lt) return tkey;
-          if (l & 1) return *rkin((l - 1) >> 1, p);
-          return *rkout((l >> 1) - 1, p);
+          if (l & 1) return ldk_in((l - 1) >> 1, p);
+          return ldk_out((l >> 1) - 1, p);
         };
         int x = Lt << 16, len = 1, err = 0;
         if (tid == 0) path[0] = (uint32_t)x;
@@ -454,7 +520,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           if (l == Lt) {  // lowest i with out_{S-1,i} + (snk_i, 1) == key(t*)
             for (int i = tid; i < n; i += CT) {
               if (snk[i] == kAbsent) continue;
-              const uint64_t k = *rkout(S - 1, i);
+              const uint64_t k = ldk_out(S - 1, i);
               if (k != INF && k + ((uint64_t)(uint32_t)snk[i] << kHopBits) + 1ull == kx) { atomicMin(&misc->red32, i); break; }
             }
             __syncthreads();
@@ -470,7 +536,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 const int32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
                 uint64_t k4[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) k4[j] = (ws[j] != kAbsent && 4 * c + j < n) ? *rkout(s - 1, 4 * c + j) : INF;
+                for (int j = 0; j < 4; ++j) k4[j] = (ws[j] != kAbsent && 4 * c + j < n) ? ldk_out(s - 1, 4 * c + j) : INF;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                   if (k4[j] != INF && k4[j] + ((uint64_t)(uint32_t)ws[j] << kHopBits) + 1ull == kx) {
@@ -482,12 +548,12 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               if (misc->red32 != INT_MAX) pred = ((2 * s) << 16) | misc->red32;
             }
             if (pred < 0) {
-              const uint64_t ko = *rkout(s, i);
+              const uint64_t ko = ldk_out(s, i);
               if (*rg(s, i) > 0 && ko != INF && ko + 1 == kx) pred = ((2 * s + 2) << 16) | i;
             }
           } else {  // out_{s,i}: in_{s,i}, then lowest tight reverse in_{s+1,v}, then t*
             const int s = (l >> 1) - 1, i = p;
-            const uint64_t ki = *rkin(s, i);
+            const uint64_t ki = ldk_in(s, i);
             if (*rg(s, i) < *rcap(s, i) && ki != INF && ki + 1 == kx) {
               pred = ((2 * s + 1) << 16) | i;
             } else if (s < S - 1) {
@@ -497,7 +563,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 const uint32_t ent = __ldcg(&al[e]);
                 if ((int)(ent >> 20) != i) continue;
                 const int v = (int)((ent >> 8) & 0xFFFu);
-                const uint64_t k = *rkin(s + 1, v);
+                const uint64_t k = ldk_in(s + 1, v);
                 const int32_t w = tile[((size_t)s * n + v) * ld + i];
                 if (k != INF && k + 1ull == kx + ((uint64_t)(uint32_t)w << kHopBits)) atomicMin(&misc->red32, v);
               }
@@ -514,8 +580,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               P.stats[8] = tkey;
               for (int s2 = 0; s2 < S && 2 * S * n + 16 < 2000; ++s2)
                 for (int i = 0; i < n; ++i) {
-                  P.stats[16 + (s2 * n + i) * 3 + 0] = *rkin(s2, i);
-                  P.stats[16 + (s2 * n + i) * 3 + 1] = *rkout(s2, i);
+                  P.stats[16 + (s2 * n + i) * 3 + 0] = ldk_in(s2, i);
+                  P.stats[16 + (s2 * n + i) * 3 + 1] = ldk_out(s2, i);
                   P.stats[16 + (s2 * n + i) * 3 + 2] = (unsigned long long)*rg(s2, i);
                 }
             }
@@ -764,8 +830,8 @@ int ssp_cluster_size(const Problem& P) {
       default: e = launch_c<2>(P, SspOut{}, nullptr, &ncl, true); break;
     }
     if (getenv("GWTF_DEBUG"))
-      fprintf(stderr, "[gwtf] cluster size %d: smem %zu B, ring %d rows, query %s, max active clusters %d\n", C,
-              cl_layout(P, C).total, cl_layout(P, C).nbr, cudaGetErrorString(e), ncl);
+      fprintf(stderr, "[gwtf] cluster size %d: smem %zu B, ring %d chunks, query %s, max active clusters %d\n", C,
+              cl_layout(P, C).total, cl_layout(P, C).nbc, cudaGetErrorString(e), ncl);
     if (e != cudaSuccess || ncl < 1) { cudaGetLastError(); continue; }
     const long long waves = (P.B + ncl - 1) / ncl;
     const long long cost = waves * ((P.n + C - 1) / C + 16);

@@ -45,8 +45,9 @@ print(json.dumps({"config": "stress", "B": a.batch, "supply": a.supply, "ms": mi
                   "algorithmic_GBps": alg / t / 1e9, "stats": fl.stats()}))
 if os.environ.get("GWTF_DEBUG_FLAGS", "0") != "0" and int(os.environ["GWTF_DEBUG_FLAGS"]) & 16:
     raw = fl.stats(raw=True)
-    names = ["gather", "relax", "relax_vote", "tstar", "trev", "backward", "trace", "lookup", "augment", "other"]
-    cyc = raw[1100:1110].astype(float)
+    names = ["gather", "relax", "relax_vote", "tstar", "trev", "backward", "trace", "lookup", "augment", "other",
+             "r:pre-wait", "r:mbar-wait", "r:row-min", "r:epilogue"]
+    cyc = raw[1100:1114].astype(float)
     tot = cyc.sum()
     print("phase cycles (leader thread, all solves, summed over clusters):")
     for nm, c in zip(names, cyc):

@@ -273,6 +273,21 @@ def test_cluster_tier_parity_forced(name, B, C, monkeypatch):
     assert (sol.status == 0).all()
 
 
+def test_cluster_tier_stress_hops():
+    """64 x 512 stress distributions: >= 17 hop bits in the 32-bit keys, register-resident keys."""
+    cfg = gen.CONFIGS["stress_h"]
+    B = 2
+    fl, *_ = _gpu_flow(cfg, 0, B)
+    sol = fl.solve_batch()
+    nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    for b in range(B):
+        r = _oracle_ssp(cfg, bt, src, snk, link, b)
+        assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
+        assert np.array_equal(af[b], r.arc_flow) and np.array_equal(nf[b], r.node_flow), b
+    assert (sol.status == 0).all()
+
+
 def test_cluster_tier_wide_keys():
     """Arc weights too large for the cluster tier's 32-bit relaxation keys (every boundary step
     takes the 64-bit path): link costs scaled by 2^16, still exact."""
