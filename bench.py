@@ -40,7 +40,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle instances for cpu_baseline (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="skip e2e and cpu baseline (profiling runs)")
+    ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline and stress tier (profiling runs)")
+    ap.add_argument("--no-stress-tier", action="store_true", help="skip the stress-config exact-solve measurement")
     return ap.parse_args()
 
 
@@ -55,6 +56,60 @@ def algorithmic_bytes_ssp(cfg, A_total):
     bytes/augmentation = E x sizeof(cost), E = (S-1) n^2 + 2n, int32 costs."""
     E = (cfg.S - 1) * cfg.n * cfg.n + 2 * cfg.n
     return float(A_total) * E * 4
+
+
+def load_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture of this bench
+    command (profiles/<round>/traffic.json, written by scripts/ncu_traffic.py), else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)
+            if kernel in t.get("kernels", {}):
+                return t["kernels"][kernel], os.path.relpath(path, ROOT)
+        except Exception:
+            pass
+    return None, None
+
+
+def stress_tier(dev):
+    """The HBM-streaming tier on the stress config (SURVEY.md 8(d) tier G): 8 instances of 64
+    stages x 1,024 clients, M = 4,096, one cold exact solve through the cluster-tier kernel.
+    Algorithmic bytes = sum_b A_b x E x 4 (E = (S-1) n^2 + 2n int32 arc costs per augmentation)."""
+    import torch
+
+    from paper_2509_21221_b200 import Flow
+    from tests import harness
+    cfg = gen.CONFIGS["stress"]
+    bt, src, snk, link = harness.device_inputs(cfg, 0, cfg.B, device=dev)
+    fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0)
+    del link
+    torch.cuda.synchronize()
+    fl.set_profiling(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(fl.stream)
+    sol = fl.solve_batch()
+    ev1.record(fl.stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    kt = fl.kernel_times()
+    fl.set_profiling(False)
+    A = int(sol.augmentations.sum().item())
+    alg = algorithmic_bytes_ssp(cfg, A)
+    kname = "ssp_cluster_kernel" if "ssp_cluster_kernel" in kt else max(kt, key=lambda k: kt[k][0])
+    kms = kt[kname][0]
+    peak, peak_src = load_peaks()
+    tr, tsrc = load_traffic("stress:" + kname)
+    # the capture ran a supply-capped solve: its DRAM bytes per augmentation x this launch's A
+    traffic = tr["dram_bytes_per_aug"] * A if tr and "dram_bytes_per_aug" in tr else None
+    out = {"workload": workload_name(cfg), "instances": cfg.B, "solve_ms": ms, "instances_per_s": cfg.B / (ms / 1e3),
+           "augmentations": A, "status_ok": bool((sol.status == 0).all().item()),
+           "roofline": {"kernel": kname, "bound": "hbm", "achieved": alg / (kms / 1e3) / 1e9, "peak": peak,
+                        "unit": "GB/s", "frac": alg / (kms / 1e3) / 1e9 / peak, "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": alg, "traffic": traffic, "traffic_source": tsrc}}
+    fl.close()
+    return out
 
 
 def load_peaks():
@@ -240,7 +295,9 @@ def main():
     peak, peak_src = load_peaks()
     dom = max(ktimes, key=lambda k: ktimes[k][0])
     dom_ms, dom_launches = ktimes[dom]
-    roof = {"kernel": dom, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src, "traffic": None}
+    tr, tsrc = load_traffic(dom)
+    roof = {"kernel": dom, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+            "traffic": tr["dram_bytes_per_launch"] if tr else None, "traffic_source": tsrc}
     if dom == "ssp_kernel":
         alg = algorithmic_bytes_ssp(cfg, A_total)
         roof["achieved"] = alg / (dom_ms / 1e3) / 1e9
@@ -274,6 +331,8 @@ def main():
         line["e2e"] = e2e(cfg, B, inst0, dev, args)
     if rank == 0 and not (args.quick or args.no_cpu_baseline):
         line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0 and world == 1 and not (args.quick or args.no_stress_tier):
+        line["stress_tier"] = stress_tier(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -414,8 +414,9 @@ gwtf_status gwtf_flow_solve_batch(gwtf_flow_t h, int64_t* flow_value, int64_t* t
   if ((s = map_out(h, augmentations, B, 2, &o.A, maps)) != GWTF_OK) return s;
   if ((s = map_out(h, inst_status, B, 3, &o.status, maps)) != GWTF_OK) return s;
   Timer t;
-  prof_begin(h, "ssp_kernel", &t);
   const int tier = (h->flags & GWTF_FORCE_GLOBAL_TIER) ? 1 : (h->flags & GWTF_FORCE_CLUSTER_TIER) ? 2 : 0;
+  const bool cluster = tier != 1 && h->P.cluster_size > 0 && (tier == 2 || ssp_smem_bytes(h->P) > 227 * 1024);
+  prof_begin(h, cluster ? "ssp_cluster_kernel" : "ssp_kernel", &t);
   CK(h, launch_ssp(h->P, o, h->stream, h->num_sms, tier));
   prof_end(h, &t);
   h->has_assignment = true;

@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--supply", type=int, default=64)
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--rounds", type=int, default=0, help="also time decentralized_rounds(max_rounds)")
 a = ap.parse_args()
 cfg = gen.CONFIGS["stress"]
 bt = gen.generate(cfg, 0, a.batch, device="cuda")
@@ -43,6 +44,13 @@ print(json.dumps({"config": "stress", "B": a.batch, "supply": a.supply, "ms": mi
                   "F": sol.flow_value.tolist(), "cost": sol.total_cost.tolist(), "status": sol.status.tolist(),
                   "ms_per_aug_per_instance": min(ms) / max(A / a.batch, 1),
                   "algorithmic_GBps": alg / t / 1e9, "stats": fl.stats()}))
+if a.rounds:
+    ev0.record()
+    rr = fl.decentralized_rounds(a.rounds)
+    ev1.record()
+    torch.cuda.synchronize()
+    print(json.dumps({"rounds_ms": ev0.elapsed_time(ev1), "rounds_run": rr.rounds_run.tolist(),
+                      "F_dec": rr.dec_flow.tolist(), "cost_dec": rr.dec_cost.tolist()}))
 if os.environ.get("GWTF_DEBUG_FLAGS", "0") != "0" and int(os.environ["GWTF_DEBUG_FLAGS"]) & 16:
     raw = fl.stats(raw=True)
     names = ["gather", "relax", "relax_vote", "tstar", "trev", "backward", "trace", "lookup", "augment", "other",
