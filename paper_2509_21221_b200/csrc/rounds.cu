@@ -14,9 +14,14 @@
 // path).  The per-instance state either lives in global memory (L1/L2 resident; reservation
 // minima read with ld.global.cg since they are produced by L2 atomics) or is staged in
 // shared memory (tiles by TMA bulk copy) when it fits.
+#include <cooperative_groups.h>
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gwtf {
 
@@ -176,8 +181,40 @@ struct Inst {
   }
 };
 
+// A team that spans a thread-block cluster of C CTAs x 1,024 threads (stress-sized instances:
+// 64 x 1,024 relays would leave one CTA with 256 relays per thread).  Barriers are cluster
+// barriers (release/acquire; the acquire invalidates L1, so plain global loads after a barrier
+// see every CTA's writes); the OR vote goes through per-CTA DSMEM slots read by every CTA.
+template <int C>
+struct ClusterTeam {
+  static constexpr int kTPI = C * 1024;
+  int tid, id;
+  uint32_t* vslot;  // this CTA's two vote slots (shared memory)
+  uint32_t vid;     // vote counter (uniform over the cluster)
+  __device__ __forceinline__ void sync() const { cg::this_cluster().sync(); }
+  __device__ int sync_or(int p) {
+    const int any = __syncthreads_or(p);
+    ++vid;
+    if (threadIdx.x == 0) vslot[vid & 1] = any ? vid : 0u;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    int res = 0;
+    for (int q = 0; q < C; ++q) res |= cl.map_shared_rank(vslot, q)[vid & 1] == vid;
+    return res;
+  }
+};
 template <int TPI>
-__device__ void compute_costs(const Team<TPI>& T, const Inst& I) {
+struct TeamOf {  // adapter giving Team<TPI> the same interface
+  static constexpr int kTPI = TPI;
+  Team<TPI> t;
+  int tid, id;
+  __device__ __forceinline__ void sync() const { t.sync(); }
+  __device__ __forceinline__ int sync_or(int p) const { return t.sync_or(p); }
+};
+
+template <class TT>
+__device__ void compute_costs(TT& T, const Inst& I) {
+  constexpr int TPI = TT::kTPI;
   const int per = I.n * I.MC;
   for (int s = I.S - 1; s >= 0; --s) {
     for (int t = T.tid; t < per; t += TPI) {
@@ -206,7 +243,7 @@ __host__ __device__ inline bool rounds_tile_in_smem(const Problem& P) {
 }
 struct RoundsLayout {
   size_t res, scost, adv_cost, pkey, up, down, src_down, snk_up, kacc, deny, req_slot, req_target, grant, prop,
-      ptouch, capv, summ, tile, total;
+      ptouch, capv, summ, tile, mbar, cells, total;
 };
 // smem: everything of one instance; otherwise only the per-instance scratch (the state
 // arrays then live in the handle's global buffers)
@@ -232,7 +269,9 @@ __host__ __device__ inline RoundsLayout rounds_layout(const Problem& P, bool sme
   L.capv = o; o += al16r(Sn * 4);
   L.summ = o; o += al16r(Sn * 4);
   L.tile = o; if (smem && rounds_tile_in_smem(P)) o += al16r((size_t)(P.S > 1 ? P.S - 1 : 0) * P.n * P.ld * 4);
-  L.total = o + 16;  // + mbarrier
+  L.mbar = o; o += 16;
+  L.cells = o; o += 64;  // the cluster team's reduction cells
+  L.total = o;
   return L;
 }
 
@@ -247,29 +286,32 @@ __device__ __forceinline__ void st_res(uint64_t* p, uint64_t v) {
   else __stcg(p, v);
 }
 
-template <int TPI, bool kSmem>
-__global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const RoundsOut o, const size_t ws_bytes) {
-  extern __shared__ __align__(128) uint8_t dsm[];
-  __shared__ uint64_t sh_u64[8][2];
-  __shared__ int sh_i32[8][4];
-  __shared__ int sh_inst[8];
-  __shared__ int tma_init[8];
-  __shared__ uint32_t tma_phase_of[8];
-  if (threadIdx.x < 8) { tma_init[threadIdx.x] = 0; tma_phase_of[threadIdx.x] = 0; }
-  __syncthreads();
-  const Team<TPI> T{(int)(threadIdx.x % TPI), (int)(threadIdx.x / TPI)};
+// Team reduction cells: shared memory for CTA teams, the team workspace (global, L2 atomics)
+// for cluster teams.  [0..1] u64 sums, [0..3] i32 min/or/sum, instance index.
+struct Red {
+  unsigned long long* u64;
+  int* i32;
+  int* inst;
+};
+
+template <class TT, bool kSmem>
+__device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o, const size_t ws_bytes, TT& T,
+                                            uint8_t* base, Red red, uint8_t* dsm, int* tma_init,
+                                            uint32_t* tma_phase_of) {
+  constexpr int TPI = TT::kTPI;
+  constexpr bool kCl = TPI > 1024;
   const int lane = threadIdx.x & 31;
   const int S = P.S, n = P.n, MC = P.MC, Sn = S * n;
   const int nres = Sn * MC + 2 * (int)P.Mmax;
-  const int teams_per_cta = blockDim.x / TPI;
   const RoundsLayout Lr = rounds_layout(P, kSmem);
-  uint8_t* base = kSmem ? dsm + (size_t)T.id * ws_bytes
-                        : P.ws_rounds + (size_t)(blockIdx.x * teams_per_cta + T.id) * ws_bytes;
+  unsigned long long* const sh_u64 = red.u64;
+  int* const sh_i32 = red.i32;
 
   for (;;) {
-    if (T.tid == 0) sh_inst[T.id] = atomicAdd(&P.counters[1], 1);
+    if (T.tid == 0) *(volatile int*)red.inst = atomicAdd(&P.counters[1], 1);
     T.sync();
-    const int b = sh_inst[T.id];
+    const int b = *(volatile int*)red.inst;
+    T.sync();  // every thread of the team has read it before it can be rewritten
     if (b >= P.B) break;
     Inst I;
     I.P = &P; I.S = S; I.n = n; I.ld = P.ld; I.MC = MC; I.Sn = Sn; I.inst = b;
@@ -307,7 +349,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
     int32_t* g_kacc = I.kacc;
     int32_t* g_deny = I.deny;
     if constexpr (kSmem) {  // stage the round state (and small tiles, by TMA) in shared memory
-      uint64_t* mbar = (uint64_t*)(base + Lr.total - 16);
+      uint64_t* mbar = (uint64_t*)(base + Lr.mbar);
       I.up = (int32_t*)(base + Lr.up);
       I.down = (int32_t*)(base + Lr.down);
       I.src_down = (int32_t*)(base + Lr.src_down);
@@ -348,7 +390,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       int changed = 0;
       I.set_round(round);
       // ---------- R0a candidates: a relay holding an IN and an OUT slot ----------
-      if (T.tid == 0) { sh_i32[T.id][0] = INT_MAX; sh_i32[T.id][1] = 0; }
+      if (T.tid == 0) { sh_i32[0] = INT_MAX; sh_i32[1] = 0; }
       int cand = 0;
       for (int v = T.tid; v < Sn; v += TPI) {
         const uint32_t w = I.summarize(v);
@@ -377,7 +419,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       }
       // ---------- R0 cost to sink + advertisements; data-node slots ----------
       if (cost_mode == 0) {  // stage-synchronous back-to-front recursion, then advertisements
-        compute_costs(T, I);
+        compute_costs<TT>(T, I);
         for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
       } else if (cost_mode == 1) {  // one chain walk per slot, then advertisements
         for (int t = T.tid; t < Sn * MC; t += TPI) I.slot_cost(t);
@@ -392,12 +434,12 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
           if (I.src_down[k] == kNone && k < fs) fs = k;
           anyfree |= I.snk_up[k] == kNone;
         }
-        if (fs != INT_MAX) atomicMin(&sh_i32[T.id][0], fs);
-        if (anyfree) atomicOr(&sh_i32[T.id][1], 1);
+        if (fs != INT_MAX) atomicMin(&sh_i32[0], fs);
+        if (anyfree) atomicOr(&sh_i32[1], 1);
       }
       T.sync();
-      const int d_rslot = sh_i32[T.id][0];
-      const int dsink_free = sh_i32[T.id][1];
+      const int d_rslot = *(volatile int*)&sh_i32[0];
+      const int dsink_free = *(volatile int*)&sh_i32[1];
       // ---------- R1 requests (one per node) ----------
       for (int rr = T.tid; rr <= Sn; rr += TPI) {
         int32_t rs = kNone, tg = -2;
@@ -628,7 +670,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
       quiet = any ? 0 : quiet + 1;
       round += 1;
       if (o.digests) {
-        if (T.tid == 0) sh_u64[T.id][0] = 0;
+        if (T.tid == 0) sh_u64[0] = 0;
         T.sync();
         uint64_t acc = 0;
         const int nslot = Sn * MC;
@@ -651,9 +693,9 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
         }
         if (T.tid == 0) acc += digest_elem(b4, (uint64_t)(uint32_t)quiet);
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) atomicAdd((unsigned long long*)&sh_u64[T.id][0], (unsigned long long)acc);
+        if (lane == 0) atomicAdd(&sh_u64[0], (unsigned long long)acc);
         T.sync();
-        if (T.tid == 0) o.digests[(size_t)b * o.max_rounds + r] = sh_u64[T.id][0];
+        if (T.tid == 0) o.digests[(size_t)b * o.max_rounds + r] = *(volatile unsigned long long*)&sh_u64[0];
       }
       ++r;
       if (quiet >= P.W) break;
@@ -661,7 +703,7 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
     if (o.digests)
       for (int k = r + T.tid; k < o.max_rounds; k += TPI) o.digests[(size_t)b * o.max_rounds + k] = 0;
     // ---------- results: complete SRC -> SNK chains and dangling outflows ----------
-    if (T.tid == 0) { sh_u64[T.id][0] = 0; sh_u64[T.id][1] = 0; sh_i32[T.id][3] = 0; }
+    if (T.tid == 0) { sh_u64[0] = 0; sh_u64[1] = 0; sh_i32[3] = 0; }
     T.sync();
     {
       unsigned long long f = 0, c = 0;
@@ -687,9 +729,9 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
         dg += __shfl_xor_sync(0xffffffffu, dg, off);
       }
       if (lane == 0) {
-        atomicAdd((unsigned long long*)&sh_u64[T.id][0], f);
-        atomicAdd((unsigned long long*)&sh_u64[T.id][1], c);
-        atomicAdd(&sh_i32[T.id][3], dg);
+        atomicAdd(&sh_u64[0], f);
+        atomicAdd(&sh_u64[1], c);
+        atomicAdd(&sh_i32[3], dg);
       }
     }
     T.sync();
@@ -700,14 +742,48 @@ __global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const Roun
     }
     if (T.tid == 0) {
       if (o.rounds_run) o.rounds_run[b] = r;
-      if (o.F_dec) o.F_dec[b] = (int64_t)sh_u64[T.id][0];
-      if (o.cost_dec) o.cost_dec[b] = (int64_t)sh_u64[T.id][1];
-      if (o.dangling) o.dangling[b] = sh_i32[T.id][3];
+      if (o.F_dec) o.F_dec[b] = (int64_t)*(volatile unsigned long long*)&sh_u64[0];
+      if (o.cost_dec) o.cost_dec[b] = (int64_t)*(volatile unsigned long long*)&sh_u64[1];
+      if (o.dangling) o.dangling[b] = *(volatile int*)&sh_i32[3];
       P.quiet[b] = quiet;
       P.round[b] = (int64_t)round;
     }
     T.sync();
   }
+}
+
+template <int TPI, bool kSmem>
+__global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const RoundsOut o, const size_t ws_bytes) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ unsigned long long sh_u64[8][2];
+  __shared__ int sh_i32[8][4];
+  __shared__ int sh_inst[8];
+  __shared__ int tma_init[8];
+  __shared__ uint32_t tma_phase_of[8];
+  if (threadIdx.x < 8) { tma_init[threadIdx.x] = 0; tma_phase_of[threadIdx.x] = 0; }
+  __syncthreads();
+  TeamOf<TPI> T{{(int)(threadIdx.x % TPI), (int)(threadIdx.x / TPI)}, (int)(threadIdx.x % TPI), (int)(threadIdx.x / TPI)};
+  const int teams_per_cta = blockDim.x / TPI;
+  uint8_t* base = kSmem ? dsm + (size_t)T.id * ws_bytes
+                        : P.ws_rounds + (size_t)(blockIdx.x * teams_per_cta + T.id) * ws_bytes;
+  rounds_body<TeamOf<TPI>, kSmem>(P, o, ws_bytes, T, base, Red{sh_u64[T.id], sh_i32[T.id], &sh_inst[T.id]}, dsm,
+                                  tma_init, tma_phase_of);
+}
+
+// cluster tier of the rounds: one cluster of C CTAs x 1,024 threads per instance, state and
+// scratch in the global workspace (one per cluster; its last 64 bytes hold the reduction cells)
+template <int C>
+__global__ void __launch_bounds__(1024, 1) rounds_cluster_kernel(const Problem P, const RoundsOut o, const size_t ws_bytes) {
+  __shared__ uint32_t vslot[2];
+  if (threadIdx.x < 2) vslot[threadIdx.x] = 0;
+  cg::cluster_group cl = cg::this_cluster();
+  ClusterTeam<C> T{(int)(cl.block_rank() * 1024 + threadIdx.x), 0, vslot, 0u};
+  uint8_t* base = P.ws_rounds + (size_t)(blockIdx.x / C) * ws_bytes;
+  uint8_t* cells = base + rounds_layout(P, false).cells;
+  cl.sync();
+  rounds_body<ClusterTeam<C>, false>(P, o, ws_bytes, T, base,
+                                     Red{(unsigned long long*)cells, (int*)(cells + 16), (int*)(cells + 32)},
+                                     nullptr, nullptr, nullptr);
 }
 
 __global__ void init_round_state_kernel(const Problem P) {
@@ -748,6 +824,65 @@ cudaError_t launch_rounds_tpi(const Problem& P, const RoundsOut& o, cudaStream_t
   return cudaGetLastError();
 }
 
+template <int C>
+cudaError_t launch_rounds_cluster(const Problem& P, const RoundsOut& o, cudaStream_t st, int* ncl_out, bool query) {
+  const size_t ws = rounds_layout(P, false).total;
+  auto k = rounds_cluster_kernel<C>;
+  cudaError_t e;
+  if (C > 8) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(1024);
+  cfg.gridDim = dim3(C);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  e = cudaOccupancyMaxActiveClusters(&ncl, (void*)k, &cfg);
+  if (e != cudaSuccess) return e;
+  if (ncl < 1) return cudaErrorInvalidConfiguration;
+  if (ncl > P.B) ncl = P.B;
+  if (ncl > P.ws_rounds_teams) ncl = P.ws_rounds_teams;
+  if (ncl_out) *ncl_out = ncl;
+  if (query) return cudaSuccess;
+  cfg.gridDim = dim3(ncl * C);
+  return cudaLaunchKernelEx(&cfg, k, P, o, ws);
+}
+
+// instances with more relay slots than a 256-thread team handles well run on clusters
+bool rounds_use_cluster(const Problem& P) {
+  const int f = getenv_int("GWTF_ROUNDS_CLUSTER", -1);
+  if (f >= 0) return f > 0;
+  return (long long)P.S * P.n * std::max(P.MC, 1) > 32768;
+}
+
+// cluster size of the rounds: smallest waves x (relays per thread + fixed barrier cost)
+int rounds_cluster_size(const Problem& P) {
+  if (const char* f = getenv("GWTF_ROUNDS_CLUSTER_SIZE")) return atoi(f);
+  int best = 0;
+  long long best_cost = 0;
+  for (int C : {16, 8, 4, 2}) {
+    int ncl = 0;
+    cudaError_t e = C == 16 ? launch_rounds_cluster<16>(P, RoundsOut{}, nullptr, &ncl, true)
+                  : C == 8  ? launch_rounds_cluster<8>(P, RoundsOut{}, nullptr, &ncl, true)
+                  : C == 4  ? launch_rounds_cluster<4>(P, RoundsOut{}, nullptr, &ncl, true)
+                            : launch_rounds_cluster<2>(P, RoundsOut{}, nullptr, &ncl, true);
+    if (e != cudaSuccess || ncl < 1) { cudaGetLastError(); continue; }
+    const long long waves = (P.B + ncl - 1) / ncl;
+    const long long per = ((long long)P.S * P.n + C * 1024 - 1) / (C * 1024);
+    const long long cost = waves * (per + 2);
+    if (best == 0 || cost < best_cost) { best = C; best_cost = cost; }
+  }
+  return best;
+}
+
 }  // namespace
 
 size_t rounds_ws_bytes(const Problem& P, bool smem) { return rounds_layout(P, smem).total; }
@@ -774,6 +909,13 @@ cudaError_t launch_rounds(const Problem& P0, const RoundsOut& o, cudaStream_t st
   if (e != cudaSuccess) return e;
   const int tpi = rounds_tpi(P);
   const bool smem = rounds_use_smem(P);
+  if (!smem && rounds_use_cluster(P)) {
+    const int C = rounds_cluster_size(P);
+    if (C == 16) return launch_rounds_cluster<16>(P, o, st, nullptr, false);
+    if (C == 8) return launch_rounds_cluster<8>(P, o, st, nullptr, false);
+    if (C == 4) return launch_rounds_cluster<4>(P, o, st, nullptr, false);
+    if (C == 2) return launch_rounds_cluster<2>(P, o, st, nullptr, false);
+  }
   if (tpi <= 32) return launch_rounds_tpi<32>(P, o, st, num_sms, smem);
   if (tpi <= 64) return launch_rounds_tpi<64>(P, o, st, num_sms, smem);
   if (tpi <= 128) return launch_rounds_tpi<128>(P, o, st, num_sms, smem);

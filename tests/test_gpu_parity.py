@@ -125,6 +125,34 @@ def test_rounds_digest_parity(name, B):
         assert int(st["round"][b]) == ost["round"]
 
 
+@pytest.mark.parametrize("name,B,C", [("churn", 4, None), ("llama", 3, 4), ("flow3", 8, 2), ("gpt", 6, 16),
+                                      ("stress_s", 2, None)])
+def test_rounds_cluster_tier_parity(name, B, C, monkeypatch):
+    """The rounds on thread-block-cluster teams (C CTAs x 1,024 threads per instance, cluster
+    barriers, DSMEM votes): round-by-round digests and final state equal the oracle's."""
+    monkeypatch.setenv("GWTF_ROUNDS_GLOBAL", "1")
+    monkeypatch.setenv("GWTF_ROUNDS_CLUSTER", "1")
+    if C is not None:
+        monkeypatch.setenv("GWTF_ROUNDS_CLUSTER_SIZE", str(C))
+    cfg = gen.CONFIGS[name]
+    fl, *_ = _gpu_flow(cfg, 0, B, seed=17)
+    rr = fl.decentralized_rounds(cfg.max_rounds, digests=True)
+    st = fl.export_round_state()
+    torch.cuda.synchronize()
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    for b in range(B):
+        I = oracle.instance_from_batch(bt, b, link[b], src[b], snk[b])
+        R = oracle.Rounds(I, seed=17, inst_id=b)
+        o = R.run(cfg.max_rounds, digests=True)
+        n_r = int(rr.rounds_run[b])
+        assert n_r == o["rounds"], (name, b)
+        got = rr.digests[b, :n_r].cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, o["digests"]), (name, b, int(np.argmax(got != o["digests"])))
+        assert (int(rr.dec_flow[b]), int(rr.dec_cost[b]), int(rr.dangling[b])) == (o["F_dec"], o["cost_dec"], o["dangling"])
+        ost = R.export()
+        assert np.array_equal(st["up"][b].cpu().numpy(), ost["up"]) and np.array_equal(st["down"][b].cpu().numpy(), ost["down"])
+
+
 @pytest.mark.parametrize("objective", [0, 1])
 def test_rounds_parity_minimax_and_annealing_off(objective):
     cfg = gen.CONFIGS["flow2"]
