@@ -94,6 +94,11 @@ def stress_tier(dev):
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     kt = fl.kernel_times()
+    ev0.record(fl.stream)
+    rr = fl.decentralized_rounds(cfg.max_rounds)  # cold, to steady state (W = 5) or max_rounds
+    ev1.record(fl.stream)
+    torch.cuda.synchronize()
+    rms = ev0.elapsed_time(ev1)
     fl.set_profiling(False)
     A = int(sol.augmentations.sum().item())
     alg = algorithmic_bytes_ssp(cfg, A)
@@ -103,8 +108,13 @@ def stress_tier(dev):
     tr, tsrc = load_traffic("stress:" + kname)
     # the capture ran a supply-capped solve: its DRAM bytes per augmentation x this launch's A
     traffic = tr["dram_bytes_per_aug"] * A if tr and "dram_bytes_per_aug" in tr else None
-    out = {"workload": workload_name(cfg), "instances": cfg.B, "solve_ms": ms, "instances_per_s": cfg.B / (ms / 1e3),
-           "augmentations": A, "status_ok": bool((sol.status == 0).all().item()),
+    out = {"workload": workload_name(cfg), "instances": cfg.B, "solve_ms": ms, "rounds_ms": rms,
+           "instances_per_s": cfg.B / ((ms + rms) / 1e3), "ssp_instances_per_s": cfg.B / (ms / 1e3),
+           "rounds_instances_per_s": cfg.B / (rms / 1e3), "augmentations": A,
+           "rounds_run": [int(x) for x in rr.rounds_run.tolist()], "max_rounds": cfg.max_rounds,
+           "F": int(sol.flow_value.sum().item()), "cost": int(sol.total_cost.sum().item()),
+           "F_dec": int(rr.dec_flow.sum().item()), "cost_dec": int(rr.dec_cost.sum().item()),
+           "status_ok": bool((sol.status == 0).all().item()),
            "roofline": {"kernel": kname, "bound": "hbm", "achieved": alg / (kms / 1e3) / 1e9, "peak": peak,
                         "unit": "GB/s", "frac": alg / (kms / 1e3) / 1e9 / peak, "peak_source": peak_src,
                         "algorithmic_bytes_per_launch": alg, "traffic": traffic, "traffic_source": tsrc}}

@@ -753,7 +753,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
 }
 
 template <int TPI, bool kSmem>
-__global__ void __launch_bounds__(256) rounds_kernel(const Problem P, const RoundsOut o, const size_t ws_bytes) {
+__global__ void __launch_bounds__(256, 4) rounds_kernel(const Problem P, const RoundsOut o, const size_t ws_bytes) {
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ unsigned long long sh_u64[8][2];
   __shared__ int sh_i32[8][4];

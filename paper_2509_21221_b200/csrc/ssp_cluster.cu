@@ -47,6 +47,7 @@ struct Misc {  // per-CTA control block; the leader's copy is authoritative
   int32_t inst, A, status, pathlen;
   uint32_t votes[2];  // alternating slots: a CTA is at most one phase ahead of the slowest
   int32_t red32, pred, nrem;
+  uint32_t p2;  // 1 << H32, read back through a volatile load (see the relaxation)
 };
 
 struct ClLayout {
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   auto rsnkf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(snkf, q) + (v - q * R); };
 
   if (tid == 0) {
+    misc->p2 = 1u << H32;
     for (int b = 0; b < nbc; ++b) { mbar_init(&mbar[b], 1); ecnt[b] = 0; }
     fence_barrier_init();
   }
@@ -147,6 +149,18 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   } while (0)
   int slot0 = 0;          // ring slot of the next chunk (uniform over the CTA)
   uint64_t php = 0;       // per-slot mbarrier phase parity (uniform over the CTA)
+  int pf_s = -1, pf_n = 0;  // boundary whose first pf_n chunks were streamed ahead (uniform)
+  // wait out the chunks streamed ahead for a boundary that is not next after all
+  auto drain = [&]() {
+    for (int k = 0, b = slot0; k < pf_n; ++k, b = b + 1 == nbc ? 0 : b + 1) {
+      mbar_wait(&mbar[b], (uint32_t)(php >> b) & 1u);
+      php ^= 1ull << b;
+    }
+    slot0 = (slot0 + pf_n) % nbc;
+    pf_s = -1;
+    pf_n = 0;
+    __syncthreads();  // every warp is past the waits before a slot is re-armed
+  };
   uint32_t vote_id = 0;   // phase counter of the votes (uniform over the cluster)
   uint32_t tphase = 0;    // phase counter of the t* reductions
   __syncthreads();
@@ -213,21 +227,35 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           fwd &= ~(1ull << s);
           if (r == 0 && tid == 0) atomicAdd(&P.stats[0], 1ull);
           TMARK(9);
-          const uint8_t* rows = t16 ? (const uint8_t*)(P.tile16 + (((size_t)inst * (S - 1) + s) * n + v0) * P.ld16)
-                                    : (const uint8_t*)(tile + ((size_t)s * n + v0) * ld);
           // chunk k (rows k*NW .. k*NW+NW-1, one per warp) goes to slot (slot0 + k) % nbc; the last
-          // warp to finish a chunk refills its slot with chunk k + nbc
+          // warp to finish a chunk refills its slot with chunk k + nbc, or, past the last chunk,
+          // with chunk k + nbc - nch of boundary s + 1: the forward sweep's likely next step is
+          // streamed across the vote (speculative; a mismatch drains it)
           const int nch = (nr + NW - 1) / NW;
           const uint32_t cbytes = (uint32_t)NW * rowbytes;
-          auto issue = [&](int k, int b) {  // chunk k into slot b
+          auto rows_of = [&](int sb) -> const uint8_t* {
+            return t16 ? (const uint8_t*)(P.tile16 + (((size_t)inst * (S - 1) + sb) * n + v0) * P.ld16)
+                       : (const uint8_t*)(tile + ((size_t)sb * n + v0) * ld);
+          };
+          const uint8_t* rows = rows_of(s);
+          auto issue_from = [&](const uint8_t* src, int k, int b) {  // chunk k of `src` into slot b
             const uint32_t bytes = (uint32_t)min(NW, nr - k * NW) * rowbytes;
             mbar_arrive_expect_tx(&mbar[b], bytes);
-            bulk_g2s(ring + (size_t)b * cbytes, rows + (size_t)k * cbytes, bytes, &mbar[b]);
+            bulk_g2s(ring + (size_t)b * cbytes, src + (size_t)k * cbytes, bytes, &mbar[b]);
           };
+          auto issue = [&](int k, int b) { issue_from(rows, k, b); };
           const bool nostream = P.debug & 64;  // testing: time the compute without the stream
+          if (pf_n && pf_s != s) drain();     // the speculation missed
+          const int pre = pf_n;                // chunks of this boundary already in flight
+          const int nxt = (s + 2 < S && !nostream && !(P.debug & 512)) ? s + 1 : -1;
+          const uint8_t* rows_next = nxt >= 0 ? rows_of(nxt) : nullptr;
+          pf_s = nxt;
+          pf_n = nxt >= 0 ? min(nbc, nch) : 0;
           if (tid == 0 && !nostream) {
             fence_proxy_async_smem();
-            for (int k = 0; k < min(nbc, nch); ++k) issue(k, slot0 + k < nbc ? slot0 + k : slot0 + k - nbc);
+            for (int k = pre; k < min(nbc, nch); ++k) issue(k, slot0 + k < nbc ? slot0 + k : slot0 + k - nbc);
+            for (int k2 = 0; k2 < pf_n && k2 + nch < nbc; ++k2)  // free slots: next boundary now
+              issue_from(rows_next, k2, (slot0 + nch + k2) % nbc);
           }
           // lane k of warp w prefetches the keys of the warp's row j = k * NW + w of in/out_{s+1}
           // (consumed by lane k after the row's minimum; rows beyond 32 per warp load late)
@@ -285,29 +313,33 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             const uint8_t* rowb = ring + (size_t)b * cbytes + (size_t)warp * rowbytes;
             uint64_t best;
             if (!wide) {
-              // 32-bit: per weight one clamp, one shift and one DPX add-min (VIADDMNMX); four
+              // 32-bit: per weight one shift, one add and one min (IADD + VIMNMX, full rate; the fused
+              // DPX VIADDMNMX issues at a quarter of that rate on sm_100a); four
               // independent accumulators keep the add-min chains short
               const uint4* kv4 = (const uint4*)kb32;
               uint32_t a0 = 0xFFFFFFFFu, a1 = a0, a2 = a0, a3 = a0;
+              // (w << H32) + key as one IMAD by p2 = 2^H32, opaque to ptxas: it would otherwise turn it
+              // into shift + add and fuse the add with the min into the quarter-rate DPX VIADDMNMX
+              const uint32_t p2 = *(volatile const uint32_t*)&misc->p2;
               if (t16) {
                 // 16-bit rows, pre-clamped (absent = T32): two weights per word, shifted into the
                 // cost field; with H32 >= 16 the low weight is one shift, the high one shift + mask
                 const uint4* row = (const uint4*)rowb;
                 const uint32_t hm = ~((1u << H32) - 1u);
                 if (kreg && H32 >= 16) {
-                  const int hs = H32 - 16;
+                  // IMAD + VIMNMX: 3 issue slots per weight against 5 for SHF + VIADDMNMX
 #pragma unroll
                   for (int q = 0; q < KQ; ++q) {
                     if (lane + 32 * q < ldk / 8) {
                       const uint4 w = row[lane + 32 * q];
-                      a0 = __viaddmin_u32(kr[2 * q].x, w.x << H32, a0);
-                      a1 = __viaddmin_u32(kr[2 * q].y, (w.x << hs) & hm, a1);
-                      a2 = __viaddmin_u32(kr[2 * q].z, w.y << H32, a2);
-                      a3 = __viaddmin_u32(kr[2 * q].w, (w.y << hs) & hm, a3);
-                      a0 = __viaddmin_u32(kr[2 * q + 1].x, w.z << H32, a0);
-                      a1 = __viaddmin_u32(kr[2 * q + 1].y, (w.z << hs) & hm, a1);
-                      a2 = __viaddmin_u32(kr[2 * q + 1].z, w.w << H32, a2);
-                      a3 = __viaddmin_u32(kr[2 * q + 1].w, (w.w << hs) & hm, a3);
+                      a0 = min(a0, w.x * p2 + kr[2 * q].x);          // low half: bits above 32 drop
+                      a1 = min(a1, (w.x >> 16) * p2 + kr[2 * q].y);
+                      a2 = min(a2, w.y * p2 + kr[2 * q].z);
+                      a3 = min(a3, (w.y >> 16) * p2 + kr[2 * q].w);
+                      a0 = min(a0, w.z * p2 + kr[2 * q + 1].x);
+                      a1 = min(a1, (w.z >> 16) * p2 + kr[2 * q + 1].y);
+                      a2 = min(a2, w.w * p2 + kr[2 * q + 1].z);
+                      a3 = min(a3, (w.w >> 16) * p2 + kr[2 * q + 1].w);
                     }
                   }
                 } else {
@@ -315,14 +347,14 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                   for (int c = lane; c < ldk / 8; c += 32) {
                     const uint4 w = row[c];
                     const uint4 ka = kv4[2 * c], kc = kv4[2 * c + 1];
-                    a0 = __viaddmin_u32(ka.x, (w.x & 0xFFFFu) << H32, a0);
-                    a1 = __viaddmin_u32(ka.y, (w.x >> 16) << H32, a1);
-                    a2 = __viaddmin_u32(ka.z, (w.y & 0xFFFFu) << H32, a2);
-                    a3 = __viaddmin_u32(ka.w, (w.y >> 16) << H32, a3);
-                    a0 = __viaddmin_u32(kc.x, (w.z & 0xFFFFu) << H32, a0);
-                    a1 = __viaddmin_u32(kc.y, (w.z >> 16) << H32, a1);
-                    a2 = __viaddmin_u32(kc.z, (w.w & 0xFFFFu) << H32, a2);
-                    a3 = __viaddmin_u32(kc.w, (w.w >> 16) << H32, a3);
+                    a0 = min(a0, (w.x & 0xFFFFu) * p2 + ka.x);
+                    a1 = min(a1, (w.x >> 16) * p2 + ka.y);
+                    a2 = min(a2, (w.y & 0xFFFFu) * p2 + ka.z);
+                    a3 = min(a3, (w.y >> 16) * p2 + ka.w);
+                    a0 = min(a0, (w.z & 0xFFFFu) * p2 + kc.x);
+                    a1 = min(a1, (w.z >> 16) * p2 + kc.y);
+                    a2 = min(a2, (w.w & 0xFFFFu) * p2 + kc.z);
+                    a3 = min(a3, (w.w >> 16) * p2 + kc.w);
                   }
                 }
               } else {
@@ -331,10 +363,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 for (int c = lane; c < ld / 4; c += 32) {
                   const int4 w = row[c];
                   const uint4 kq = kv4[c];
-                  a0 = __viaddmin_u32(kq.x, min((uint32_t)w.x, T32) << H32, a0);
-                  a1 = __viaddmin_u32(kq.y, min((uint32_t)w.y, T32) << H32, a1);
-                  a2 = __viaddmin_u32(kq.z, min((uint32_t)w.z, T32) << H32, a2);
-                  a3 = __viaddmin_u32(kq.w, min((uint32_t)w.w, T32) << H32, a3);
+                  a0 = min(a0, min((uint32_t)w.x, T32) * p2 + kq.x);
+                  a1 = min(a1, min((uint32_t)w.y, T32) * p2 + kq.y);
+                  a2 = min(a2, min((uint32_t)w.z, T32) * p2 + kq.z);
+                  a3 = min(a3, min((uint32_t)w.w, T32) * p2 + kq.w);
                 }
               }
               const uint32_t acc = __reduce_min_sync(0xffffffffu, min(min(a0, a1), min(a2, a3)));
@@ -388,11 +420,13 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             // every lane is done with its row of slot b (its values fed the warp minimum); the
             // last warp to finish the chunk refills the slot through the async proxy
             php ^= 1ull << b;  // slot b's phase advanced (every thread tracks every chunk)
-            if (lane == 0 && k + nbc < nch && !nostream) {
+            const int k2 = k + nbc - nch;  // chunk of the next boundary that reuses slot b
+            if (lane == 0 && !nostream && (k + nbc < nch || (k2 >= 0 && k2 < pf_n))) {
               if (atomicAdd(&ecnt[b], 1u) % NW == NW - 1) {  // last reader of the chunk
                 __threadfence_block();
                 fence_proxy_async_smem();
-                issue(k + nbc, b);
+                if (k + nbc < nch) issue(k + nbc, b);
+                else issue_from(rows_next, k2, b);
               }
             }
           }
@@ -746,6 +780,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
       cl.sync();
     }
 
+    drain();  // nothing may stay in flight past the instance (or the kernel)
     // ---- results and the canonical assignment ----
     if (r == 0 && tid == 0) {
       o.F[inst] = misc->F;
