@@ -306,6 +306,63 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           }
           TMARK(0);
           int ch = 0;
+          // the lane holding row j's prefetched keys applies its minimum (and the fused node arc)
+          auto apply = [&](int k, int j, uint64_t best) {
+            if (lane != (k & 31)) return;
+            const int e = (s + 1) * R + j;
+            uint64_t kv = pkv, ko = pko;
+            int res = pres;
+            if (k >= 32) { kv = kin[e]; ko = kout[e]; res = g[e] < capE[e]; }
+            if (best < kv) { kin[e] = best; kv = best; ch = 1; }
+            if (kv != INF && res && kv + 1 < ko) { kout[e] = kv + 1; ch = 1; }
+          };
+          // every lane is done with its row of slot b (its values fed the warp minimum); the last
+          // warp to finish the chunk refills the slot through the async proxy
+          auto release = [&](int k, int b) {
+            php ^= 1ull << b;  // slot b's phase advanced (every thread tracks every chunk)
+            const int k2 = k + nbc - nch;  // chunk of the next boundary that reuses slot b
+            if (lane == 0 && !nostream && (k + nbc < nch || (k2 >= 0 && k2 < pf_n))) {
+              if (atomicAdd(&ecnt[b], 1u) % NW == NW - 1) {  // last reader of the chunk
+                __threadfence_block();
+                fence_proxy_async_smem();
+                if (k + nbc < nch) issue(k + nbc, b);
+                else issue_from(rows_next, k2, b);
+              }
+            }
+          };
+          const uint32_t p2 = *(volatile const uint32_t*)&misc->p2;  // 2^H32, opaque to ptxas (below)
+          if (t16 && kreg && H32 >= 16 && ldk == 8 * 32 * KQ && !wide && !nostream) {
+            // the stress fast path: 1,024-weight 16-bit rows, register-resident 32-bit keys, no
+            // predicates.  (w << H32) + key is one IMAD by p2 (ptxas would otherwise fuse a shift's
+            // add with the min into the quarter-rate DPX VIADDMNMX); the low half-word needs no
+            // mask (its high bits leave the register), the high one a shift.
+            for (int k = 0, b = slot0; k < nch; ++k, b = b + 1 == nbc ? 0 : b + 1) {
+              const int j = k * NW + warp;
+              if (j < nr) {
+                mbar_wait(&mbar[b], (uint32_t)(php >> b) & 1u);
+                const uint4* row = (const uint4*)(ring + (size_t)b * cbytes + (size_t)warp * rowbytes) + lane;
+                uint4 w[KQ];
+#pragma unroll
+                for (int q = 0; q < KQ; ++q) w[q] = row[32 * q];
+                uint32_t a0 = 0xFFFFFFFFu, a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+                for (int q = 0; q < KQ; ++q) {
+                  a0 = min(a0, w[q].x * p2 + kr[2 * q].x);
+                  a1 = min(a1, (w[q].x >> 16) * p2 + kr[2 * q].y);
+                  a2 = min(a2, w[q].y * p2 + kr[2 * q].z);
+                  a3 = min(a3, (w[q].y >> 16) * p2 + kr[2 * q].w);
+                  a0 = min(a0, w[q].z * p2 + kr[2 * q + 1].x);
+                  a1 = min(a1, (w[q].z >> 16) * p2 + kr[2 * q + 1].y);
+                  a2 = min(a2, w[q].w * p2 + kr[2 * q + 1].z);
+                  a3 = min(a3, (w[q].w >> 16) * p2 + kr[2 * q + 1].w);
+                }
+                const uint32_t acc = __reduce_min_sync(0xffffffffu, min(min(a0, a1), min(a2, a3)));
+                apply(k, j, (acc >> H32) >= T32 ? INF
+                                                : ((uint64_t)(acc >> H32) << kHopBits) | (uint64_t)(acc & ((1u << H32) - 1u)));
+              }
+              release(k, b);
+            }
+          } else
           for (int k = 0, b = slot0; k < nch; ++k, b = b + 1 == nbc ? 0 : b + 1) {
             const int j = k * NW + warp;
             if (j < nr) {
@@ -318,9 +375,6 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               // independent accumulators keep the add-min chains short
               const uint4* kv4 = (const uint4*)kb32;
               uint32_t a0 = 0xFFFFFFFFu, a1 = a0, a2 = a0, a3 = a0;
-              // (w << H32) + key as one IMAD by p2 = 2^H32, opaque to ptxas: it would otherwise turn it
-              // into shift + add and fuse the add with the min into the quarter-rate DPX VIADDMNMX
-              const uint32_t p2 = *(volatile const uint32_t*)&misc->p2;
               if (t16) {
                 // 16-bit rows, pre-clamped (absent = T32): two weights per word, shifted into the
                 // cost field; with H32 >= 16 the low weight is one shift, the high one shift + mask
@@ -408,27 +462,9 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 acc = umin64(acc, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)acc, off));
               best = acc >= kBig ? INF : acc;
             }
-            if (lane == (k & 31)) {  // the lane holding the row's prefetched keys
-              const int e = (s + 1) * R + j;
-              uint64_t kv = pkv, ko = pko;
-              int res = pres;
-              if (k >= 32) { kv = kin[e]; ko = kout[e]; res = g[e] < capE[e]; }
-              if (best < kv) { kin[e] = best; kv = best; ch = 1; }
-              if (kv != INF && res && kv + 1 < ko) { kout[e] = kv + 1; ch = 1; }
+            apply(k, j, best);
             }
-            }
-            // every lane is done with its row of slot b (its values fed the warp minimum); the
-            // last warp to finish the chunk refills the slot through the async proxy
-            php ^= 1ull << b;  // slot b's phase advanced (every thread tracks every chunk)
-            const int k2 = k + nbc - nch;  // chunk of the next boundary that reuses slot b
-            if (lane == 0 && !nostream && (k + nbc < nch || (k2 >= 0 && k2 < pf_n))) {
-              if (atomicAdd(&ecnt[b], 1u) % NW == NW - 1) {  // last reader of the chunk
-                __threadfence_block();
-                fence_proxy_async_smem();
-                if (k + nbc < nch) issue(k + nbc, b);
-                else issue_from(rows_next, k2, b);
-              }
-            }
+            release(k, b);
           }
           slot0 = (slot0 + nch) % nbc;
           TMARK(1);
