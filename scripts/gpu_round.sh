@@ -8,7 +8,7 @@ timeout 600 python bench.py --steps 2 --warmup 3 --quick > $O/bench_quick.json 2
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_gpt.csv \
   python bench.py --steps 2 --warmup 3 --quick > $O/ncu_launches.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"rounds_kernel|ssp_kernel" \
-  --launch-skip 2 --launch-count 2 -o $O/gpt_full python bench.py --steps 1 --warmup 3 --quick > $O/ncu_gpt_full.log 2>&1
+  --launch-skip 13 --launch-count 3 -o $O/gpt_full python bench.py --steps 1 --warmup 3 --quick > $O/ncu_gpt_full.log 2>&1
 timeout 300 python scripts/stress_probe.py --supply 64 --reps 1 > $O/stress_probe64.json 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ssp_cluster -c 1 -o $O/stress_full \
   python scripts/stress_probe.py --supply 64 --reps 1 > $O/ncu_stress_full.log 2>&1

@@ -3,6 +3,10 @@
 Bar: everything here is integer, so bit-exact -- flow value, cost, augmentation
 count, the canonical assignment (node flows, source/sink flows, dense arc flows), every
 per-round state digest of the decentralized rounds and the final exported round state."""
+import hashlib
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -348,3 +352,24 @@ def test_cluster_tier_stress_scaled():
         r = _oracle_ssp(cfg, bt, src, snk, link, b)
         assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
         assert np.array_equal(af[b], r.arc_flow) and np.array_equal(nf[b], r.node_flow), b
+
+
+def test_stress_full_golden():
+    """Full-size stress instances (64 x 1,024, M = 4,096) through the cluster tier against the
+    oracle's values stored by scripts/stress_golden.py (oracle.ssp: ~1-2 h of CPU each): F, cost,
+    augmentations and SHA-256 digests of the canonical assignment."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "stress_ssp.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/stress_ssp.json not generated yet")
+    gold = json.load(open(path))["instances"]
+    cfg = gen.CONFIGS["stress"]
+    sha = lambda x: hashlib.sha256(np.ascontiguousarray(x, dtype=np.int32).tobytes()).hexdigest()  # noqa: E731
+    for key, g in sorted(gold.items()):
+        i = int(key)
+        fl, *_ = _gpu_flow(cfg, i, 1)
+        sol = fl.solve_batch()
+        nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+        assert (int(sol.flow_value[0]), int(sol.total_cost[0]), int(sol.augmentations[0])) == (g["F"], g["cost"], g["A"]), i
+        assert sha(nf[0]) == g["node_flow_sha256"] and sha(af[0]) == g["arc_flow_sha256"], i
+        assert sha(sf[0]) == g["src_flow_sha256"] and sha(kf[0]) == g["snk_flow_sha256"], i
+        fl.close()
