@@ -373,3 +373,27 @@ def test_stress_full_golden():
         assert sha(nf[0]) == g["node_flow_sha256"] and sha(af[0]) == g["arc_flow_sha256"], i
         assert sha(sf[0]) == g["src_flow_sha256"] and sha(kf[0]) == g["snk_flow_sha256"], i
         fl.close()
+
+
+def test_stress_rounds_full_golden():
+    """Decentralized rounds on full-size stress instances (cluster-team tier), cold, to
+    max_rounds = 8,312 or quiescence, against the oracle trajectory stored by
+    scripts/stress_rounds_golden.py: rounds run, F_dec, cost_dec, dangling, every 256th per-round
+    digest and the SHA-256 of the whole digest sequence."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "stress_rounds.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/stress_rounds.json not generated yet")
+    gold = json.load(open(path))
+    cfg = gen.CONFIGS["stress"]
+    for key, g in sorted(gold["instances"].items()):
+        i = int(key)
+        fl, *_ = _gpu_flow(cfg, i, 1, seed=gold["seed"], inst_base=i)
+        rr = fl.decentralized_rounds(gold["max_rounds"], digests=True)
+        torch.cuda.synchronize()
+        n_r = int(rr.rounds_run[0])
+        assert n_r == g["rounds"], i
+        assert (int(rr.dec_flow[0]), int(rr.dec_cost[0]), int(rr.dangling[0])) == (g["F_dec"], g["cost_dec"], g["dangling"]), i
+        d = np.ascontiguousarray(rr.digests[0, :n_r].cpu().numpy().view(np.uint64))
+        assert [str(int(x)) for x in d[::256]] == g["digest_every_256"], i
+        assert hashlib.sha256(d.tobytes()).hexdigest() == g["digests_sha256"], i
+        fl.close()
