@@ -115,6 +115,10 @@ CONFIGS = {
     # carry >= 17 hop bits (its shift-and-mask weight path), with a small supply for the oracle
     "stress_h": Config("stress_h", 6, S=64, n=512, M=16, max_cap=20, cap=(1, 20), B=2, cost=(1, 100),
                        max_rounds=120 + 2 * 16),
+    # node-addition setting 1 (PAPER.md:446-471 and its Table, "Node addition (top)"): 97 nodes = 1 data
+    # holder + 8 stages x 12 clients, capacities U{1..20}, interlayer costs U{1..100}; S candidates join
+    "addition": Config("addition", 7, S=8, n=12, M=64, max_cap=20, cap=(1, 20), B=1, cost=(1, 100),
+                       max_rounds=120 + 2 * 64),
     # flow-test settings 1-4: 1 source, 40 relays, 8 or 10 stages
     "flow1": Config("flow1", 11, S=8, n=5, M=128, max_cap=3, cap=(1, 3), B=64, cost=(1, 20), max_rounds=120 + 256),
     "flow2": Config("flow2", 12, S=10, n=4, M=128, max_cap=3, cap=(1, 3), B=64, cost=(1, 20), max_rounds=120 + 256),
@@ -255,6 +259,7 @@ def linkdrop_to_updates(linkdrop, inst_offset: int = 0):
 # ----------------------------------------------------------------------------------------
 _M64 = (1 << 64) - 1
 GEN_F_VICTIM_STAGE, GEN_F_VICTIM_PICK = 15, 16
+GEN_F_CAND_CAP, GEN_F_CAND_IN, GEN_F_CAND_OUT, GEN_F_CAND_CC = 17, 18, 19, 20
 
 
 def mix64(z: int) -> int:
@@ -301,3 +306,36 @@ def llama_victims(up, down, alive, draws) -> np.ndarray:
                 out[b, s, cand[pick(int(draws[b, 1]), cand.size)]] = 0
                 break
     return out
+
+
+_C1, _C2 = np.uint64(0xBF58476D1CE4E5B9), np.uint64(0x94D049BB133111EB)
+
+
+def _mix_np(z):
+    z = np.asarray(z, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * _C1
+        z = (z ^ (z >> np.uint64(27))) * _C2
+    return z ^ (z >> np.uint64(31))
+
+
+def _uniform_np(iseed: int, field_id: int, idx, lo: int, hi: int):
+    """draw(iseed, field, idx) -> U{lo..hi} for an index array (the same counter hash as draw())."""
+    with np.errstate(over="ignore"):
+        base = np.uint64((iseed + field_id * 0x9E3779B97F4A7C15) & _M64)
+    d = _mix_np(_mix_np(base) ^ np.asarray(idx, dtype=np.uint64))
+    return (np.uint64(lo) + (((d >> np.uint64(32)) * np.uint64(hi - lo + 1)) >> np.uint64(32))).astype(np.int32)
+
+
+def generate_candidates(cfg: Config, inst: int, base_seed: int = BASE_SEED):
+    """S joining candidates of node-addition instance `inst` ("every node is a
+    candidate for each stage ... each node knows its costs for each stage"): capacity U{cap},
+    cost to / from every client of every stage and between candidates U{cost} (inputs of
+    gwtf_addition_build; include/gwtf.h documents the layout)."""
+    S, n = cfg.S, cfg.n
+    s = instance_seed(cfg, inst, base_seed)
+    cap = _uniform_np(s, GEN_F_CAND_CAP, np.arange(S), cfg.cap[0], cfg.cap[1])
+    cin = _uniform_np(s, GEN_F_CAND_IN, np.arange(S * S * n), cfg.cost[0], cfg.cost[1]).reshape(S, S, n)
+    cout = _uniform_np(s, GEN_F_CAND_OUT, np.arange(S * S * n), cfg.cost[0], cfg.cost[1]).reshape(S, S, n)
+    cc = _uniform_np(s, GEN_F_CAND_CC, np.arange(S * S), cfg.cost[0], cfg.cost[1]).reshape(S, S)
+    return {"cap": cap, "cin": cin, "cout": cout, "cc": cc}

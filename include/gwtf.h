@@ -89,6 +89,34 @@ gwtf_status gwtf_eq1_cost_tiles(int32_t B, int32_t S, int32_t n, int32_t L, cons
                                 const int32_t* bw, int64_t size_kbit, int32_t* src_out,
                                 int32_t* snk_out, int32_t* link_out, void* stream);
 
+/* Node addition ("the optimal choice of node addition is
+ * determined by running the minimum cost flow algorithm for each combination of S candidate
+ * nodes added to each of the S stages").  Builds placements
+ * p = first .. first+count-1 of S candidates, one per stage, into a base instance, as a batch of
+ * (n+1)-client instances in the gwtf_problem_desc layout: placement p is the p-th permutation of
+ * the candidates in lexicographic order (factorial number system; perm[s] = candidate placed in
+ * stage s, as client n).  Inputs (device pointers, read only):
+ *   cap [S][n], src_cost [n], snk_cost [n], link_cost [S-1][n][n] (dest-major) of the base;
+ *   cand_cap [S]; cand_in [S][S][n]: cand_in[c][s][u] = d((s-1,u) -> c in stage s) for s >= 1,
+ *   cand_in[c][0][0] = d(D -> c in stage 0); cand_out [S][S][n]: cand_out[c][s][v] =
+ *   d(c in stage s -> (s+1,v)) for s <= S-2, cand_out[c][S-1][0] = d(c -> D);
+ *   cand_cc [S][S]: d(c1 -> c2) when c1 is in stage s and c2 in stage s+1.
+ * Outputs (device, caller-owned): cap_out [count][S][n+1], src_out/snk_out [count][n+1],
+ * link_out [count][S-1][n+1][n+1].  Solve them with gwtf_flow_create + gwtf_flow_solve_batch.
+ * INVALID on S outside 1..20, n < 1, first/count outside [0, S!], NULL arrays. */
+gwtf_status gwtf_addition_build(int32_t S, int32_t n, const int32_t* cap, const int32_t* src_cost,
+                                const int32_t* snk_cost, const int32_t* link_cost, const int32_t* cand_cap,
+                                const int32_t* cand_in, const int32_t* cand_out, const int32_t* cand_cc,
+                                int64_t first, int64_t count, int32_t* cap_out, int32_t* src_out,
+                                int32_t* snk_out, int32_t* link_out, void* stream);
+
+/* The optimal placement among `count` solved placements (device arrays F, cost [count]): the
+ * largest max-flow value, then the lowest cost, then the lowest index (the lexicographically first
+ * assignment).  Writes its index to best_index (device int64).  INVALID on
+ * count < 1 or NULL arrays. */
+gwtf_status gwtf_addition_select(int64_t count, const int64_t* flow_value, const int64_t* total_cost,
+                                 int64_t* best_index, void* stream);
+
 /* Validate the description (errors: INVALID, OVERFLOW when (2Sn+2)*maxcost >= 2^42 or
  * (2Sn+2)*maxcost*M >= 2^62, UNSUPPORTED), allocate the handle's workspace, copy the
  * inputs into the handle's padded tiles, build the annealing threshold table on the

@@ -358,3 +358,62 @@ def digest_state(st: dict, S: int, n: int, MC: int, M: int) -> int:
         vals += [int(st["kacc"].reshape(-1)[g]) & 0xFFFFFFFF, int(st["deny"].reshape(-1)[g]) & 0xFFFFFFFF]
     vals.append(int(st["quiet"]) & 0xFFFFFFFF)
     return sum(mix64(mix64(pos) ^ v) for pos, v in enumerate(vals)) & m
+
+
+# ---- node addition ----
+
+def placed_instance(I: Instance, cand: dict, assign) -> Instance:
+    """The base instance with candidate assign[s] joined to stage s as client n (assign[s] < 0:
+    no candidate, a zero-capacity client).  Costs as generated (gen.generate_candidates):
+    cin[c][s][u] = d((s-1,u) -> c@s), cin[c][0][0] = d(D -> c@0); cout[c][s][v] = d(c@s -> (s+1,v)),
+    cout[c][S-1][0] = d(c@S-1 -> D); cc[c1][c2] = d(c1@s -> c2@s+1)."""
+    S, n = I.S, I.n
+    n1 = n + 1
+    cap = np.zeros((S, n1), np.int32)
+    cap[:, :n] = I.cap_eff()
+    src = np.full(n1, ABSENT, np.int32)
+    snk = np.full(n1, ABSENT, np.int32)
+    src[:n], snk[:n] = I.src, I.snk
+    link = np.full((max(S - 1, 0), n1, n1), ABSENT, np.int32)
+    if S > 1:
+        link[:, :n, :n] = I.link
+    for s in range(S):
+        c = assign[s]
+        if c < 0:
+            continue
+        cap[s, n] = cand["cap"][c]
+        if s == 0:
+            src[n] = cand["cin"][c][0][0]
+        else:
+            link[s - 1, n, :n] = cand["cin"][c][s]          # (s-1,u) -> c@s
+        if s == S - 1:
+            snk[n] = cand["cout"][c][S - 1][0]
+        else:
+            link[s, :n, n] = cand["cout"][c][s]             # c@s -> (s+1,v)
+            if assign[s + 1] >= 0:
+                link[s, n, n] = cand["cc"][c][assign[s + 1]]
+    return Instance(S, n1, max(I.max_cap, int(cand["cap"].max(initial=0))), I.M, cap, src, snk, link)
+
+
+def optimal_addition(I: Instance, cand: dict):
+    """The optimal placement of S candidates, one per stage, by exhaustive enumeration
+    (PAPER.md:449 "for each combination of S candidate nodes added to each of the S stages"):
+    every permutation in lexicographic order (itertools.permutations of range(S)), each solved
+    by the oracle SSP.  Best = max F, then min cost, then the first (lexicographic) placement
+    (SPEC.md:193).  Returns (best index, its permutation, F[], cost[])."""
+    perms = list(itertools.permutations(range(I.S)))
+    F = np.zeros(len(perms), np.int64)
+    C = np.zeros(len(perms), np.int64)
+    for k, p in enumerate(perms):
+        r = ssp(placed_instance(I, cand, p))
+        F[k], C[k] = r.F, r.cost
+    best = 0
+    for k in range(1, len(perms)):
+        if F[k] > F[best] or (F[k] == F[best] and C[k] < C[best]):
+            best = k
+    return best, perms[best], F, C
+
+
+def improvement(cost_now: float, cost_after: float) -> float:
+    """(cost_now - cost_after) / cost_now (PAPER.md:450; SPEC.md:695-701)."""
+    return (cost_now - cost_after) / cost_now

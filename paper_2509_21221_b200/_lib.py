@@ -39,6 +39,8 @@ class GwtfError(RuntimeError):
 
 EXPORTS = {
     "gwtf_eq1_cost_tiles": ([I32, I32, I32, I32, P, P, P, P, P, I64, P, P, P, P], I32),
+    "gwtf_addition_build": ([I32, I32, P, P, P, P, P, P, P, P, I64, I64, P, P, P, P, P], I32),
+    "gwtf_addition_select": ([I64, P, P, P, P], I32),
     "gwtf_flow_create": ([ctypes.POINTER(ProblemDesc), ctypes.POINTER(P)], I32),
     "gwtf_flow_solve_batch": ([P, P, P, P, P], I32),
     "gwtf_flow_decentralized_rounds": ([P, I32, P, P, P, P, P], I32),

@@ -210,6 +210,32 @@ gwtf_status gwtf_eq1_cost_tiles(int32_t B, int32_t S, int32_t n, int32_t L, cons
   return GWTF_OK;
 }
 
+gwtf_status gwtf_addition_build(int32_t S, int32_t n, const int32_t* cap, const int32_t* src_cost,
+                                const int32_t* snk_cost, const int32_t* link_cost, const int32_t* cand_cap,
+                                const int32_t* cand_in, const int32_t* cand_out, const int32_t* cand_cc,
+                                int64_t first, int64_t count, int32_t* cap_out, int32_t* src_out, int32_t* snk_out,
+                                int32_t* link_out, void* stream) {
+  if (S < 1 || S > 20 || n < 1) return fail(GWTF_E_INVALID, "addition: S must be in 1..20 and n >= 1");
+  int64_t fact = 1;
+  for (int i = 2; i <= S; ++i) fact *= i;
+  if (first < 0 || count < 0 || first + count > fact) return fail(GWTF_E_INVALID, "addition: placements outside [0, S!)");
+  if (!cap || !src_cost || !snk_cost || (S > 1 && !link_cost) || !cand_cap || !cand_in || !cand_out || !cand_cc ||
+      !cap_out || !src_out || !snk_out || (S > 1 && !link_out))
+    return fail(GWTF_E_INVALID, "addition: NULL array");
+  cudaError_t e = launch_addition_build(S, n, cap, src_cost, snk_cost, link_cost, cand_cap, cand_in, cand_out, cand_cc,
+                                        first, count, cap_out, src_out, snk_out, link_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(GWTF_E_CUDA, std::string("addition build: ") + cudaGetErrorString(e));
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_addition_select(int64_t count, const int64_t* flow_value, const int64_t* total_cost,
+                                 int64_t* best_index, void* stream) {
+  if (count < 1 || !flow_value || !total_cost || !best_index) return fail(GWTF_E_INVALID, "addition select: count/NULL");
+  cudaError_t e = launch_addition_select(count, flow_value, total_cost, best_index, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(GWTF_E_CUDA, std::string("addition select: ") + cudaGetErrorString(e));
+  return GWTF_OK;
+}
+
 gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   if (!d || !out) return fail(GWTF_E_INVALID, "NULL desc/out");
   *out = nullptr;

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 namespace gwtf {
 
 constexpr int32_t kAbsent = INT32_MAX;
@@ -98,6 +100,11 @@ cudaError_t launch_dense_arcs(const Problem& P, int32_t* dense, cudaStream_t st)
 cudaError_t launch_eq1(int32_t B, int32_t S, int32_t n, int32_t L, const int32_t* comp, const int32_t* loc,
                        const int32_t* dloc, const int32_t* lat, const int32_t* bw, int64_t size_kbit,
                        int32_t* src, int32_t* snk, int32_t* link, cudaStream_t st);
+cudaError_t launch_addition_build(int32_t S, int32_t n, const int32_t* cap, const int32_t* src, const int32_t* snk,
+                                  const int32_t* link, const int32_t* ccap, const int32_t* cin, const int32_t* cout,
+                                  const int32_t* ccc, int64_t first, int64_t count, int32_t* cap_o, int32_t* src_o,
+                                  int32_t* snk_o, int32_t* link_o, cudaStream_t st);
+cudaError_t launch_addition_select(int64_t count, const int64_t* F, const int64_t* cost, int64_t* best, cudaStream_t st);
 cudaError_t launch_scan_costs(const int32_t* v, int64_t count, int32_t* out_max, int32_t* out_min,
                               cudaStream_t st);
 
