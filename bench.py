@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline and stress tier (profiling runs)")
     ap.add_argument("--no-stress-tier", action="store_true", help="skip the stress-config exact-solve measurement")
+    ap.add_argument("--no-addition", action="store_true", help="skip the node-addition optimizer measurement")
     return ap.parse_args()
 
 
@@ -120,6 +121,48 @@ def stress_tier(dev):
                         "algorithmic_bytes_per_launch": alg, "traffic": traffic, "traffic_source": tsrc}}
     fl.close()
     return out
+
+
+def node_addition(dev, steps=5):
+    """SURVEY.md 8(f) f1 on node-addition setting 1 (PAPER.md Table "Node addition", 8 stages x 12
+    clients + 8 candidates): all 8! = 40,320 placements built, solved and reduced on the device per
+    step; improvement (cost_now - cost_after)/cost_now of the optimal placement and the two
+    baselines (capacity-first, random) over the base instance."""
+    import torch
+
+    from paper_2509_21221_b200 import Flow, addition
+    cfg = gen.CONFIGS["addition"]
+    bt = gen.generate(cfg, 0, 1)
+    cand = gen.generate_candidates(cfg, 0)
+    cap = (bt.cap[0] * (bt.alive[0] != 0)).astype(np.int32)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    args = (d(cap), d(bt.src[0]), d(bt.snk[0]), d(bt.link[0]), d(cand["cap"]), d(cand["cin"]), d(cand["cout"]),
+            d(cand["cc"]), int(cfg.M))
+    r = addition.optimal_addition(*args, max_cap=cfg.max_cap)  # warm-up
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(steps):
+        r = addition.optimal_addition(*args, max_cap=cfg.max_cap)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    base = Flow(d(cap[None]), d(bt.src[:1]), d(bt.snk[:1]), d(bt.link[:1]),
+                torch.full((1,), cfg.M, dtype=torch.int64, device=dev), max_cap=cfg.max_cap)
+    bs = base.solve_batch()
+    F0, C0 = int(bs.flow_value[0]), int(bs.total_cost[0])
+    base.close()
+    cost = r["all_cost"].cpu().numpy()
+    cf = addition.placement_index(addition.capacity_first(cand["cap"], cap.sum(axis=1), F0))
+    rnd = addition.placement_index(addition.random_placement(cfg.S, 0))
+    return {"workload": f"node addition setting 1: {cfg.S} stages x {cfg.n} clients + {cfg.S} candidates, "
+                        f"M={cfg.M}, caps U{{1..20}}, costs U{{1..100}}",
+            "placements": addition.num_placements(cfg.S), "ms_per_optimization": ms,
+            "placements_per_s": addition.num_placements(cfg.S) / (ms / 1e3),
+            "base": {"F": F0, "cost": C0}, "optimal": {"perm": r["perm"], "F": r["F"], "cost": r["cost"],
+                                                       "improvement": addition.improvement(C0, r["cost"])},
+            "capacity_first": {"cost": int(cost[cf]), "improvement": addition.improvement(C0, int(cost[cf]))},
+            "random": {"cost": int(cost[rnd]), "improvement": addition.improvement(C0, int(cost[rnd]))}}
 
 
 def load_peaks():
@@ -343,6 +386,8 @@ def main():
         line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0 and world == 1 and not (args.quick or args.no_stress_tier):
         line["stress_tier"] = stress_tier(dev)
+    if rank == 0 and world == 1 and not (args.quick or args.no_addition):
+        line["node_addition"] = node_addition(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
