@@ -175,6 +175,14 @@ gwtf_status gwtf_flow_set_profiling(gwtf_flow_t h, int32_t on);
 gwtf_status gwtf_flow_kernel_times(gwtf_flow_t h, const char** names, float* ms, int32_t* launches,
                                    int32_t cap, int32_t* count);
 
+/* SWARM-style greedy routing baseline (SPEC.md:199-207 greedy_route) on the
+ * current (masked) graph of every instance: microbatches routed one at a time from the data node,
+ * each hop to the alive next-stage client with spare capacity and a link, cheapest first, lowest
+ * index on ties; the first microbatch that finds no successor (or no sink arc) stops the routing
+ * (DESIGN.md 8c).  Outputs [B] (caller-owned, device or host per GWTF_HOST_PTRS): routed
+ * microbatches and their total cost.  Does not touch the solver or round state. */
+gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_t* total_cost);
+
 /* Work counters of the exact solve accumulated since create (host int64 out[cap], cap <= 8):
  * [0] dense boundary relaxations, [1] backward (reverse-arc) phases, [2] augmentations,
  * [3] Bellman-Ford passes, [4] traced path nodes (cluster tier).  Synchronizes the stream. */

@@ -417,3 +417,39 @@ def optimal_addition(I: Instance, cand: dict):
 def improvement(cost_now: float, cost_after: float) -> float:
     """(cost_now - cost_after) / cost_now (PAPER.md:450; SPEC.md:695-701)."""
     return (cost_now - cost_after) / cost_now
+
+
+# ---- SWARM-style greedy baseline (SURVEY.md 8(f) f4; PAPER.md:111-113; SPEC.md:199-207) ----
+
+def greedy_route(I: Instance):
+    """Microbatches routed one at a time from the data node D: each hop goes to the alive
+    next-stage client with spare capacity and a link, minimum cost first, lowest index on ties
+    (SPEC.md:202); a microbatch without a successor or sink arc is not routed, its reservations
+    are released and routing stops (every later microbatch would retrace it).  Returns
+    (routed microbatches, total cost, per-microbatch paths)."""
+    rem = I.cap_eff().astype(np.int64).copy()
+    F, cost, paths = 0, 0, []
+    for _ in range(I.M):
+        path, c, u = [], 0, None
+        for s in range(I.S):
+            best = None
+            for v in range(I.n):
+                d = int(I.src[v]) if s == 0 else int(I.link[s - 1, v, u])
+                if d == ABSENT or rem[s, v] <= 0:
+                    continue
+                if best is None or d < best[0]:
+                    best = (d, v)
+            if best is None:
+                break
+            rem[s, best[1]] -= 1
+            path.append(best[1])
+            c += best[0]
+            u = best[1]
+        if len(path) < I.S or int(I.snk[u]) == ABSENT:
+            for s, v in enumerate(path):
+                rem[s, v] += 1
+            break
+        F += 1
+        cost += c + int(I.snk[u])
+        paths.append(path)
+    return F, cost, paths

@@ -620,6 +620,24 @@ gwtf_status gwtf_flow_kernel_times(gwtf_flow_t h, const char** names, float* ms,
   return GWTF_OK;
 }
 
+gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_t* total_cost) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!flow_value || !total_cost) return fail(GWTF_E_INVALID, "greedy: NULL output");
+  const size_t B = h->P.B;
+  std::vector<OutMap> maps;
+  int64_t *F = nullptr, *C = nullptr;
+  if ((s = map_out(h, flow_value, B, 14, &F, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, total_cost, B, 15, &C, maps)) != GWTF_OK) return s;
+  int32_t* rem = (int32_t*)scratch(h, 16, B * (size_t)h->P.S * h->P.n * 4);
+  if (!rem) return fail(GWTF_E_NOMEM, "greedy scratch");
+  Timer t;
+  prof_begin(h, "greedy_kernel", &t);
+  CK(h, launch_greedy(h->P, rem, F, C, h->stream));
+  prof_end(h, &t);
+  return finish_out(h, maps);
+}
+
 gwtf_status gwtf_flow_stats(gwtf_flow_t h, int64_t* out, int32_t cap) {
   gwtf_status s = enter(h);
   if (s != GWTF_OK) return s;

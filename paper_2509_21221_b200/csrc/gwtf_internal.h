@@ -105,6 +105,7 @@ cudaError_t launch_addition_build(int32_t S, int32_t n, const int32_t* cap, cons
                                   const int32_t* ccc, int64_t first, int64_t count, int32_t* cap_o, int32_t* src_o,
                                   int32_t* snk_o, int32_t* link_o, cudaStream_t st);
 cudaError_t launch_addition_select(int64_t count, const int64_t* F, const int64_t* cost, int64_t* best, cudaStream_t st);
+cudaError_t launch_greedy(const Problem& P, int32_t* rem, int64_t* F, int64_t* cost, cudaStream_t st);
 cudaError_t launch_scan_costs(const int32_t* v, int64_t count, int32_t* out_max, int32_t* out_min,
                               cudaStream_t st);
 

@@ -195,6 +195,14 @@ class Flow:
             ctypes.cast(ctypes.byref(cnt), ctypes.c_void_p)))
         return {names[i].decode(): (ms[i], nl[i]) for i in range(min(cnt.value, cap))}
 
+    def greedy_baseline(self):
+        """SWARM-style greedy routing on the current graph (gwtf_flow_greedy_baseline): (routed
+        microbatches [B], their total cost [B])."""
+        F = self._out((self.B,), torch.int64)
+        C = self._out((self.B,), torch.int64)
+        check("gwtf_flow_greedy_baseline", lib().gwtf_flow_greedy_baseline(self.h, _ptr(F), _ptr(C)))
+        return F, C
+
     def stats(self, raw: bool = False):
         """Exact-solve work counters since create (gwtf_flow_stats)."""
         import numpy as np
