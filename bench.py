@@ -165,6 +165,37 @@ def node_addition(dev, steps=5):
             "random": {"cost": int(cost[rnd]), "improvement": addition.improvement(C0, int(cost[rnd]))}}
 
 
+def flow_quality(dev, B=256):
+    """PAPER.md:612-620 ablation, flow-test settings 1-4: the decentralized rounds
+    (120 iterations), the SWARM greedy baseline and the optimum (exact solve) on B seeded
+    instances each; mean costs, mean flows and GWTF's improvement over SWARM
+    (cost_swarm - cost_gwtf) / cost_swarm over the instances where both route the same flow."""
+    import torch
+
+    from paper_2509_21221_b200 import Flow
+    from tests import harness
+    out = {}
+    for name in ("flow1", "flow2", "flow3", "flow4"):
+        cfg = gen.CONFIGS[name]
+        bt, src, snk, link = harness.device_inputs(cfg, 0, B, device=dev)
+        fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0)
+        sol = fl.solve_batch()
+        rr = fl.decentralized_rounds(120)
+        gF, gC = fl.greedy_baseline()
+        torch.cuda.synchronize()
+        F, C = sol.flow_value.double(), sol.total_cost.double()
+        dF, dC = rr.dec_flow.double(), rr.dec_cost.double()
+        same = (dF == gF.double()) & (gF > 0)
+        imp = ((gC.double() - dC) / gC.double())[same]
+        out[name] = {"instances": B, "F_opt": float(F.mean()), "F_gwtf": float(dF.mean()), "F_swarm": float(gF.double().mean()),
+                     "cost_opt": float(C.mean()), "cost_gwtf": float(dC.mean()), "cost_swarm": float(gC.double().mean()),
+                     "gwtf_vs_swarm_improvement_mean": float(imp.mean()) if imp.numel() else None,
+                     "gwtf_vs_swarm_improvement_max": float(imp.max()) if imp.numel() else None,
+                     "same_flow_instances": int(same.sum())}
+        fl.close()
+    return out
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -388,6 +419,7 @@ def main():
         line["stress_tier"] = stress_tier(dev)
     if rank == 0 and world == 1 and not (args.quick or args.no_addition):
         line["node_addition"] = node_addition(dev)
+        line["flow_quality"] = flow_quality(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
