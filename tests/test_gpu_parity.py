@@ -286,11 +286,15 @@ def test_full_size_bench_config_sampled():
 
 
 @pytest.mark.parametrize("name,B,C", [("gpt", 24, None), ("gpt", 24, 16), ("gpt", 24, 8), ("llama", 6, None),
-                                      ("churn", 4, None), ("churn", 4, 16), ("flow3", 16, None)])
+                                      ("churn", 4, None), ("churn", 4, 16), ("flow3", 16, None), ("churn", 4, "int32"),
+                                      ("stress_s", 2, "int32")])
 def test_cluster_tier_parity_forced(name, B, C, monkeypatch):
     """Instances forced through the thread-block-cluster tier (HBM-streamed tiles, DSMEM keys), with
-    the automatic cluster size and with pinned ones (R = n / C destination rows per CTA)."""
-    if C is not None:
+    the automatic cluster size, pinned ones (R = n / C destination rows per CTA) and the int32 tile
+    stream instead of the 16-bit copy ("int32")."""
+    if C == "int32":
+        monkeypatch.setenv("GWTF_NO_TILE16", "1")
+    elif C is not None:
         monkeypatch.setenv("GWTF_CLUSTER_SIZE", str(C))
     cfg = gen.CONFIGS[name]
     fl, *_ = _gpu_flow(cfg, 0, B, force_cluster_tier=True)
