@@ -196,6 +196,56 @@ def flow_quality(dev, B=256):
     return out
 
 
+def other_configs(dev, steps=5, warmup=3):
+    """The other churn-protocol configs of SURVEY.md 8(d) on this GPU, same step and timing as the
+    main line (device events, L2 flushed, restore untimed): tiny (cold, no churn), llama (victim
+    crash), churn (random crash/rejoin + link drops)."""
+    import torch
+
+    from paper_2509_21221_b200 import Flow
+    from tests import harness
+    out = {}
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for name in ("tiny", "llama", "churn"):
+        cfg = gen.CONFIGS[name]
+        B, mr = cfg.B, cfg.max_rounds
+        bt, src, snk, link = harness.device_inputs(cfg, 0, B, device=dev)
+        fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0)
+        an = upd = None
+        if cfg.churn != "none":
+            fl.decentralized_rounds(mr)
+            if cfg.churn == "random":
+                an, upd = harness.churn_inputs(cfg, 0, bt.alive, device=dev)
+            else:
+                st = fl.export_round_state()
+                an = torch.from_numpy(gen.llama_victims(st["up"].cpu().numpy(), st["down"].cpu().numpy(),
+                                                        bt.alive.cpu().numpy(), gen.victim_draws(cfg, 0, B))).to(dev)
+        fl.snapshot()
+        sol = fl.solve_batch()
+        rr = fl.decentralized_rounds(mr)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        total = 0.0
+        for it in range(warmup + steps):
+            fl.restore()
+            flush.random_(0, 255)
+            torch.cuda.synchronize()
+            ev0.record(fl.stream)
+            if an is not None or upd is not None:
+                fl.apply_churn(an, upd)
+            fl.solve_batch(out=sol)
+            fl.decentralized_rounds(mr, out=rr)
+            ev1.record(fl.stream)
+            torch.cuda.synchronize()
+            if it >= warmup:
+                total += ev0.elapsed_time(ev1)
+        out[name] = {"workload": workload_name(cfg), "instances": B, "ms_per_step": total / steps,
+                     "instances_per_s": B * steps / (total / 1e3),
+                     "augmentations_mean": float(sol.augmentations.double().mean()),
+                     "rounds_mean": float(rr.rounds_run.double().mean())}
+        fl.close()
+    return out
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -420,6 +470,7 @@ def main():
     if rank == 0 and world == 1 and not (args.quick or args.no_addition):
         line["node_addition"] = node_addition(dev)
         line["flow_quality"] = flow_quality(dev)
+        line["other_configs"] = other_configs(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

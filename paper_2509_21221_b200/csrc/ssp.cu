@@ -17,6 +17,10 @@
 // since its last relaxation, the backward (reverse-arc) phases likewise.  Reverse residual arcs
 // are relaxed from the per-boundary list of positive-flow arcs.  The augmenting path is traced
 // by warp 0 with ballots (lowest (layer, position) tight predecessor) and augmented in place.
+#include <cstdlib>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gwtf {
@@ -624,10 +628,18 @@ cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int n
     if (force_tier != 1 && P.cluster_size > 0) return launch_ssp_cluster(P, o, st, P.cluster_size);
     return launch_tpi<256>(P, o, st, num_sms, false);
   }
-  if (P.n <= 32) return launch_tpi<32>(P, o, st, num_sms, true);
-  if (P.n <= 64) return launch_tpi<64>(P, o, st, num_sms, true);
-  if (P.n <= 128) return launch_tpi<128>(P, o, st, num_sms, true);
-  return launch_tpi<256>(P, o, st, num_sms, true);
+  // team size: about one thread per destination row to start with, then doubled while the teams
+  // that fit in an SM's shared memory would leave it with fewer than 512 threads (large tiles:
+  // churn 8 x 64 runs one 130 KB team per SM, llama 16 x 32 three 70 KB teams)
+  int tpi = P.n <= 32 ? 32 : P.n <= 64 ? 64 : P.n <= 128 ? 128 : 256;
+  const long long teams_per_sm = std::max<long long>(1, (long long)(227 * 1024) / (long long)ssp_layout(P, true, 4).total);
+  while (tpi < 512 && teams_per_sm * tpi < 512) tpi *= 2;
+  if (const char* f = getenv("GWTF_SSP_TPI")) tpi = atoi(f);  // testing override
+  if (tpi <= 32) return launch_tpi<32>(P, o, st, num_sms, true);
+  if (tpi <= 64) return launch_tpi<64>(P, o, st, num_sms, true);
+  if (tpi <= 128) return launch_tpi<128>(P, o, st, num_sms, true);
+  if (tpi <= 256) return launch_tpi<256>(P, o, st, num_sms, true);
+  return launch_tpi<512>(P, o, st, num_sms, true);
 }
 
 }  // namespace gwtf
