@@ -140,6 +140,15 @@ gwtf_status gwtf_flow_decentralized_rounds(gwtf_flow_t h, int32_t max_rounds, in
                                            int64_t* dec_flow, int64_t* dec_cost, int32_t* dangling,
                                            uint64_t* round_digests);
 
+/* gwtf_flow_solve_batch and gwtf_flow_decentralized_rounds of the same step issued together: the two
+ * solvers read the same (masked) graph and write disjoint state, so the rounds run on a second
+ * stream of the handle concurrently with the exact solve and are joined back into the handle's
+ * stream before the call returns (device mode: before later work on the stream runs).  Outputs
+ * as in the two calls (no digests).  Same errors. */
+gwtf_status gwtf_flow_solve_and_rounds(gwtf_flow_t h, int32_t max_rounds, int64_t* flow_value, int64_t* total_cost,
+                                       int32_t* augmentations, int32_t* inst_status, int32_t* rounds_run,
+                                       int64_t* dec_flow, int64_t* dec_cost, int32_t* dangling);
+
 /* Churn between solves/rounds: alive_new [B][S][n] (NULL = unchanged)
  * replaces the alive mask (crash / rejoin); edge_updates [k][5] = {b, s, v_dst, u_src, cost}
  * sets link_cost[b][s][v_dst][u_src] = cost for 0 <= s < S-1, src_cost[b][v_dst] for

@@ -44,6 +44,7 @@ EXPORTS = {
     "gwtf_flow_create": ([ctypes.POINTER(ProblemDesc), ctypes.POINTER(P)], I32),
     "gwtf_flow_solve_batch": ([P, P, P, P, P], I32),
     "gwtf_flow_decentralized_rounds": ([P, I32, P, P, P, P, P], I32),
+    "gwtf_flow_solve_and_rounds": ([P, I32, P, P, P, P, P, P, P, P], I32),
     "gwtf_flow_apply_churn": ([P, P, P, I64], I32),
     "gwtf_flow_get_assignment": ([P, P, P, P, P], I32),
     "gwtf_flow_export_round_state": ([P, P, P, P, P, P, P, P, P], I32),

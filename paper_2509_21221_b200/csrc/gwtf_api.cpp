@@ -62,6 +62,9 @@ struct gwtf_flow_s {
   std::vector<float> ms;
   std::vector<int32_t> launches;
   int32_t* bad_flag = nullptr;
+  // second stream of gwtf_flow_solve_and_rounds (created on first use)
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -107,16 +110,16 @@ void* scratch(gwtf_flow_s* h, size_t i, size_t bytes) {
   return b.p;
 }
 
-void prof_begin(gwtf_flow_s* h, const char* name, Timer* t) {
+void prof_begin(gwtf_flow_s* h, const char* name, Timer* t, cudaStream_t st = nullptr) {
   if (!h->profiling) return;
   t->name = name;
   cudaEventCreate(&t->a);
   cudaEventCreate(&t->b);
-  cudaEventRecord(t->a, h->stream);
+  cudaEventRecord(t->a, st ? st : h->stream);
 }
-void prof_end(gwtf_flow_s* h, Timer* t) {
+void prof_end(gwtf_flow_s* h, Timer* t, cudaStream_t st = nullptr) {
   if (!h->profiling) return;
-  cudaEventRecord(t->b, h->stream);
+  cudaEventRecord(t->b, st ? st : h->stream);
   h->pending.push_back(*t);
 }
 
@@ -470,6 +473,50 @@ gwtf_status gwtf_flow_decentralized_rounds(gwtf_flow_t h, int32_t max_rounds, in
   return finish_out(h, maps);
 }
 
+gwtf_status gwtf_flow_solve_and_rounds(gwtf_flow_t h, int32_t max_rounds, int64_t* flow_value, int64_t* total_cost,
+                                       int32_t* augmentations, int32_t* inst_status, int32_t* rounds_run,
+                                       int64_t* dec_flow, int64_t* dec_cost, int32_t* dangling) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!flow_value || !total_cost) return fail(GWTF_E_INVALID, "flow_value/total_cost must not be NULL");
+  if (max_rounds < 0) return fail(GWTF_E_INVALID, "max_rounds < 0");
+  if (!h->stream2) {
+    CK(h, cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+    CK(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CK(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  }
+  const size_t B = h->P.B;
+  std::vector<OutMap> maps;
+  SspOut so{};
+  if ((s = map_out(h, flow_value, B, 0, &so.F, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, total_cost, B, 1, &so.cost, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, augmentations, B, 2, &so.A, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, inst_status, B, 3, &so.status, maps)) != GWTF_OK) return s;
+  RoundsOut ro{};
+  ro.max_rounds = max_rounds;
+  if ((s = map_out(h, rounds_run, B, 4, &ro.rounds_run, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, dec_flow, B, 5, &ro.F_dec, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, dec_cost, B, 6, &ro.cost_dec, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, dangling, B, 7, &ro.dangling, maps)) != GWTF_OK) return s;
+  // fork: the rounds (second stream) and the exact solve (handle stream) read the same masked graph
+  // and write disjoint state and counters; join before anything else runs on the handle's stream
+  CK(h, cudaEventRecord(h->ev_fork, h->stream));
+  CK(h, cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+  Timer tr, ts;
+  prof_begin(h, "rounds_kernel", &tr, h->stream2);
+  CK(h, launch_rounds(h->P, ro, h->stream2, h->num_sms));
+  prof_end(h, &tr, h->stream2);
+  const int tier = (h->flags & GWTF_FORCE_GLOBAL_TIER) ? 1 : (h->flags & GWTF_FORCE_CLUSTER_TIER) ? 2 : 0;
+  const bool cluster = tier != 1 && h->P.cluster_size > 0 && (tier == 2 || ssp_smem_bytes(h->P) > 227 * 1024);
+  prof_begin(h, cluster ? "ssp_cluster_kernel" : "ssp_kernel", &ts);
+  CK(h, launch_ssp(h->P, so, h->stream, h->num_sms, tier));
+  prof_end(h, &ts);
+  CK(h, cudaEventRecord(h->ev_join, h->stream2));
+  CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  h->has_assignment = true;
+  return finish_out(h, maps);
+}
+
 gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const int32_t* edge_updates, int64_t k) {
   gwtf_status s = enter(h);
   if (s != GWTF_OK) return s;
@@ -653,6 +700,12 @@ gwtf_status gwtf_flow_destroy(gwtf_flow_t h) {
   if (!h) return GWTF_OK;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
+  if (h->stream2) {
+    cudaStreamSynchronize(h->stream2);
+    cudaStreamDestroy(h->stream2);
+    cudaEventDestroy(h->ev_fork);
+    cudaEventDestroy(h->ev_join);
+  }
   for (Timer& t : h->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
   for (void* p : h->allocs) cudaFree(p);
   for (void* p : h->snap) cudaFree(p);

@@ -621,7 +621,11 @@ size_t ssp_smem_bytes(const Problem& P) { return ssp_layout(P, true, 8).total; }
 size_t ssp_global_ws_bytes(const Problem& P) { return ssp_layout(P, false, 8).total; }
 
 cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, int force_tier) {
-  cudaError_t e = cudaMemsetAsync(P.counters, 0, 4 * sizeof(int32_t), st);
+  // counters [0] ssp queue, [2] redo count, [3] redo queue ([1] is the rounds queue, which may be
+  // running concurrently on another stream: gwtf_flow_solve_and_rounds)
+  cudaError_t e = cudaMemsetAsync(P.counters, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(P.counters + 2, 0, 2 * sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
   const bool smem_tier = force_tier == 0 && ssp_smem_bytes(P) <= 227 * 1024;
   if (!smem_tier) {

@@ -150,6 +150,23 @@ class Flow:
             _ptr(out.digests)))
         return out
 
+    def solve_and_rounds(self, max_rounds: int, out_sol: SolveResult | None = None,
+                         out_rounds: RoundsResult | None = None):
+        """solve_batch and decentralized_rounds of one step issued together: the rounds run on a
+        second stream concurrently with the exact solve (gwtf_flow_solve_and_rounds)."""
+        B = self.B
+        if out_sol is None:
+            out_sol = SolveResult(self._out((B,), torch.int64), self._out((B,), torch.int64),
+                                  self._out((B,), torch.int32), self._out((B,), torch.int32))
+        if out_rounds is None:
+            out_rounds = RoundsResult(self._out((B,), torch.int32), self._out((B,), torch.int64),
+                                      self._out((B,), torch.int64), self._out((B,), torch.int32), None)
+        check("gwtf_flow_solve_and_rounds", lib().gwtf_flow_solve_and_rounds(
+            self.h, max_rounds, _ptr(out_sol.flow_value), _ptr(out_sol.total_cost), _ptr(out_sol.augmentations),
+            _ptr(out_sol.status), _ptr(out_rounds.rounds_run), _ptr(out_rounds.dec_flow), _ptr(out_rounds.dec_cost),
+            _ptr(out_rounds.dangling)))
+        return out_sol, out_rounds
+
     def apply_churn(self, alive_new=None, edge_updates=None):
         k = 0 if edge_updates is None else int(edge_updates.shape[0])
         check("gwtf_flow_apply_churn", lib().gwtf_flow_apply_churn(

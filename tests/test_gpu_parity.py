@@ -401,3 +401,29 @@ def test_stress_rounds_full_golden():
         assert [str(int(x)) for x in d[::256]] == g["digest_every_256"], i
         assert hashlib.sha256(d.tobytes()).hexdigest() == g["digests_sha256"], i
         fl.close()
+
+
+@pytest.mark.parametrize("name,B", [("gpt", 256), ("churn", 16)])
+def test_solve_and_rounds_matches_serial(name, B):
+    """gwtf_flow_solve_and_rounds (solve and rounds on two streams) returns exactly what the two
+    serial calls return, after churn, and leaves the same assignment."""
+    cfg = gen.CONFIGS[name]
+    outs = []
+    for concurrent in (False, True):
+        fl, dbt, *_ = _gpu_flow(cfg, 0, B, seed=3)
+        fl.decentralized_rounds(cfg.max_rounds)
+        an, upd = harness.churn_inputs(cfg, 0, dbt.alive, device="cuda")
+        fl.apply_churn(an, upd)
+        if concurrent:
+            sol, rr = fl.solve_and_rounds(cfg.max_rounds)
+        else:
+            sol = fl.solve_batch()
+            rr = fl.decentralized_rounds(cfg.max_rounds)
+        nf, sf, kf, af = fl.get_assignment()
+        st = fl.export_round_state()
+        torch.cuda.synchronize()
+        outs.append([x.cpu() for x in (sol.flow_value, sol.total_cost, sol.augmentations, rr.rounds_run, rr.dec_flow,
+                                       rr.dec_cost, rr.dangling, nf, af, st["up"], st["down"])])
+        fl.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
