@@ -268,13 +268,15 @@ def test_validation_errors():
         fl.apply_churn(None, t([[5, 0, 0, 0, 1]]).int())
 
 
-def test_full_size_bench_config_sampled():
-    """GPT at the bench's full batch size and launch configuration; sampled instances vs the oracle."""
-    cfg = gen.CONFIGS["gpt"]
+@pytest.mark.parametrize("name,samples", [("gpt", 48), ("llama", 8), ("churn", 6)])
+def test_full_size_bench_config_sampled(name, samples):
+    """GPT (the bench line), LLaMA and churn (the bench's other_configs) at their full batch sizes and
+    launch configurations; sampled instances of the whole churn pipeline vs the oracle."""
+    cfg = gen.CONFIGS[name]
     B = cfg.B
     _, pre, sol, rr = harness.gpu_pipeline(cfg, 0, B, seed=0, digests=False)
     rng = np.random.default_rng(1)
-    idx = np.sort(rng.choice(B, 48, replace=False))
+    idx = np.sort(rng.choice(B, samples, replace=False))
     for b in idx:
         o = harness.oracle_pipeline(cfg, int(b), 1, seed=0)
         # instance b of the big batch == instance 0 of a batch starting at global id b
