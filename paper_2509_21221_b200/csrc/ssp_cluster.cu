@@ -836,6 +836,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   }
 }
 
+#undef TMARK
+
 template <int C>
 cudaError_t launch_c(const Problem& P, const SspOut& o, cudaStream_t st, int* nclusters_out, bool query) {
   const size_t smem = cl_layout(P, C).total;

@@ -27,5 +27,5 @@ for rep in range(2):
     torch.cuda.synchronize()
     kt = fl.kernel_times()
     fl.set_profiling(False)
-print(name, B, {k: round(v[0], 2) for k, v in kt.items()}, "rounds mean", float(rr.rounds_run.double().mean()),
+print(name, B, fl.stats(), {k: round(v[0], 2) for k, v in kt.items()}, "rounds mean", float(rr.rounds_run.double().mean()),
       "A mean", float(sol.augmentations.double().mean()), "rounds>=max", int((rr.rounds_run >= cfg.max_rounds).sum()))
