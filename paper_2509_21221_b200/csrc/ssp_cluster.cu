@@ -34,6 +34,7 @@ namespace {
 constexpr int CT = 512;      // threads per CTA
 constexpr int NW = CT / 32;  // warps per CTA: warp w relaxes rows w, w + NW, ... of a boundary
 constexpr int NBMAX = 64;    // chunk slots of the TMA ring (one chunk of NW rows per bulk copy)
+constexpr int KSP = 32;       // frontier relaxation when at most this many out-keys changed
 constexpr int KQ = 4;        // register-resident key chunks per lane (16-bit rows up to 1,024 weights)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr uint64_t INF = ~0ull;
@@ -46,12 +47,12 @@ struct Misc {  // per-CTA control block; the leader's copy is authoritative
   uint64_t tpart[2], red64;
   int32_t inst, A, status, pathlen;
   uint32_t votes[2];  // alternating slots: a CTA is at most one phase ahead of the slowest
-  int32_t red32, pred, nrem;
+  int32_t red32, pred, nrem, ucnt;
   uint32_t p2;  // 1 << H32, read back through a volatile load (see the relaxation)
 };
 
 struct ClLayout {
-  size_t misc, kin, kout, g, capE, srcf, snkf, kbuf, kb32, aq, ring, mbar, total;
+  size_t misc, kin, kout, g, capE, srcf, snkf, kbuf, kb32, aq, dmask, ring, mbar, total;
   int nbc;  // chunk slots of the ring (chunk = NW consecutive rows = one bulk copy)
 };
 __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
@@ -71,6 +72,7 @@ __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   L.kbuf = o; o += al16c(ldk * 8);
   L.kb32 = o; o += al16c(ldk * 4);
   L.aq = o; o += al16c((size_t)CT * 12);
+  L.dmask = o; o += al16c((size_t)P.S * ((R + 31) / 32) * 4);
   // as many chunk slots in flight as fit, up to the ceil(R / NW) chunks a CTA streams per
   // boundary.  Chunks, not rows: a bulk copy costs the TMA unit a fixed ~46 cycles, so 2 KB
   // rows would cap an SM at ~44 B/cycle (scratch probe), 32-64 KB chunks run at ~80 B/cycle.
@@ -101,6 +103,16 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   uint64_t* kbuf = (uint64_t*)(sm + L.kbuf);
   uint32_t* kb32 = (uint32_t*)(sm + L.kb32);
   uint32_t* aq = (uint32_t*)(sm + L.aq);  // staged path arcs: list key, boundary, list length
+  // out-keys changed since their boundary was last relaxed: bit (s, lv) of the owner, [S][DW]
+  const int DW = (R + 31) / 32;
+  uint32_t* dmask = (uint32_t*)(sm + L.dmask);
+  const bool track = true;
+  int ksp = KSP;  // frontier threshold (testing override GWTF_DEBUG_FLAGS bits 16..23; 8192: dense only)
+  if (P.debug & 8192) ksp = 0;
+  else if ((P.debug >> 16) & 0xFF) ksp = min(KSP, (P.debug >> 16) & 0xFF);
+  uint32_t* spu = aq;                       // frontier step: changed columns (reuses aq)
+  uint64_t* spk = (uint64_t*)(aq + KSP);    // ... and their out-keys
+  uint64_t* rowmin = kbuf;                  // ... per-row minima (reuses the gather buffer)
   uint8_t* ring = sm + L.ring;
   const int nbc = L.nbc;
   uint32_t* ecnt = (uint32_t*)(mbar + NBMAX);  // per chunk slot: rows consumed (monotonic)
@@ -216,6 +228,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
         kin[k] = ki;
         kout[k] = ko;
       }
+      if (track) for (int k = tid; k < S * DW; k += CT) dmask[k] = 0u;
+      uint64_t fresh = ~0ull;
       uint64_t tkey = INF;
       uint64_t fwd = S > 1 ? 1ull : 0ull, bwd = 1ull;
       bool tdirty = S == 1, trev = false;
@@ -227,6 +241,64 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           fwd &= ~(1ull << s);
           if (r == 0 && tid == 0) atomicAdd(&P.stats[0], 1ull);
           TMARK(9);
+          const bool fresh_s = (fresh >> s) & 1ull;
+          fresh &= ~(1ull << s);
+          if (!fresh_s && ksp > 0 && C * DW <= CT) {
+            // ---- frontier relaxation: after its first relaxation since the reset, boundary s only
+            // needs the columns u whose out-key changed since (dirty bits of the owners, DSMEM);
+            // in_{s+1,v} = min(in_{s+1,v}, out_{s,u} + w(u,v)) over those u is the same fixed point
+            if (tid == 0) { misc->ucnt = 0; misc->red32 = 0; }
+            __syncthreads();
+            uint32_t m = 0;  // one mask word per thread (C * DW <= CT)
+            if (tid < C * DW) {
+              m = *(cl.map_shared_rank(dmask, tid / DW) + s * DW + (tid % DW));
+              if (m) atomicAdd(&misc->red32, __popc(m));
+            }
+            __syncthreads();
+            const int nU = misc->red32;
+            if (nU <= ksp) {
+              if (m) {
+                int k = atomicAdd(&misc->ucnt, __popc(m));
+                for (; m; m &= m - 1) spu[k++] = (tid / DW) * R + (tid % DW) * 32 + (__ffs(m) - 1);
+              }
+              __syncthreads();
+              for (int i = tid; i < nU; i += CT) spk[i] = ldk_out(s, (int)spu[i]);
+              for (int j = tid; j < nr; j += CT) rowmin[j] = INF;
+              __syncthreads();
+              for (int t = tid; t < nr * nU; t += CT) {
+                const int j = t / nU, i = t - j * nU;
+                const uint64_t k = spk[i];
+                if (k == INF) continue;
+                const int32_t w = tile[((size_t)s * n + v0 + j) * ld + spu[i]];
+                if (w == kAbsent) continue;
+                atomicMin((unsigned long long*)&rowmin[j], (unsigned long long)(k + ((uint64_t)(uint32_t)w << kHopBits) + 1ull));
+              }
+              __syncthreads();
+              int chs = 0;
+              for (int j = tid; j < nr; j += CT) {
+                const uint64_t best = rowmin[j];
+                const int e = (s + 1) * R + j;
+                uint64_t kv = kin[e];
+                if (best < kv) { kin[e] = best; kv = best; chs = 1; }
+                if (kv != INF && g[e] < capE[e] && kv + 1 < kout[e]) {
+                  kout[e] = kv + 1;
+                  chs = 1;
+                  atomicOr(&dmask[(s + 1) * DW + (j >> 5)], 1u << (j & 31));
+                }
+              }
+              if (r == 0 && tid == 0) atomicAdd(&P.stats[11], 1ull);
+              TMARK(1);
+              const bool vfs = vote(chs);
+              for (int k = tid; k < DW; k += CT) dmask[s * DW + k] = 0u;  // every CTA has read it
+              TMARK(2);
+              if (vfs) {
+                if (s + 1 < S - 1) fwd |= 1ull << (s + 1);
+                else tdirty = true;
+                bwd |= 1ull << (s + 1);
+              }
+              continue;
+            }
+          }
           // chunk k (rows k*NW .. k*NW+NW-1, one per warp) goes to slot (slot0 + k) % nbc; the last
           // warp to finish a chunk refills its slot with chunk k + nbc, or, past the last chunk,
           // with chunk k + nbc - nch of boundary s + 1: the forward sweep's likely next step is
@@ -314,7 +386,11 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             int res = pres;
             if (k >= 32) { kv = kin[e]; ko = kout[e]; res = g[e] < capE[e]; }
             if (best < kv) { kin[e] = best; kv = best; ch = 1; }
-            if (kv != INF && res && kv + 1 < ko) { kout[e] = kv + 1; ch = 1; }
+            if (kv != INF && res && kv + 1 < ko) {
+              kout[e] = kv + 1;
+              ch = 1;
+              if (track) atomicOr(&dmask[(s + 1) * DW + (j >> 5)], 1u << (j & 31));
+            }
           };
           // every lane is done with its row of slot b (its values fed the warp minimum); the last
           // warp to finish the chunk refills the slot through the async proxy
@@ -469,6 +545,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           slot0 = (slot0 + nch) % nbc;
           TMARK(1);
           const bool vf = vote(ch);
+          if (track) for (int k = tid; k < DW; k += CT) dmask[s * DW + k] = 0u;  // every CTA read it
           TMARK(2);
           if (vf) {
             if (s + 1 < S - 1) fwd |= 1ull << (s + 1);
@@ -509,7 +586,11 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             for (int lv = tid; lv < nr; lv += CT) {
               if (snkf[lv] <= 0) continue;
               const uint64_t c = tkey - ((uint64_t)(uint32_t)snk[v0 + lv] << kHopBits) + 1ull;
-              if (c < kout[(S - 1) * R + lv]) { kout[(S - 1) * R + lv] = c; ch = 1; }
+              if (c < kout[(S - 1) * R + lv]) {
+                kout[(S - 1) * R + lv] = c;
+                ch = 1;
+                if (track) atomicOr(&dmask[(S - 1) * DW + (lv >> 5)], 1u << (lv & 31));
+              }
             }
           if (vote(ch)) bwd |= 1ull << (S - 1);
         }
@@ -539,6 +620,11 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             const uint64_t cand = ki - ((uint64_t)(uint32_t)w << kHopBits) + 1ull;
             const int q = own(u);
             const uint64_t old = dsmem_atomic_min_u64(dsmem_addr(kout + (s - 1) * R + (u - q * R), (uint32_t)q), cand);
+            if (track && cand < old) {
+              const int lu = u - q * R;
+              asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(dsmem_addr(dmask + (s - 1) * DW + (lu >> 5), (uint32_t)q)),
+                           "r"(1u << (lu & 31)) : "memory");
+            }
             if (cand < old) ch = 1;
           }
           if (vote(ch)) {

@@ -60,3 +60,7 @@ if os.environ.get("GWTF_DEBUG_FLAGS", "0") != "0" and int(os.environ["GWTF_DEBUG
     print("phase cycles (leader thread, all solves, summed over clusters):")
     for nm, c in zip(names, cyc):
         print(f"  {nm:10s} {c:14.0f}  {100 * c / tot:5.1f}%")
+if os.environ.get("GWTF_DEBUG_FLAGS", "0") != "0" and int(os.environ["GWTF_DEBUG_FLAGS"]) & 2048:
+    raw = fl.stats(raw=True)
+    h = raw[1200:1216]
+    print("changed columns per non-first relaxation (bucket: 0, 1, 2-3, 4-7, ...):", h.tolist())
