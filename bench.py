@@ -412,6 +412,7 @@ def main():
     A_total = 0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    launches0 = int(fl.stats(raw=True)[15])
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             prep()
@@ -426,6 +427,8 @@ def main():
             A_total += int(sol.augmentations.sum().item())
     ktimes = fl.kernel_times()
     fl.set_profiling(False)
+    # restore() between steps launches no kernels (device memcpys), so the difference is the steps'
+    launches_timed = int(fl.stats(raw=True)[15]) - launches0
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -464,9 +467,8 @@ def main():
                        "parallelism": f"instance-sharded x{world}"},
             "roofline": roof, "kernels": kshare, "clocks": clk.summary(),
             "gpu_launches": None}
-    # launches of our kernels per step: churn (edge updates if any + state clear) + ssp + rounds
-    per_step = 1 + (1 if upd is not None and upd.shape[0] else 0) + 1 + 1
-    line["gpu_launches"] = per_step * args.steps
+    # our kernels launched inside the timed steps, counted by the library (gwtf_flow_stats[15])
+    line["gpu_launches"] = launches_timed
 
     if rank == 0 and not (args.quick or args.no_e2e):
         line["e2e"] = e2e(cfg, B, inst0, dev, args)

@@ -192,9 +192,10 @@ gwtf_status gwtf_flow_kernel_times(gwtf_flow_t h, const char** names, float* ms,
  * microbatches and their total cost.  Does not touch the solver or round state. */
 gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_t* total_cost);
 
-/* Work counters of the exact solve accumulated since create (host int64 out[cap], cap <= 8):
+/* Work counters of the exact solve accumulated since create (host int64 out[cap], cap <= 2048):
  * [0] dense boundary relaxations, [1] backward (reverse-arc) phases, [2] augmentations,
- * [3] Bellman-Ford passes, [4] traced path nodes (cluster tier).  Synchronizes the stream. */
+ * [3] Bellman-Ford passes, [4] traced path nodes (cluster tier), [11] frontier relaxations (cluster
+ * tier), [15] kernels launched by this handle (host count).  Synchronizes the stream. */
 gwtf_status gwtf_flow_stats(gwtf_flow_t h, int64_t* out, int32_t cap);
 
 /* Synchronizes the stream, frees everything.  NULL is a no-op. */

@@ -64,6 +64,7 @@ struct gwtf_flow_s {
   int32_t* bad_flag = nullptr;
   // second stream of gwtf_flow_solve_and_rounds (created on first use)
   cudaStream_t stream2 = nullptr;
+  int64_t kernel_launches = 0;  // kernels this handle has launched (gwtf_flow_stats[15])
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
@@ -447,6 +448,7 @@ gwtf_status gwtf_flow_solve_batch(gwtf_flow_t h, int64_t* flow_value, int64_t* t
   const bool cluster = tier != 1 && h->P.cluster_size > 0 && (tier == 2 || ssp_smem_bytes(h->P) > 227 * 1024);
   prof_begin(h, cluster ? "ssp_cluster_kernel" : "ssp_kernel", &t);
   CK(h, launch_ssp(h->P, o, h->stream, h->num_sms, tier));
+  h->kernel_launches += ssp_launch_count(h->P, tier);
   prof_end(h, &t);
   h->has_assignment = true;
   return finish_out(h, maps);
@@ -469,6 +471,7 @@ gwtf_status gwtf_flow_decentralized_rounds(gwtf_flow_t h, int32_t max_rounds, in
   Timer t;
   prof_begin(h, "rounds_kernel", &t);
   CK(h, launch_rounds(h->P, o, h->stream, h->num_sms));
+  h->kernel_launches += 1;
   prof_end(h, &t);
   return finish_out(h, maps);
 }
@@ -505,11 +508,13 @@ gwtf_status gwtf_flow_solve_and_rounds(gwtf_flow_t h, int32_t max_rounds, int64_
   Timer tr, ts;
   prof_begin(h, "rounds_kernel", &tr, h->stream2);
   CK(h, launch_rounds(h->P, ro, h->stream2, h->num_sms));
+  h->kernel_launches += 1;
   prof_end(h, &tr, h->stream2);
   const int tier = (h->flags & GWTF_FORCE_GLOBAL_TIER) ? 1 : (h->flags & GWTF_FORCE_CLUSTER_TIER) ? 2 : 0;
   const bool cluster = tier != 1 && h->P.cluster_size > 0 && (tier == 2 || ssp_smem_bytes(h->P) > 227 * 1024);
   prof_begin(h, cluster ? "ssp_cluster_kernel" : "ssp_kernel", &ts);
   CK(h, launch_ssp(h->P, so, h->stream, h->num_sms, tier));
+  h->kernel_launches += ssp_launch_count(h->P, tier);
   prof_end(h, &ts);
   CK(h, cudaEventRecord(h->ev_join, h->stream2));
   CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
@@ -542,6 +547,7 @@ gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const
   Timer t;
   prof_begin(h, "churn", &t);
   CK(h, launch_churn(P, a, u, k, h->bad_flag, h->stream));
+  h->kernel_launches += 1 + (u && k > 0 ? 1 : 0);
   prof_end(h, &t);
   h->has_assignment = false;
   if (u) {
@@ -681,6 +687,7 @@ gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_
   Timer t;
   prof_begin(h, "greedy_kernel", &t);
   CK(h, launch_greedy(h->P, rem, F, C, h->stream));
+  h->kernel_launches += 1;
   prof_end(h, &t);
   return finish_out(h, maps);
 }
@@ -692,6 +699,7 @@ gwtf_status gwtf_flow_stats(gwtf_flow_t h, int64_t* out, int32_t cap) {
   std::vector<unsigned long long> v(2048);
   CK(h, cudaMemcpyAsync(v.data(), h->P.stats, 2048 * 8, cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
+  v[15] = (unsigned long long)h->kernel_launches;  // host-side: kernels launched by this handle
   for (int i = 0; i < std::min(cap, 2048); ++i) out[i] = (int64_t)v[i];
   return GWTF_OK;
 }

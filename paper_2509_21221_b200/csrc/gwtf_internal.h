@@ -87,6 +87,7 @@ int rounds_tpi(const Problem& P);
 bool rounds_use_smem(const Problem& P);
 // tier: 0 automatic (shared memory, else cluster, else global), 1 force global, 2 force cluster
 cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, int force_tier);
+int ssp_launch_count(const Problem& P, int force_tier);  // kernels launch_ssp issues
 size_t ssp_cluster_smem_bytes(const Problem& P, int C);
 int ssp_cluster_size(const Problem& P);
 cudaError_t launch_ssp_cluster(const Problem& P, const SspOut& o, cudaStream_t st, int C);

@@ -299,7 +299,6 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
                                             uint8_t* base, Red red, uint8_t* dsm, int* tma_init,
                                             uint32_t* tma_phase_of) {
   constexpr int TPI = TT::kTPI;
-  constexpr bool kCl = TPI > 1024;
   const int lane = threadIdx.x & 31;
   const int S = P.S, n = P.n, MC = P.MC, Sn = S * n;
   const int nres = Sn * MC + 2 * (int)P.Mmax;

@@ -620,6 +620,12 @@ cudaError_t launch_tpi(const Problem& P, const SspOut& o, cudaStream_t st, int n
 size_t ssp_smem_bytes(const Problem& P) { return ssp_layout(P, true, 8).total; }
 size_t ssp_global_ws_bytes(const Problem& P) { return ssp_layout(P, false, 8).total; }
 
+int ssp_launch_count(const Problem& P, int force_tier) {
+  const bool smem_tier = force_tier == 0 && ssp_smem_bytes(P) <= 227 * 1024;
+  if (!smem_tier) return 1;           // cluster tier or global tier: one kernel
+  return P.hbits == 0 ? 1 : 2;        // 32-bit keys: the solve and its 64-bit redo launch
+}
+
 cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, int force_tier) {
   // counters [0] ssp queue, [2] redo count, [3] redo queue ([1] is the rounds queue, which may be
   // running concurrently on another stream: gwtf_flow_solve_and_rounds)

@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const int H32 = 32 - __clz(2 * S * n + 2);
   const int CB32 = 32 - H32;
   const uint32_t T32 = CB32 >= 4 ? min((1u << (CB32 - 1)) - 1u, t16 ? 0xFFFFu : 0xFFFFFFFFu) : 0u;
-  const uint32_t T2 = T32 | (T32 << 16);  // per-halfword clamp of the 16-bit rows
   auto ldk_in = [&](int s, int v) -> uint64_t { const int q = own(v); return *(cl.map_shared_rank(kin, q) + s * R + (v - q * R)); };
   auto ldk_out = [&](int s, int v) -> uint64_t { const int q = own(v); return *(cl.map_shared_rank(kout, q) + s * R + (v - q * R)); };
   auto rg = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
@@ -455,7 +454,6 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 // 16-bit rows, pre-clamped (absent = T32): two weights per word, shifted into the
                 // cost field; with H32 >= 16 the low weight is one shift, the high one shift + mask
                 const uint4* row = (const uint4*)rowb;
-                const uint32_t hm = ~((1u << H32) - 1u);
                 if (kreg && H32 >= 16) {
                   // IMAD + VIMNMX: 3 issue slots per weight against 5 for SHF + VIADDMNMX
 #pragma unroll
