@@ -246,6 +246,39 @@ def other_configs(dev, steps=5, warmup=3):
     return out
 
 
+def multi_source(dev, B=8192, reps=1):
+    """SURVEY.md 8(f) f2, exact-solve part: flow-test settings 5 and 6 (2 / 4 data nodes),
+    single-commodity solves over the residual capacities in round-robin order, one
+    microbatch per data node per turn, B instances."""
+    import torch
+
+    from paper_2509_21221_b200.multisource import multi_source_ssp_unit as multi_source_ssp
+    out = {}
+    for name in ("flow5", "flow6"):
+        cfg = gen.CONFIGS[name]
+        K = cfg.extra["data_nodes"]
+        bt = gen.generate(cfg, 0, B)
+        xs, xk = gen.generate_data_nodes(cfg, 0, B, K)
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        srcs = [d(bt.src)] + [d(xs[k]) for k in range(K - 1)]
+        snks = [d(bt.snk)] + [d(xk[k]) for k in range(K - 1)]
+        sup = [d(np.full(B, cfg.M, np.int64)) for _ in range(K)]
+        args = (d(bt.cap), d(bt.alive), d(bt.link), srcs, snks, sup)
+        multi_source_ssp(*args, max_cap=cfg.max_cap)  # warm-up
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(reps):
+            res = multi_source_ssp(*args, max_cap=cfg.max_cap)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t) / reps
+        out[name] = {"data_nodes": K, "instances": B, "ms": dt * 1e3, "instances_per_s": B / dt,
+                     "F_per_data_node": [float(r[0].double().mean()) for r in res],
+                     "cost_per_data_node": [float(r[1].double().mean()) for r in res],
+                     "what": "wall clock per batch, one microbatch per data node per turn (a supply-1 solve "
+                             "and a handle create per turn)"}
+    return out
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -480,6 +513,7 @@ def main():
         line["node_addition"] = node_addition(dev)
         line["flow_quality"] = flow_quality(dev)
         line["other_configs"] = other_configs(dev)
+        line["multi_source"] = multi_source(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

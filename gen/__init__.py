@@ -124,6 +124,12 @@ CONFIGS = {
     "flow2": Config("flow2", 12, S=10, n=4, M=128, max_cap=3, cap=(1, 3), B=64, cost=(1, 20), max_rounds=120 + 256),
     "flow3": Config("flow3", 13, S=8, n=5, M=128, max_cap=15, cap=(5, 15), B=64, cost=(1, 20), max_rounds=120 + 256),
     "flow4": Config("flow4", 14, S=8, n=5, M=128, max_cap=3, cap=(1, 3), B=64, cost=(5, 100), max_rounds=120 + 256),
+    # flow-test settings 5-6: 2 / 4 data nodes, 40 / 80 relays over 8 stages; the extra
+    # data nodes' source and sink costs come from generate_data_nodes()
+    "flow5": Config("flow5", 15, S=8, n=5, M=128, max_cap=3, cap=(1, 3), B=64, cost=(1, 20), max_rounds=120 + 256,
+                    extra={"data_nodes": 2}),
+    "flow6": Config("flow6", 16, S=8, n=10, M=128, max_cap=3, cap=(1, 3), B=64, cost=(1, 20), max_rounds=120 + 256,
+                    extra={"data_nodes": 4}),
 }
 
 
@@ -260,6 +266,7 @@ def linkdrop_to_updates(linkdrop, inst_offset: int = 0):
 _M64 = (1 << 64) - 1
 GEN_F_VICTIM_STAGE, GEN_F_VICTIM_PICK = 15, 16
 GEN_F_CAND_CAP, GEN_F_CAND_IN, GEN_F_CAND_OUT, GEN_F_CAND_CC = 17, 18, 19, 20
+GEN_F_DN_SRC, GEN_F_DN_SNK = 21, 22
 
 
 def mix64(z: int) -> int:
@@ -339,3 +346,18 @@ def generate_candidates(cfg: Config, inst: int, base_seed: int = BASE_SEED):
     cout = _uniform_np(s, GEN_F_CAND_OUT, np.arange(S * S * n), cfg.cost[0], cfg.cost[1]).reshape(S, S, n)
     cc = _uniform_np(s, GEN_F_CAND_CC, np.arange(S * S), cfg.cost[0], cfg.cost[1]).reshape(S, S)
     return {"cap": cap, "cin": cin, "cout": cout, "cc": cc}
+
+
+def generate_data_nodes(cfg: Config, inst0: int, B: int, K: int, base_seed: int = BASE_SEED):
+    """Source and sink costs of data nodes 1..K-1 of instances inst0.. (data node 0 keeps the batch's
+    src/snk): src [K-1][B][n], snk [K-1][B][n], costs U{cost} like the flow-test links."""
+    n = cfg.n
+    src = np.zeros((max(K - 1, 0), B, n), np.int32)
+    snk = np.zeros_like(src)
+    for b in range(B):
+        s = instance_seed(cfg, inst0 + b, base_seed)
+        for k in range(1, K):
+            idx = np.arange((k - 1) * n, k * n)
+            src[k - 1, b] = _uniform_np(s, GEN_F_DN_SRC, idx, cfg.cost[0], cfg.cost[1])
+            snk[k - 1, b] = _uniform_np(s, GEN_F_DN_SNK, idx, cfg.cost[0], cfg.cost[1])
+    return src, snk

@@ -159,6 +159,12 @@ gwtf_status gwtf_flow_solve_and_rounds(gwtf_flow_t h, int32_t max_rounds, int64_
 gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const int32_t* edge_updates,
                                   int64_t k);
 
+/* Residual node capacities after the last solve_batch, cap_out [B][S][n] = (alive ? cap : 0) - node flow:
+ * the capacities the next data node's single-commodity problem sees in the multi-data-node
+ * decomposition (one single-commodity problem per data node over
+ * residual capacities, in round-robin order).  STATE if no solve has run since create/churn. */
+gwtf_status gwtf_flow_residual_caps(gwtf_flow_t h, int32_t* cap_out);
+
 /* Canonical assignment of the last solve_batch: node_flow [B][S][n], src_flow [B][n],
  * snk_flow [B][n], arc_flow_dense [B][S-1][n_dst][n_src] (any may be NULL).  STATE if no
  * solve has run since create/churn. */

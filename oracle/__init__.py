@@ -453,3 +453,48 @@ def greedy_route(I: Instance):
         cost += c + int(I.snk[u])
         paths.append(path)
     return F, cost, paths
+
+
+# ---- multi-data-node flows ----
+
+def multi_source_ssp_unit(I: Instance, srcs, snks, supplies):
+    """Round-robin by microbatch (the other reading of SPEC.md:215's "round-robin order"): the data
+    nodes take turns, each turn routing one microbatch of one data node by a single-commodity
+    canonical SSP with supply 1 on the node capacities left so far; a data node that cannot route
+    drops out.  Returns per data node (F, cost, node_flow)."""
+    K = len(srcs)
+    cap = I.cap_eff().astype(np.int32).copy()
+    F = [0] * K
+    C = [0] * K
+    nf = [np.zeros((I.S, I.n), np.int32) for _ in range(K)]
+    active = [int(M) > 0 for M in supplies]
+    while any(active):
+        for k in range(K):
+            if not active[k]:
+                continue
+            r = ssp(Instance(I.S, I.n, I.max_cap, 1, cap, srcs[k], snks[k], I.link))
+            if r.F == 0:
+                active[k] = False
+                continue
+            F[k] += 1
+            C[k] += r.cost
+            nf[k] += r.node_flow
+            cap = cap - r.node_flow
+            if F[k] >= int(supplies[k]):
+                active[k] = False
+    return [(F[k], C[k], nf[k]) for k in range(K)]
+
+
+def multi_source_ssp(I: Instance, srcs, snks, supplies):
+    """One single-commodity canonical SSP per data node, in data-node order, each on the node
+    capacities the earlier data nodes left ("one single-commodity problem per data node
+    over residual capacities in round-robin order" -- a heuristic decomposition; the paper does not
+    compare settings 5-6 with an optimum).  Returns per data node (F, cost, node_flow)."""
+    cap = I.cap_eff().astype(np.int32).copy()
+    out = []
+    for src, snk, M in zip(srcs, snks, supplies):
+        Ik = Instance(I.S, I.n, I.max_cap, int(M), cap, src, snk, I.link)
+        r = ssp(Ik)
+        out.append((r.F, r.cost, r.node_flow.copy()))
+        cap = cap - r.node_flow
+    return out

@@ -6,3 +6,4 @@ its thin Python binding plus the multi-GPU sharding helper (dist.py).  See DESIG
 from ._lib import GWTF_HOST_PTRS, OBJ_MINIMAX, OBJ_SUM, GwtfError, lib  # noqa: F401
 from .flow import ABSENT, Flow, RoundsResult, SolveResult, eq1_cost_tiles  # noqa: F401
 from . import addition  # noqa: F401,E402
+from . import multisource  # noqa: F401,E402

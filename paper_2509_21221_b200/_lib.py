@@ -47,6 +47,7 @@ EXPORTS = {
     "gwtf_flow_solve_and_rounds": ([P, I32, P, P, P, P, P, P, P, P], I32),
     "gwtf_flow_apply_churn": ([P, P, P, I64], I32),
     "gwtf_flow_get_assignment": ([P, P, P, P, P], I32),
+    "gwtf_flow_residual_caps": ([P, P], I32),
     "gwtf_flow_export_round_state": ([P, P, P, P, P, P, P, P, P], I32),
     "gwtf_flow_snapshot": ([P], I32),
     "gwtf_flow_restore": ([P], I32),

@@ -219,6 +219,18 @@ cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32
   return cudaGetLastError();
 }
 
+// residual node capacities after the last exact solve: (alive ? cap : 0) - node flow
+__global__ void residual_caps_kernel(const Problem P, int32_t* __restrict__ out) {
+  const size_t total = (size_t)P.B * P.S * P.n;
+  for (size_t t = gtid(); t < total; t += gstride()) out[t] = (P.alive[t] ? P.cap[t] : 0) - P.g[t];
+}
+
+cudaError_t launch_residual_caps(const Problem& P, int32_t* out, cudaStream_t st) {
+  const size_t total = (size_t)P.B * P.S * P.n;
+  if (total) residual_caps_kernel<<<grid_for(total), 256, 0, st>>>(P, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dense_arcs(const Problem& P, int32_t* dense, cudaStream_t st) {
   const size_t total = (size_t)P.B * (P.S - 1) * P.Lcap;
   if (total) dense_arcs_kernel<<<grid_for(total), 256, 0, st>>>(P, dense);

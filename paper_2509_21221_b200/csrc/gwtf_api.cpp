@@ -586,6 +586,27 @@ gwtf_status gwtf_flow_get_assignment(gwtf_flow_t h, int32_t* node_flow, int32_t*
   return GWTF_OK;
 }
 
+gwtf_status gwtf_flow_residual_caps(gwtf_flow_t h, int32_t* cap_out) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!cap_out) return fail(GWTF_E_INVALID, "residual_caps: NULL output");
+  if (!h->has_assignment) return fail(GWTF_E_STATE, "no solve_batch since create/churn");
+  const Problem& P = h->P;
+  const size_t bytes = (size_t)P.B * P.S * P.n * 4;
+  int32_t* dst = cap_out;
+  if (host_mode(h)) {
+    dst = (int32_t*)scratch(h, 17, bytes);
+    if (!dst) return fail(GWTF_E_NOMEM, "scratch");
+  }
+  CK(h, launch_residual_caps(P, dst, h->stream));
+  h->kernel_launches += 1;
+  if (host_mode(h)) {
+    CK(h, cudaMemcpyAsync(cap_out, dst, bytes, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  }
+  return GWTF_OK;
+}
+
 gwtf_status gwtf_flow_export_round_state(gwtf_flow_t h, int32_t* up, int32_t* down, int32_t* src_down,
                                          int32_t* snk_up, int32_t* kacc, int32_t* deny, int32_t* quiet,
                                          int64_t* round) {

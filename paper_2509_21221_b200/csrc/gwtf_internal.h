@@ -98,6 +98,7 @@ cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st);
 cudaError_t launch_pack_tile16(const Problem& P, cudaStream_t st);
 cudaError_t launch_dense_arcs(const Problem& P, int32_t* dense, cudaStream_t st);
+cudaError_t launch_residual_caps(const Problem& P, int32_t* out, cudaStream_t st);
 cudaError_t launch_eq1(int32_t B, int32_t S, int32_t n, int32_t L, const int32_t* comp, const int32_t* loc,
                        const int32_t* dloc, const int32_t* lat, const int32_t* bw, int64_t size_kbit,
                        int32_t* src, int32_t* snk, int32_t* link, cudaStream_t st);

@@ -172,6 +172,12 @@ class Flow:
         check("gwtf_flow_apply_churn", lib().gwtf_flow_apply_churn(
             self.h, _ptr(alive_new), _ptr(edge_updates) if k else None, k))
 
+    def residual_caps(self):
+        """(alive ? cap : 0) - node flow of the last solve (gwtf_flow_residual_caps), [B][S][n] int32."""
+        out = self._out((self.B, self.S, self.n), torch.int32)
+        check("gwtf_flow_residual_caps", lib().gwtf_flow_residual_caps(self.h, _ptr(out)))
+        return out
+
     def get_assignment(self, dense_arcs: bool = True):
         B, S, n = self.B, self.S, self.n
         nf = self._out((B, S, n), torch.int32)

@@ -1,0 +1,60 @@
+"""Multi-data-node flows (exact-solve part) over the C-ABI.
+
+PAPER.md:203 and the flow-test settings 5-6 have several data nodes, each of which
+must get its own microbatches back.  SPEC.md:215 decomposes this heuristically: one single-commodity
+problem per data node, in data-node order, each over the node capacities the earlier ones left.
+Every step of the method runs in the library's kernels: the exact solves (gwtf_flow_solve_batch) and the
+residual capacities (gwtf_flow_residual_caps); this module sequences the calls and keeps per-data-node
+totals (torch additions of the per-call outputs).  Two readings of "round-robin order": whole data nodes
+one after another (multi_source_ssp), or one microbatch per data node per turn (multi_source_ssp_unit).
+"""
+from __future__ import annotations
+
+import torch
+
+from .flow import Flow
+
+
+def multi_source_ssp(cap, alive, link_cost, src_costs, snk_costs, supplies, *, max_cap: int, stream=None):
+    """cap/alive [B][S][n], link_cost [B][S-1][n][n], src_costs/snk_costs: K tensors [B][n] (one per
+    data node), supplies: K tensors [B] (int64).  Returns K (flow_value, total_cost, node_flow) triples."""
+    out = []
+    cap_k, alive_k = cap, alive
+    for src, snk, M in zip(src_costs, snk_costs, supplies):
+        fl = Flow(cap_k, src, snk, link_cost, M, max_cap=max_cap, alive=alive_k, stream=stream)
+        sol = fl.solve_batch()
+        nf, _, _, _ = fl.get_assignment(dense_arcs=False)
+        cap_k, alive_k = fl.residual_caps(), None
+        out.append((sol.flow_value, sol.total_cost, nf))
+        fl.close()
+    return out
+
+
+def multi_source_ssp_unit(cap, alive, link_cost, src_costs, snk_costs, supplies, *, max_cap: int, stream=None):
+    """Round-robin by microbatch: the data nodes take turns routing one microbatch each (a supply-1
+    exact solve over the capacities left so far) until none can; same outputs as multi_source_ssp.
+    Instances whose data node k is done get supply 0 in its later turns."""
+    K = len(src_costs)
+    B = cap.shape[0]
+    dev = cap.device
+    cap_r = torch.where(alive != 0, cap, torch.zeros_like(cap)) if alive is not None else cap.clone()
+    F = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(K)]
+    C = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(K)]
+    NF = [torch.zeros_like(cap) for _ in range(K)]
+    active = [torch.ones(B, dtype=torch.bool, device=dev) & (supplies[k] > 0) for k in range(K)]
+    while any(bool(a.any()) for a in active):
+        for k in range(K):
+            if not bool(active[k].any()):
+                continue
+            fl = Flow(cap_r, src_costs[k], snk_costs[k], link_cost, active[k].to(torch.int64), max_cap=max_cap,
+                      stream=stream)
+            sol = fl.solve_batch()
+            nf, _, _, _ = fl.get_assignment(dense_arcs=False)
+            cap_r = fl.residual_caps()
+            fl.close()
+            routed = sol.flow_value > 0
+            F[k] += sol.flow_value
+            C[k] += sol.total_cost
+            NF[k] += nf
+            active[k] = active[k] & routed & (F[k] < supplies[k])
+    return [(F[k], C[k], NF[k]) for k in range(K)]
