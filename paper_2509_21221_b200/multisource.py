@@ -37,7 +37,7 @@ def multi_source_ssp_unit(cap, alive, link_cost, src_costs, snk_costs, supplies,
     K = len(src_costs)
     B = cap.shape[0]
     dev = cap.device
-    cap_r = torch.where(alive != 0, cap, torch.zeros_like(cap)) if alive is not None else cap.clone()
+    cap_r, alive_r = cap, alive  # the first solve applies the alive mask; residual caps include it
     F = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(K)]
     C = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(K)]
     NF = [torch.zeros_like(cap) for _ in range(K)]
@@ -47,10 +47,10 @@ def multi_source_ssp_unit(cap, alive, link_cost, src_costs, snk_costs, supplies,
             if not bool(active[k].any()):
                 continue
             fl = Flow(cap_r, src_costs[k], snk_costs[k], link_cost, active[k].to(torch.int64), max_cap=max_cap,
-                      stream=stream)
+                      alive=alive_r, stream=stream)
             sol = fl.solve_batch()
             nf, _, _, _ = fl.get_assignment(dense_arcs=False)
-            cap_r = fl.residual_caps()
+            cap_r, alive_r = fl.residual_caps(), None
             fl.close()
             routed = sol.flow_value > 0
             F[k] += sol.flow_value
