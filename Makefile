@@ -9,7 +9,9 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fno-fas
 PKG := paper_2509_21221_b200
 CSRC := $(PKG)/csrc
 KERN := $(wildcard $(CSRC)/*.cu)
-HDRS := $(wildcard $(CSRC)/*.cuh) include/gwtf.h
+HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/gwtf_internal.h include/gwtf.h
+OBJDIR := $(CSRC)/build
+OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(KERN)) $(OBJDIR)/gwtf_api.o
 
 all: gen/libgwtfgen.so oracle/liboracle.so $(PKG)/libgwtf.so
 
@@ -19,10 +21,20 @@ gen/libgwtfgen.so: gen/gen.cu gen/gwtf_gen.h
 oracle/liboracle.so: oracle/oracle.cpp oracle/oracle.h
 	$(CXX) -O2 -std=c++17 -fPIC -fno-fast-math -Wall -shared -o $@ oracle/oracle.cpp -lpthread
 
-$(PKG)/libgwtf.so: $(KERN) $(CSRC)/gwtf_api.cpp $(HDRS)
-	$(NVCC) $(NVFLAGS) -Iinclude -Xptxas -v -shared -o $@ $(KERN) $(CSRC)/gwtf_api.cpp 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
+# one object per translation unit (parallel with make -j), ptxas resource usage in build/*.ptxas.log
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Iinclude -Xptxas -v -c -o $@ $< 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; false)
+
+$(OBJDIR)/gwtf_api.o: $(CSRC)/gwtf_api.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $<
+
+$(PKG)/libgwtf.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	@cat $(OBJDIR)/*.ptxas.log > $(CSRC)/ptxas.log
 
 clean:
-	rm -f gen/libgwtfgen.so oracle/liboracle.so $(PKG)/libgwtf.so
+	rm -rf gen/libgwtfgen.so oracle/liboracle.so $(PKG)/libgwtf.so $(OBJDIR)
 
 .PHONY: all clean
