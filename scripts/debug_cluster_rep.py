@@ -1,3 +1,4 @@
+"""Repeats small forced-cluster-tier solves (flow1, gpt, flow3) 80 times against the oracle (races show up as mismatches)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

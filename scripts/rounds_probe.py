@@ -1,5 +1,6 @@
+"""Rounds run per instance in the GPT churn protocol (base convergence and repair), augmentations per solve."""
 import sys, os, json
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np
 import gen
 from tests import harness
