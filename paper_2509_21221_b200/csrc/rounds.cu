@@ -193,9 +193,8 @@ struct ClusterTeam {
   uint32_t vid;     // vote counter (uniform over the cluster)
   __device__ __forceinline__ void sync() const { cg::this_cluster().sync(); }
   __device__ int sync_or(int p) {
-    const int any = __syncthreads_or(p);
     ++vid;
-    if (threadIdx.x == 0) vslot[vid & 1] = any ? vid : 0u;
+    if (p) vslot[vid & 1] = vid;  // stamp (idempotent); the cluster barrier orders it before the reads
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     int res = 0;

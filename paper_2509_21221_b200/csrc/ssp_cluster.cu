@@ -204,9 +204,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
 
     // vote: did any CTA of the cluster change something in this phase?  (cluster barrier)
     auto vote = [&](int ch) -> bool {
-      const int any = __syncthreads_or(ch);
+      // a thread that changed something stamps its CTA's slot with the vote id (idempotent); the
+      // cluster barrier orders every stamp before the reads, so no CTA-level reduction is needed
       ++vote_id;
-      if (tid == 0) misc->votes[vote_id & 1] = any ? vote_id : 0u;  // own slot, double-buffered
+      if (ch) misc->votes[vote_id & 1] = vote_id;  // own slot, double-buffered
       cl.sync();
       bool res = false;
       for (int q = 0; q < C; ++q) res |= cl.map_shared_rank(misc, q)->votes[vote_id & 1] == vote_id;
