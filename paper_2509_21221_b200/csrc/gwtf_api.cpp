@@ -342,6 +342,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
       uint8_t* wc = nullptr;
       if ((s = alloc(h, &wc, (size_t)P.ws_cluster_slots * 2 * (2 * Sn + 4) * 4)) != GWTF_OK) return bail(s);
       P.ws_cluster = wc;
+      if ((s = alloc(h, &P.arcw, B * std::max<size_t>(nb, 1) * P.Lcap)) != GWTF_OK) return bail(s);
     } else if (h->flags & GWTF_FORCE_CLUSTER_TIER) {
       return bail(fail(GWTF_E_UNSUPPORTED, "cluster tier unavailable for this shape"));
     }

@@ -33,6 +33,7 @@ struct Problem {
   int32_t* snk_f;              // [B][n]
   uint32_t* arcs;              // [B][S-1][Lcap]  (u << 20 | v << 8 | f)
   int32_t* arc_cnt;            // [B][S-1]
+  int32_t* arcw;               // cluster tier: [B][S-1][Lcap] weight of each list entry
   // round state
   int32_t* up;                 // [B][S*n*MC]
   int32_t* down;               // [B][S*n*MC]

@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
     const int32_t* src = P.src + (size_t)inst * n;
     const int32_t* snk = P.snk + (size_t)inst * n;
     uint32_t* arcs = P.arcs + (size_t)inst * (S - 1) * Lcap;
+    int32_t* arcw = P.arcw + (size_t)inst * (S - 1) * Lcap;  // weight of each list entry (no tile fetch)
     int32_t* cnt = P.arc_cnt + (size_t)inst * (S - 1);
     for (int k = tid; k < S * R; k += CT) {
       const int s = k / R, v = v0 + k % R;
@@ -610,12 +611,12 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           int ch = 0;
           for (int e = r * CT + tid; e < c; e += C * CT) {
             const uint32_t ent = __ldcg(&al[e]);
+            const int32_t w = __ldcg(&arcw[(size_t)(s - 1) * Lcap + e]);
             const int u = (int)(ent >> 20), v = (int)((ent >> 8) & 0xFFFu);
             uint64_t ki = ldk_in(s, v);
             const uint64_t kov = ldk_out(s, v);
             if (*rg(s, v) > 0 && kov != INF && kov + 1 < ki) ki = kov + 1;
             if (ki == INF) continue;
-            const int32_t w = tile[((size_t)(s - 1) * n + v) * ld + u];
             const uint64_t cand = ki - ((uint64_t)(uint32_t)w << kHopBits) + 1ull;
             const int q = own(u);
             const uint64_t old = dsmem_atomic_min_u64(dsmem_addr(kout + (s - 1) * R + (u - q * R), (uint32_t)q), cand);
@@ -719,7 +720,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 if ((int)(ent >> 20) != i) continue;
                 const int v = (int)((ent >> 8) & 0xFFFu);
                 const uint64_t k = ldk_in(s + 1, v);
-                const int32_t w = tile[((size_t)s * n + v) * ld + i];
+                const int32_t w = __ldcg(&arcw[(size_t)s * Lcap + e]);
                 if (k != INF && k + 1ull == kx + ((uint64_t)(uint32_t)w << kHopBits)) atomicMin(&misc->red32, v);
               }
               __syncthreads();
@@ -873,6 +874,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 if (q < 0) { misc->status = 2; continue; }
                 const int c = __ldcg(&cnt[sb]);
                 __stcg(&al[q], __ldcg(&al[c - 1]));
+                __stcg(&arcw[(size_t)sb * Lcap + q], __ldcg(&arcw[(size_t)sb * Lcap + c - 1]));
                 __stcg(&cnt[sb], c - 1);
               }
             __syncthreads();
@@ -884,8 +886,12 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             if (u == 0 || lv == Lt || !(!(lu & 1) && lv == lu + 1) || __ldcg(&found[e]) != INT_MAX) continue;
             const int sb = (lu >> 1) - 1;
             const int q = atomicAdd(&cnt[sb], 1);
-            if (q < Lcap) __stcg(&arcs[(size_t)sb * Lcap + q], ((uint32_t)pu << 20) | ((uint32_t)pv << 8) | (uint32_t)d);
-            else misc->status = 2;
+            if (q < Lcap) {
+              __stcg(&arcs[(size_t)sb * Lcap + q], ((uint32_t)pu << 20) | ((uint32_t)pv << 8) | (uint32_t)d);
+              __stcg(&arcw[(size_t)sb * Lcap + q], tile[((size_t)sb * n + pv) * ld + pu]);
+            } else {
+              misc->status = 2;
+            }
           }
           __syncthreads();
           if (tid == 0) {
