@@ -1,7 +1,7 @@
 // Exact solve, cluster tier: one thread-block cluster (up to 16 CTAs, one per SM) per instance,
 // for instances whose tiles cannot live in shared memory (e.g. the stress shape: 64 stages x
 // 1,024 clients = 252 MB of int32 tiles).  Same canonical SSP as ssp.cu with
-// 64-bit (cost, hops) keys; only the data placement differs:
+// 64-bit (cost, hops) keys; only the data placement differs (K1c):
 //   * CTA r of the cluster owns destination rows v in [r*R, r*R+R) of every stage: their in/out
 //     keys, node flows and capacities live in its shared memory (read remotely through DSMEM;
 //     reverse arcs relax into the owner's keys with a DSMEM 64-bit compare-and-swap min,
@@ -9,14 +9,17 @@
 //   * the dense min-plus relaxation of boundary s streams the CTA's R rows of tile s from HBM
 //     in chunks of NW rows (one cp.async.bulk per chunk, one mbarrier per ring slot; the last
 //     warp to finish a chunk refills its slot), from a 16-bit copy of the tiles when the costs
-//     fit (half the bytes), with 32-bit DPX keys (VIADDMNMX) held in registers when the costs
-//     allow, while the out_s key vector is gathered from the owner CTAs through DSMEM;
+//     fit (half the bytes), with 32-bit keys held in registers when the costs allow (IMAD +
+//     VIMNMX per weight, not the quarter-rate DPX VIADDMNMX), while the out_s key vector is
+//     gathered from the owner CTAs through DSMEM;
+//   * after a boundary's first relaxation since the reset, later ones relax only the columns
+//     whose out-key changed (owner dirty bits) when there are at most KSP of them (frontier);
 //   * one cluster barrier per boundary step; phase votes and the t* minimum are reduced from
 //     per-CTA slots read by every CTA (no remote atomics, no resets);
 //   * the leader CTA traces the canonical path; the whole cluster locates the path's arcs in the
-//     positive-arc lists; the leader augments.  The lists stay in global memory and are only
-//     accessed through L2: written by the leader's SM, read by the other SMs of the cluster,
-//     whose L1 would otherwise serve stale lines.
+//     positive-arc lists (with each entry's weight beside it); the leader augments.  The lists
+//     stay in global memory and are only accessed through L2: written by the leader's SM, read
+//     by the other SMs of the cluster, whose L1 would otherwise serve stale lines.
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
