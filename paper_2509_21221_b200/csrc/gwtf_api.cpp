@@ -83,13 +83,37 @@ gwtf_status cuda_fail(gwtf_flow_s* h, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail((h), _e, #expr);  \
   } while (0)
 
+// Device memory of a handle comes from the device's stream-ordered pool (cudaMallocAsync on the
+// handle's stream): creating and destroying handles back to back (the e2e pipeline, node-addition
+// batches, multi-source turns) then reuses pool memory instead of paying cudaMalloc/cudaFree,
+// whose unmap synchronises the device.  The pool keeps up to kPoolKeep bytes across handles.
+constexpr uint64_t kPoolKeep = 8ull << 30;
+void* dev_alloc(gwtf_flow_s* h, size_t bytes) {
+  static bool configured[64] = {};
+  if (h->device >= 0 && h->device < 64 && !configured[h->device]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+      uint64_t keep = kPoolKeep;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    configured[h->device] = true;
+  }
+  void* q = nullptr;
+  if (cudaMallocAsync(&q, bytes, h->stream) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  return q;
+}
+void dev_free(gwtf_flow_s* h, void* p) {
+  if (p) cudaFreeAsync(p, h->stream);
+}
+
 template <class T>
 gwtf_status alloc(gwtf_flow_s* h, T** p, size_t count, bool is_mutable = false) {
   if (count == 0) count = 1;
-  void* q = nullptr;
-  if (cudaMalloc(&q, count * sizeof(T)) != cudaSuccess) {
+  void* q = dev_alloc(h, count * sizeof(T));
+  if (!q) {
     cudaGetLastError();
-    return fail(GWTF_E_NOMEM, "cudaMalloc failed (" + std::to_string(count * sizeof(T)) + " bytes)");
+    return fail(GWTF_E_NOMEM, "device allocation failed (" + std::to_string(count * sizeof(T)) + " bytes)");
   }
   h->allocs.push_back(q);
   if (is_mutable) h->mutable_bufs.push_back({q, count * sizeof(T)});
@@ -102,10 +126,10 @@ void* scratch(gwtf_flow_s* h, size_t i, size_t bytes) {
   if (h->scratch.size() <= i) h->scratch.resize(i + 1);
   DevBuf& b = h->scratch[i];
   if (b.bytes < bytes) {
-    if (b.p) cudaFree(b.p);
+    dev_free(h, b.p);
     b.p = nullptr;
     b.bytes = 0;
-    if (cudaMalloc(&b.p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    if (!(b.p = dev_alloc(h, bytes))) return nullptr;
     b.bytes = bytes;
   }
   return b.p;
@@ -407,7 +431,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     P.hbits = (H < 29 && ((maxc << H) + 1) < (1ll << 29)) ? H : 0;
   }
   if (link_tmp) {
-    cudaFree(link_tmp);
+    dev_free(h, link_tmp);
     h->allocs.erase(std::find(h->allocs.begin(), h->allocs.end(), (void*)link_tmp));
   }
   {  // absent code of the 16-bit tiles = the cluster tier's 32-bit key clamp T32 (ssp_cluster.cu)
@@ -635,7 +659,7 @@ gwtf_status gwtf_flow_snapshot(gwtf_flow_t h) {
   if (!h->has_snapshot) {
     for (auto& mb : h->mutable_bufs) {
       void* q = nullptr;
-      if (cudaMalloc(&q, mb.second) != cudaSuccess) { cudaGetLastError(); return fail(GWTF_E_NOMEM, "snapshot"); }
+      if (!(q = dev_alloc(h, mb.second))) return fail(GWTF_E_NOMEM, "snapshot");
       h->snap.push_back(q);
     }
     h->has_snapshot = true;
@@ -737,9 +761,9 @@ gwtf_status gwtf_flow_destroy(gwtf_flow_t h) {
     cudaEventDestroy(h->ev_join);
   }
   for (Timer& t : h->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
-  for (void* p : h->allocs) cudaFree(p);
-  for (void* p : h->snap) cudaFree(p);
-  for (DevBuf& b : h->scratch) if (b.p) cudaFree(b.p);
+  for (void* p : h->allocs) dev_free(h, p);
+  for (void* p : h->snap) dev_free(h, p);
+  for (DevBuf& b : h->scratch) dev_free(h, b.p);
   cudaGetLastError();
   delete h;
   return GWTF_OK;

@@ -384,9 +384,15 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     uint64_t round = (uint64_t)P.round[b];
     int r = 0;
     T.sync();
+    bool prev_quiet = false;  // the last round changed nothing (the first round of a call always runs)
     while (r < o.max_rounds) {
       int changed = 0;
       I.set_round(round);
+      // after a quiet round the slot state is what it was at that round's start (only the deny
+      // counters moved, and R0-R3 do not read them): R0a..R3 would recompute the same costs, the
+      // same requests and again no grant, so the round starts at R4 (its RNG is the only input
+      // that differs); scost, adv_cost and req_* still hold the previous round's values
+      if (!prev_quiet) {
       // ---------- R0a candidates: a relay holding an IN and an OUT slot ----------
       if (T.tid == 0) { sh_i32[0] = INT_MAX; sh_i32[1] = 0; }
       int cand = 0;
@@ -535,6 +541,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         }
       }
       T.sync();
+      }  // !prev_quiet
       // ---------- R4 proposals by idle relays (post-R3 state) + R5 reservations ----------
       for (int p = T.tid; p < Sn; p += TPI) {
         int kind = K_NONE;
@@ -666,6 +673,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       // ---------- R7 ----------
       const int any = T.sync_or(changed);
       quiet = any ? 0 : quiet + 1;
+      prev_quiet = !any;
       round += 1;
       if (o.digests) {
         if (T.tid == 0) sh_u64[0] = 0;
