@@ -108,7 +108,7 @@ struct Inst {
   __device__ uint32_t summarize(int v) const {
     uint32_t fi = 63, ff = 63, np = 0, ho = 0;
     const int c = capv[v], base = v * MC;
-    for (int j = 0; j < c; ++j) {
+    _Pragma("unroll 1") for (int j = 0; j < c; ++j) {
       const int t = st(base + j);
       if (t == ST_IN && fi == 63) fi = j;
       if (t == ST_FREE && ff == 63) ff = j;
@@ -123,7 +123,7 @@ struct Inst {
   __device__ int64_t relay_costs(int v) const {
     const int s0 = dn.div(v), i0 = v - s0 * n, c = capv[v];
     int64_t best = INF;
-    for (int j = 0; j < c; ++j) {
+    _Pragma("unroll 1") for (int j = 0; j < c; ++j) {
       const int p0 = v * MC + j;
       int32_t p = down[p0];
       int64_t cc = p == kNone ? INF : 0;
@@ -167,7 +167,7 @@ struct Inst {
   __device__ int64_t relay_adv(int v) const {
     int64_t bc = INF;
     const int c = capv[v];
-    for (int j = 0; j < c; ++j) {
+    _Pragma("unroll 1") for (int j = 0; j < c; ++j) {
       const int p = v * MC + j;
       if (up[p] == kNone && down[p] != kNone && scost[p] < bc) bc = scost[p];
     }
@@ -175,7 +175,7 @@ struct Inst {
   }
   __device__ int nth_paired(int v, int q) const {
     const int c = capv[v], base = v * MC;
-    for (int j = 0; j < c; ++j)
+    _Pragma("unroll 1") for (int j = 0; j < c; ++j)
       if (st(base + j) == ST_PAIRED) { if (q == 0) return base + j; --q; }
     return -1;
   }
@@ -366,9 +366,9 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           bulk_g2s(base + Lr.tile + off, (const uint8_t*)gtile + off, tbytes - off < 32768u ? tbytes - off : 32768u,
                    mbar);
       }
-      for (int k = T.tid; k < Sn * MC; k += TPI) { I.up[k] = g_up[k]; I.down[k] = g_down[k]; }
-      for (int k = T.tid; k < M; k += TPI) { I.src_down[k] = g_src_down[k]; I.snk_up[k] = g_snk_up[k]; }
-      for (int k = T.tid; k < Sn; k += TPI) { I.kacc[k] = g_kacc[k]; I.deny[k] = g_deny[k]; }
+      _Pragma("unroll 1") for (int k = T.tid; k < Sn * MC; k += TPI) { I.up[k] = g_up[k]; I.down[k] = g_down[k]; }
+      _Pragma("unroll 1") for (int k = T.tid; k < M; k += TPI) { I.src_down[k] = g_src_down[k]; I.snk_up[k] = g_snk_up[k]; }
+      _Pragma("unroll 1") for (int k = T.tid; k < Sn; k += TPI) { I.kacc[k] = g_kacc[k]; I.deny[k] = g_deny[k]; }
       T.sync();
       if (tbytes) {  // barrier init visible; every thread waits on the transaction barrier
         const uint32_t ph = tma_phase_of[T.id];
@@ -742,9 +742,9 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     }
     T.sync();
     if constexpr (kSmem) {
-      for (int k = T.tid; k < Sn * MC; k += TPI) { g_up[k] = I.up[k]; g_down[k] = I.down[k]; }
-      for (int k = T.tid; k < M; k += TPI) { g_src_down[k] = I.src_down[k]; g_snk_up[k] = I.snk_up[k]; }
-      for (int k = T.tid; k < Sn; k += TPI) { g_kacc[k] = I.kacc[k]; g_deny[k] = I.deny[k]; }
+      _Pragma("unroll 1") for (int k = T.tid; k < Sn * MC; k += TPI) { g_up[k] = I.up[k]; g_down[k] = I.down[k]; }
+      _Pragma("unroll 1") for (int k = T.tid; k < M; k += TPI) { g_src_down[k] = I.src_down[k]; g_snk_up[k] = I.snk_up[k]; }
+      _Pragma("unroll 1") for (int k = T.tid; k < Sn; k += TPI) { g_kacc[k] = I.kacc[k]; g_deny[k] = I.deny[k]; }
     }
     if (T.tid == 0) {
       if (o.rounds_run) o.rounds_run[b] = r;
