@@ -216,7 +216,7 @@ __device__ void compute_costs(TT& T, const Inst& I) {
   constexpr int TPI = TT::kTPI;
   const int per = I.n * I.MC;
   for (int s = I.S - 1; s >= 0; --s) {
-    for (int t = T.tid; t < per; t += TPI) {
+    _Pragma("unroll 1") for (int t = T.tid; t < per; t += TPI) {
       const int i = I.dmc.div(t), j = t - i * I.MC, v = s * I.n + i, p = v * I.MC + j;
       int64_t c = INF;
       if (j < I.capv[v]) {
@@ -339,7 +339,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     I.summ = (uint32_t*)(base + Lr.summ);
     const int M = I.M;
     const int32_t* cap_g = P.cap + (size_t)b * Sn;
-    for (int k = T.tid; k < Sn; k += TPI) I.capv[k] = I.alive[k] ? cap_g[k] : 0;
+    _Pragma("unroll 1") for (int k = T.tid; k < Sn; k += TPI) I.capv[k] = I.alive[k] ? cap_g[k] : 0;
     int32_t* g_up = I.up;
     int32_t* g_down = I.down;
     int32_t* g_src_down = I.src_down;
@@ -378,7 +378,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       }
     }
 
-    for (int k = T.tid; k < nres; k += TPI) st_res<kSmem>(&I.res[k], RES_NONE);
+    _Pragma("unroll 1") for (int k = T.tid; k < nres; k += TPI) st_res<kSmem>(&I.res[k], RES_NONE);
     int quiet = 0;  // quiet = 0 at the start of every call (DESIGN.md 2.3 R7)
     const int cost_mode = P.rounds_cost_mode;
     uint64_t round = (uint64_t)P.round[b];
@@ -396,15 +396,15 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       // ---------- R0a candidates: a relay holding an IN and an OUT slot ----------
       if (T.tid == 0) { sh_i32[0] = INT_MAX; sh_i32[1] = 0; }
       int cand = 0;
-      for (int v = T.tid; v < Sn; v += TPI) {
+      _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
         const uint32_t w = I.summarize(v);
         cand |= (w & 63u) != 63u && ((w >> 18) & 1u);
       }
       if (T.sync_or(cand)) {
         // ---------- R0a self-pairing, costs of the round-start state ----------
-        for (int v = T.tid; v < Sn; v += TPI) I.relay_costs(v);
+        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.relay_costs(v);
         T.sync();
-        for (int v = T.tid; v < Sn; v += TPI) {
+        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
           const Summ sm{I.summarize(v)};
           if (!sm.has_in() || !sm.has_out()) continue;
           const int x = v * MC + sm.first_in();
@@ -424,17 +424,17 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       // ---------- R0 cost to sink + advertisements; data-node slots ----------
       if (cost_mode == 0) {  // stage-synchronous back-to-front recursion, then advertisements
         compute_costs<TT>(T, I);
-        for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
+        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
       } else if (cost_mode == 1) {  // one chain walk per slot, then advertisements
-        for (int t = T.tid; t < Sn * MC; t += TPI) I.slot_cost(t);
+        _Pragma("unroll 1") for (int t = T.tid; t < Sn * MC; t += TPI) I.slot_cost(t);
         T.sync();
-        for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
+        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
       } else {  // one chain walk per relay (fused advertisement)
-        for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_costs(v);
+        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_costs(v);
       }
       {
         int fs = INT_MAX, anyfree = 0;
-        for (int k = T.tid; k < M; k += TPI) {
+        _Pragma("unroll 1") for (int k = T.tid; k < M; k += TPI) {
           if (I.src_down[k] == kNone && k < fs) fs = k;
           anyfree |= I.snk_up[k] == kNone;
         }
@@ -445,12 +445,12 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       const int d_rslot = *(volatile int*)&sh_i32[0];
       const int dsink_free = *(volatile int*)&sh_i32[1];
       // ---------- R1 requests (one per node) ----------
-      for (int rr = T.tid; rr <= Sn; rr += TPI) {
+      _Pragma("unroll 1") for (int rr = T.tid; rr <= Sn; rr += TPI) {
         int32_t rs = kNone, tg = -2;
         if (rr == Sn) {  // the data node requests for its lowest unpaired SRC slot
           if (d_rslot != INT_MAX) {
             int64_t bc = INF;
-            for (int j = 0; j < n; ++j) {
+            _Pragma("unroll 1") for (int j = 0; j < n; ++j) {
               const int64_t dj = cst(I.src[j]), aj = I.adv_cost[j];
               if (dj == INF || aj == INF || !I.alive[j]) continue;
               if (dj + aj < bc) { bc = dj + aj; tg = j; }
@@ -470,7 +470,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
               int64_t bc = INF;
               const int32_t* col = I.tile + (size_t)s * n * I.ld + i;  // C[s][v][i], v = 0..n-1
               const int64_t* av = I.adv_cost + (s + 1) * n;
-              for (int jj = 0; jj < n; ++jj) {
+              _Pragma("unroll 1") for (int jj = 0; jj < n; ++jj) {
                 const int64_t aj = av[jj];
                 if (aj == INF) continue;  // dead relays advertise INF
                 const int32_t c = col[(size_t)jj * I.ld];
@@ -489,10 +489,10 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       // (a target's eligibility only reads its own OUT slots, which only it modifies; requester
       // slots are IN/FREE slots written by exactly one target, so the fused commit equals
       // "all grants on the pre-R3 state, then all commits")
-      for (int j = T.tid; j <= Sn; j += TPI) {
+      _Pragma("unroll 1") for (int j = T.tid; j <= Sn; j += TPI) {
         if (j == Sn) {  // D-sink: free SNK slots in index order to last-stage requesters in gid order
           int k = 0;
-          for (int q = (S - 1) * n; q < Sn; ++q) {
+          _Pragma("unroll 1") for (int q = (S - 1) * n; q < Sn; ++q) {
             if (I.req_target[q] != -1) continue;
             while (k < M && I.snk_up[k] != kNone) ++k;
             if (k >= M) break;
@@ -528,7 +528,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
             }
           }
         } else {
-          for (int q = (s - 1) * n; q < s * n; ++q) {
+          _Pragma("unroll 1") for (int q = (s - 1) * n; q < s * n; ++q) {
             if (I.req_target[q] != j) continue;
             const int p = next_slot();
             if (p < 0) break;
@@ -543,7 +543,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       T.sync();
       }  // !prev_quiet
       // ---------- R4 proposals by idle relays (post-R3 state) + R5 reservations ----------
-      for (int p = T.tid; p < Sn; p += TPI) {
+      _Pragma("unroll 1") for (int p = T.tid; p < Sn; p += TPI) {
         int kind = K_NONE;
         int32_t x = kNone, y = kNone, z = kNone;
         int32_t t0 = -1, t1 = -1, t2 = -1, t3 = -1;
@@ -627,12 +627,12 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       }
       T.sync();
       // ---------- R6 commit the proposals that hold every slot they touch ----------
-      for (int p = T.tid; p < Sn; p += TPI) {
+      _Pragma("unroll 1") for (int p = T.tid; p < Sn; p += TPI) {
         const int kind = I.prop[p * 4 + 0];
         if (kind == K_NONE) continue;
         const uint64_t key = I.pkey[p];
         bool win = true;
-        for (int q = 0; q < 4; ++q) {
+        _Pragma("unroll 1") for (int q = 0; q < 4; ++q) {
           const int32_t t = I.ptouch[p * 4 + q];
           if (t >= 0) win = win && ld_res<kSmem>(&I.res[t]) == key;
         }
@@ -663,9 +663,9 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         changed = 1;
       }
       T.sync();
-      for (int p = T.tid; p < Sn; p += TPI) {  // release the reservations for the next round
+      _Pragma("unroll 1") for (int p = T.tid; p < Sn; p += TPI) {  // release the reservations for the next round
         if (I.prop[p * 4 + 0] == K_NONE) continue;
-        for (int q = 0; q < 4; ++q) {
+        _Pragma("unroll 1") for (int q = 0; q < 4; ++q) {
           const int32_t t = I.ptouch[p * 4 + q];
           if (t >= 0) st_res<kSmem>(&I.res[t], RES_NONE);
         }
@@ -680,7 +680,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         T.sync();
         uint64_t acc = 0;
         const int nslot = Sn * MC;
-        for (int p = T.tid; p < nslot; p += TPI) {
+        _Pragma("unroll 1") for (int p = T.tid; p < nslot; p += TPI) {
           const int32_t u = I.up[p], dn = I.down[p];
           const uint64_t eu = u == kNone ? 0 : (u >= 0 ? 1 + (uint64_t)u : (1ull << 40) + (uint64_t)(-2 - u));
           const uint64_t ed = dn == kNone ? 0 : (dn >= 0 ? 1 + (uint64_t)dn : (1ull << 41) + (uint64_t)(-2 - dn));
@@ -688,12 +688,12 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           acc += digest_elem(3ull * p, state) + digest_elem(3ull * p + 1, eu) + digest_elem(3ull * p + 2, ed);
         }
         const uint64_t b1 = 3ull * nslot, b2 = b1 + M, b3 = b2 + M, b4 = b3 + 2ull * Sn;
-        for (int k = T.tid; k < M; k += TPI) {
+        _Pragma("unroll 1") for (int k = T.tid; k < M; k += TPI) {
           const int32_t sd = I.src_down[k], su = I.snk_up[k];
           acc += digest_elem(b1 + k, sd == kNone ? 0 : 1 + (uint64_t)sd);
           acc += digest_elem(b2 + k, su == kNone ? 0 : 1 + (uint64_t)su);
         }
-        for (int v = T.tid; v < Sn; v += TPI) {
+        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
           acc += digest_elem(b3 + 2ull * v, (uint64_t)(uint32_t)I.kacc[v]);
           acc += digest_elem(b3 + 2ull * v + 1, (uint64_t)(uint32_t)I.deny[v]);
         }
@@ -707,13 +707,13 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       if (quiet >= P.W) break;
     }
     if (o.digests)
-      for (int k = r + T.tid; k < o.max_rounds; k += TPI) o.digests[(size_t)b * o.max_rounds + k] = 0;
+      _Pragma("unroll 1") for (int k = r + T.tid; k < o.max_rounds; k += TPI) o.digests[(size_t)b * o.max_rounds + k] = 0;
     // ---------- results: complete SRC -> SNK chains and dangling outflows ----------
     if (T.tid == 0) { sh_u64[0] = 0; sh_u64[1] = 0; sh_i32[3] = 0; }
     T.sync();
     {
       unsigned long long f = 0, c = 0;
-      for (int k = T.tid; k < M; k += TPI) {
+      _Pragma("unroll 1") for (int k = T.tid; k < M; k += TPI) {
         int32_t p = I.src_down[k];
         if (p == kNone) continue;
         int64_t cc = cst(I.src[I.relay(p)]);
@@ -728,7 +728,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         if (ok && p <= -2 && cc != INF) { f += 1; c += (unsigned long long)cc; }
       }
       int dg = 0;
-      for (int p = T.tid; p < Sn * MC; p += TPI) dg += I.st(p) == ST_OUT;
+      _Pragma("unroll 1") for (int p = T.tid; p < Sn * MC; p += TPI) dg += I.st(p) == ST_OUT;
       for (int off = 16; off > 0; off >>= 1) {
         f += __shfl_xor_sync(0xffffffffu, f, off);
         c += __shfl_xor_sync(0xffffffffu, c, off);
