@@ -45,6 +45,7 @@ def lib():
         L.orc_ssp.argtypes = [IP, P, P, P, P, P, P, P, P]
         L.orc_ssp_batch.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [P] * 6 + [P, P, P, ctypes.c_int32]
         L.orc_network_simplex.argtypes = [IP, P, P]
+        L.orc_warm_reroute.argtypes = [IP, P, P, P, P, IP] + [P] * 7
         L.orc_certify.argtypes = [IP, ctypes.c_int64, ctypes.c_int64, P, P, P, P]
         L.orc_anneal_table.argtypes = [ctypes.c_double, ctypes.c_double, P, P, P, ctypes.c_int64]
         L.orc_rounds_create.restype = P
@@ -180,6 +181,28 @@ def network_simplex(I: Instance):
     if rc != 0:
         raise RuntimeError(f"network simplex failed rc={rc}")
     return F.value, cost.value
+
+
+def warm_reroute(I_old: Instance, base: SSPResult, I_new: Instance):
+    """Warm-start rerouting after churn: keep the
+    pre-churn assignment `base` of I_old, strip what I_new cannot carry, cancel negative
+    residual cycles, resume SSP.  -> (SSPResult with the new assignment, stats dict)."""
+    F = ctypes.c_int64()
+    cost = ctypes.c_int64()
+    st = np.zeros(3, np.int64)
+    nf = np.zeros((I_new.S, I_new.n), np.int32)
+    sf = np.zeros(I_new.n, np.int32)
+    kf = np.zeros(I_new.n, np.int32)
+    af = np.zeros((max(I_new.S - 1, 0), I_new.n, I_new.n), np.int32)
+    arrs = [np.ascontiguousarray(a, np.int32) for a in (base.node_flow, base.src_flow, base.snk_flow, base.arc_flow)]
+    co, cn = I_old.c(), I_new.c()
+    rc = lib().orc_warm_reroute(ctypes.byref(co), *[_ptr(a) if a.size else None for a in arrs], ctypes.byref(cn),
+                                ctypes.byref(F), ctypes.byref(cost), _ptr(st), _ptr(nf), _ptr(sf), _ptr(kf),
+                                _ptr(af) if af.size else None)
+    if rc != 0:
+        raise RuntimeError(f"oracle warm reroute failed rc={rc}")
+    r = SSPResult(F.value, cost.value, int(st[2]), nf, sf, kf, af)
+    return r, {"stripped": int(st[0]), "cycles": int(st[1]), "augment": int(st[2])}
 
 
 def certify(I: Instance, F, cost, node_flow, src_flow, snk_flow, arc_flow) -> int:

@@ -918,6 +918,175 @@ orc_instance view(int64_t b, int32_t S, int32_t n, int32_t max_cap, const int32_
   return I;
 }
 
+// ---------------------------------------------------------------------------
+// Warm-start rerouting after churn ("reroute",
+// :274-288 crash handling).  Textbook steps, in order:
+//   1. keep the pre-churn flow; strip every unit that crosses a crashed relay,
+//      a relay over its new capacity, or a link/src/snk whose new cost is ABSENT
+//      (one unit path at a time, lowest-index predecessor / successor first);
+//   2. cancel negative residual cycles (Klein): Bellman-Ford from a virtual root,
+//      a relaxation in pass N proves a cycle, walk the predecessors into it and
+//      push its bottleneck; repeat until none;
+//   3. resume successive shortest paths (Bellman-Ford on the residual graph,
+//      which has no negative cycle after 2) until F = M or t* is unreachable.
+// Explicit arc list; shares nothing with ssp() above, so it can pin it.
+// ---------------------------------------------------------------------------
+struct WArc { int from, to; int64_t cap, cost, x; };
+
+struct WarmGraph {
+  int S, n, N;
+  std::vector<WArc> A;
+  int sstar() const { return 0; }
+  int tstar() const { return 1; }
+  int in(int s, int i) const { return 2 + 2 * (s * n + i); }
+  int out(int s, int i) const { return 3 + 2 * (s * n + i); }
+  std::vector<int> src_arc, snk_arc, node_arc, link_arc;  // -1 = absent
+  explicit WarmGraph(const Inst& I) : S(I.S), n(I.n), N(2 + 2 * I.S * I.n) {
+    const int64_t U = I.M;  // no path carries more than the supply
+    src_arc.assign(n, -1); snk_arc.assign(n, -1); node_arc.assign((size_t)S * n, -1);
+    link_arc.assign(S > 1 ? (size_t)(S - 1) * n * n : 0, -1);
+    for (int i = 0; i < n; ++i)
+      if (I.src[i] != ABSENT) { src_arc[i] = (int)A.size(); A.push_back({sstar(), in(0, i), U, I.src[i], 0}); }
+    for (int s = 0; s < S; ++s)
+      for (int i = 0; i < n; ++i) {
+        node_arc[(size_t)s * n + i] = (int)A.size();
+        A.push_back({in(s, i), out(s, i), I.capE(s, i), 0, 0});
+      }
+    for (int s = 0; s + 1 < S; ++s)
+      for (int v = 0; v < n; ++v)
+        for (int u = 0; u < n; ++u)
+          if (I.C(s, v, u) != ABSENT) {
+            link_arc[((size_t)s * n + v) * n + u] = (int)A.size();
+            A.push_back({out(s, u), in(s + 1, v), U, I.C(s, v, u), 0});
+          }
+    for (int i = 0; i < n; ++i)
+      if (I.snk[i] != ABSENT) { snk_arc[i] = (int)A.size(); A.push_back({out(S - 1, i), tstar(), U, I.snk[i], 0}); }
+  }
+  // residual arc r: r = 2e forward (cap - x, +cost), r = 2e+1 backward (x, -cost)
+  int64_t rcap(int r) const { const WArc& a = A[r >> 1]; return (r & 1) ? a.x : a.cap - a.x; }
+  int64_t rcost(int r) const { return (r & 1) ? -A[r >> 1].cost : A[r >> 1].cost; }
+  int rfrom(int r) const { return (r & 1) ? A[r >> 1].to : A[r >> 1].from; }
+  int rto(int r) const { return (r & 1) ? A[r >> 1].from : A[r >> 1].to; }
+  void push(int r, int64_t d) { if (r & 1) A[r >> 1].x -= d; else A[r >> 1].x += d; }
+};
+
+// Step 1 helper: remove one unit along a path through arc e (upstream then downstream).
+// Every arc strictly inside the layered graph has an upstream/downstream path with flow
+// because the pre-churn flow is conserved.
+void warm_strip_unit(WarmGraph& G, int e) {
+  std::vector<int> path{e};
+  for (int node = G.A[e].from; node != G.sstar();) {  // upstream: lowest-index arc into node with flow
+    int pick = -1;
+    for (int k = 0; k < (int)G.A.size() && pick < 0; ++k)
+      if (G.A[k].to == node && G.A[k].x > 0) pick = k;
+    path.push_back(pick);
+    node = G.A[pick].from;
+  }
+  for (int node = G.A[e].to; node != G.tstar();) {  // downstream: lowest-index arc out of node with flow
+    int pick = -1;
+    for (int k = 0; k < (int)G.A.size() && pick < 0; ++k)
+      if (G.A[k].from == node && G.A[k].x > 0) pick = k;
+    path.push_back(pick);
+    node = G.A[pick].to;
+  }
+  for (int k : path) G.A[k].x -= 1;
+}
+
+struct WarmStats { int64_t stripped = 0, cycles = 0, augment = 0; };
+
+int warm_reroute(const Inst& Iold, const Flow& fold, const Inst& Inew, Flow& out, WarmStats& st) {
+  const int S = Inew.S, n = Inew.n;
+  WarmGraph G(Inew);
+  // Step 1: carry the old flow over.  Arcs that vanished (ABSENT) or relays with less
+  // capacity keep their old flow first on a temporary arc so that it can be stripped.
+  const size_t nbase = G.A.size();
+  auto carry = [&](int e_new, int64_t x, int from, int to, int64_t cost_old) -> int {
+    if (x == 0) return 0;
+    if (e_new < 0) {  // vanished arc: a temporary zero-capacity copy holding the old flow
+      G.A.push_back({from, to, 0, cost_old, x});
+      return 0;
+    }
+    G.A[e_new].x = x;
+    return 0;
+  };
+  for (int i = 0; i < n; ++i) {
+    carry(G.src_arc[i], fold.src_f[i], G.sstar(), G.in(0, i), Iold.src[i]);
+    carry(G.snk_arc[i], fold.snk_f[i], G.out(S - 1, i), G.tstar(), Iold.snk[i]);
+  }
+  for (int s = 0; s < S; ++s)
+    for (int i = 0; i < n; ++i) carry(G.node_arc[(size_t)s * n + i], fold.g[(size_t)s * n + i], G.in(s, i), G.out(s, i), 0);
+  for (int s = 0; s + 1 < S; ++s)
+    for (int v = 0; v < n; ++v)
+      for (int u = 0; u < n; ++u)
+        carry(G.link_arc[((size_t)s * n + v) * n + u], fold.fc(Iold, s, u, v), G.out(s, u), G.in(s + 1, v), Iold.C(s, v, u));
+  for (int e = 0; e < (int)G.A.size(); ++e)
+    while (G.A[e].x > G.A[e].cap) { warm_strip_unit(G, e); ++st.stripped; }
+  for (size_t e = nbase; e < G.A.size(); ++e)
+    if (G.A[e].x != 0) return -31;
+  G.A.resize(nbase);  // the temporary arcs are empty now
+  const int N = G.N, R = 2 * (int)G.A.size();
+  // Step 2: negative-cycle cancelling
+  for (;;) {
+    std::vector<int64_t> d(N, 0);
+    std::vector<int> pred(N, -1);
+    int last = -1;
+    for (int pass = 0; pass < N; ++pass) {
+      last = -1;
+      for (int r = 0; r < R; ++r)
+        if (G.rcap(r) > 0 && d[G.rfrom(r)] + G.rcost(r) < d[G.rto(r)]) {
+          d[G.rto(r)] = d[G.rfrom(r)] + G.rcost(r);
+          pred[G.rto(r)] = r;
+          last = G.rto(r);
+        }
+      if (last < 0) break;
+    }
+    if (last < 0) break;
+    int x = last;
+    for (int k = 0; k < N; ++k) x = G.rfrom(pred[x]);  // now on the cycle
+    std::vector<int> cyc;
+    int y = x;
+    do { cyc.push_back(pred[y]); y = G.rfrom(pred[y]); } while (y != x);
+    int64_t b = INF;
+    for (int r : cyc) b = std::min(b, G.rcap(r));
+    for (int r : cyc) G.push(r, b);
+    ++st.cycles;
+  }
+  // Step 3: successive shortest paths from the cancelled flow
+  int64_t F = 0;
+  for (int i = 0; i < n; ++i) if (G.src_arc[i] >= 0) F += G.A[G.src_arc[i]].x;
+  while (F < Inew.M) {
+    std::vector<int64_t> d(N, INF);
+    std::vector<int> pred(N, -1);
+    d[G.sstar()] = 0;
+    for (int pass = 0; pass < N; ++pass) {
+      bool ch = false;
+      for (int r = 0; r < R; ++r)
+        if (G.rcap(r) > 0 && d[G.rfrom(r)] != INF && d[G.rfrom(r)] + G.rcost(r) < d[G.rto(r)]) {
+          d[G.rto(r)] = d[G.rfrom(r)] + G.rcost(r);
+          pred[G.rto(r)] = r;
+          ch = true;
+        }
+      if (!ch) break;
+    }
+    if (d[G.tstar()] == INF) break;
+    int64_t b = Inew.M - F;
+    for (int v = G.tstar(); v != G.sstar(); v = G.rfrom(pred[v])) b = std::min(b, G.rcap(pred[v]));
+    for (int v = G.tstar(); v != G.sstar(); v = G.rfrom(pred[v])) G.push(pred[v], b);
+    F += b;
+    ++st.augment;
+  }
+  // assignment out
+  out.F = F; out.cost = 0; out.A = (int32_t)st.augment;
+  for (const WArc& a : G.A) out.cost += a.x * a.cost;
+  for (int i = 0; i < n; ++i) {
+    out.src_f[i] = G.src_arc[i] >= 0 ? (int32_t)G.A[G.src_arc[i]].x : 0;
+    out.snk_f[i] = G.snk_arc[i] >= 0 ? (int32_t)G.A[G.snk_arc[i]].x : 0;
+  }
+  for (int k = 0; k < S * n; ++k) out.g[k] = (int32_t)G.A[G.node_arc[k]].x;
+  for (size_t k = 0; k < G.link_arc.size(); ++k) out.arc[k] = G.link_arc[k] >= 0 ? (int32_t)G.A[G.link_arc[k]].x : 0;
+  return 0;
+}
+
 }  // namespace
 
 struct orc_rounds { Rounds R; };
@@ -986,6 +1155,30 @@ int orc_ssp_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const int32_
     F[b] = fl.F; cost[b] = fl.cost; A[b] = fl.A;
   });
   return err.load() ? -1 : 0;
+}
+
+int orc_warm_reroute(const orc_instance* Iold_v, const int32_t* node_flow, const int32_t* src_flow,
+                     const int32_t* snk_flow, const int32_t* arc_flow, const orc_instance* Inew_v, int64_t* F,
+                     int64_t* cost, int64_t* stats, int32_t* node_flow_out, int32_t* src_flow_out,
+                     int32_t* snk_flow_out, int32_t* arc_flow_out) {
+  Inst Io(Iold_v), In(Inew_v);
+  if (Io.S != In.S || Io.n != In.n) return -30;
+  Flow fo(Io), fn(In);
+  std::copy(node_flow, node_flow + fo.g.size(), fo.g.begin());
+  std::copy(src_flow, src_flow + Io.n, fo.src_f.begin());
+  std::copy(snk_flow, snk_flow + Io.n, fo.snk_f.begin());
+  if (arc_flow) std::copy(arc_flow, arc_flow + fo.arc.size(), fo.arc.begin());
+  WarmStats st;
+  const int rc = warm_reroute(Io, fo, In, fn, st);
+  if (rc) return rc;
+  if (F) *F = fn.F;
+  if (cost) *cost = fn.cost;
+  if (stats) { stats[0] = st.stripped; stats[1] = st.cycles; stats[2] = st.augment; }
+  if (node_flow_out) std::copy(fn.g.begin(), fn.g.end(), node_flow_out);
+  if (src_flow_out) std::copy(fn.src_f.begin(), fn.src_f.end(), src_flow_out);
+  if (snk_flow_out) std::copy(fn.snk_f.begin(), fn.snk_f.end(), snk_flow_out);
+  if (arc_flow_out) std::copy(fn.arc.begin(), fn.arc.end(), arc_flow_out);
+  return 0;
 }
 
 int orc_network_simplex(const orc_instance* Iv, int64_t* F, int64_t* cost) {

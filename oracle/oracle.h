@@ -51,6 +51,16 @@ int orc_ssp_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const int32_
                   const uint8_t* alive, const int32_t* src, const int32_t* snk, const int32_t* link,
                   const int64_t* supply, int64_t* F, int64_t* cost, int32_t* A, int32_t threads);
 
+/* Warm-start rerouting after churn:
+ * keep the pre-churn assignment of Iold (node/src/snk/arc flows, layouts as orc_ssp), strip
+ * the units the churned instance Inew cannot carry, cancel negative residual cycles, resume
+ * SSP.  (F, cost) equal orc_ssp(Inew)'s; the assignment may differ (several optima).
+ * stats[3] = {units stripped, cycles cancelled, augmentations}.  Outputs may be NULL. */
+int orc_warm_reroute(const orc_instance* Iold, const int32_t* node_flow, const int32_t* src_flow,
+                     const int32_t* snk_flow, const int32_t* arc_flow, const orc_instance* Inew, int64_t* F,
+                     int64_t* cost, int64_t* stats, int32_t* node_flow_out, int32_t* src_flow_out,
+                     int32_t* snk_flow_out, int32_t* arc_flow_out);
+
 /* Independent cross-check: primal network simplex with strongly feasible
  * spanning trees (Cunningham) on the node-split graph plus a bypass arc. */
 int orc_network_simplex(const orc_instance* I, int64_t* F, int64_t* cost);
