@@ -246,6 +246,63 @@ def other_configs(dev, steps=5, warmup=3):
     return out
 
 
+def warm_reroute(dev, names=("gpt", "llama"), steps=5, warmup=3):
+    """warm-start rerouting (gwtf_flow_warm_reroute) after the config's churn event,
+    from the pre-churn optimum, against the cold exact solve of the same churned graph (device events,
+    L2 flushed, restore and the assignment copy untimed).  (F, cost) must agree on every instance."""
+    import torch
+
+    from paper_2509_21221_b200 import Flow
+    from tests import harness
+    out = {}
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for name in names:
+        cfg = gen.CONFIGS[name]
+        B = cfg.B
+        bt, src, snk, link = harness.device_inputs(cfg, 0, B, device=dev)
+        fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0)
+        fl.solve_batch()
+        base = [t.clone() for t in fl.get_assignment()]
+        if cfg.churn == "random":
+            an, upd = harness.churn_inputs(cfg, 0, bt.alive, device=dev)
+        else:  # victim churn needs the round state: run the base rounds first
+            fl.decentralized_rounds(cfg.max_rounds)
+            st = fl.export_round_state()
+            an = torch.from_numpy(gen.llama_victims(st["up"].cpu().numpy(), st["down"].cpu().numpy(),
+                                                    bt.alive.cpu().numpy(), gen.victim_draws(cfg, 0, B))).to(dev)
+            upd = None
+        fl.snapshot()
+        work = [t.clone() for t in base]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        tw = tc = 0.0
+        for it in range(warmup + steps):
+            fl.restore()
+            fl.apply_churn(an, upd)
+            for w, b0 in zip(work, base):
+                w.copy_(b0)
+            flush.random_(0, 255)
+            torch.cuda.synchronize()
+            ev[0].record(fl.stream)
+            F, C, S, Q = fl.warm_reroute(*work)
+            ev[1].record(fl.stream)
+            flush.random_(0, 255)
+            ev[2].record(fl.stream)
+            cold = fl.solve_batch()
+            ev[3].record(fl.stream)
+            torch.cuda.synchronize()
+            if it >= warmup:
+                tw += ev[0].elapsed_time(ev[1])
+                tc += ev[2].elapsed_time(ev[3])
+        out[name] = {"workload": workload_name(cfg), "instances": B, "warm_ms": tw / steps, "cold_ms": tc / steps,
+                     "warm_instances_per_s": B * steps / (tw / 1e3), "cold_instances_per_s": B * steps / (tc / 1e3),
+                     "F_cost_mismatches": int(((F != cold.flow_value) | (C != cold.total_cost)).sum()),
+                     "status_nonzero": int((Q != 0).sum()), "stripped": int(S[:, 0].sum()),
+                     "cycles": int(S[:, 1].sum()), "augmentations": int(S[:, 2].sum()),
+                     "cold_augmentations": int(cold.augmentations.sum())}
+        fl.close()
+    return out
+
+
 def multi_source(dev, B=8192, reps=1):
     """SURVEY.md 8(f) f2, exact-solve part: flow-test settings 5 and 6 (2 / 4 data nodes),
     single-commodity solves over the residual capacities in round-robin order, one
@@ -514,6 +571,7 @@ def main():
         line["flow_quality"] = flow_quality(dev)
         line["other_configs"] = other_configs(dev)
         line["multi_source"] = multi_source(dev)
+        line["warm_reroute"] = warm_reroute(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -198,6 +198,25 @@ gwtf_status gwtf_flow_kernel_times(gwtf_flow_t h, const char** names, float* ms,
  * microbatches and their total cost.  Does not touch the solver or round state. */
 gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_t* total_cost);
 
+/* Warm-start rerouting after churn ("reroute" after a failure,
+ * PAPER.md:274-288 crash handling), on the handle's current (churned) graph,
+ * starting from a pre-churn assignment instead of zero flow:
+ *   1. strip every unit the graph can no longer carry (crashed relay, relay over capacity,
+ *      link / src / snk now GWTF_ABSENT), one unit path at a time;
+ *   2. cancel negative residual cycles (Bellman-Ford, predecessor walk, bottleneck push);
+ *   3. resume successive shortest paths until F = M or no augmenting path is left.
+ * node_flow [B][S][n], src_flow [B][n], snk_flow [B][n], arc_flow_dense [B][S-1][n_dst][n_src]
+ * (the gwtf_flow_get_assignment layouts, taken before gwtf_flow_apply_churn) are read and
+ * OVERWRITTEN in place with the repaired optimum.  Outputs [B]: max-flow value, min cost (equal
+ * to a cold gwtf_flow_solve_batch's: the optimum's (F, cost) is unique; the assignment may
+ * differ), stats [B][3] = {units stripped, cycles cancelled, augmentations} (may be NULL),
+ * inst_status (0 ok, 1 distance bound 2^38 exceeded, 2/3 no convergence, 4 the given
+ * assignment is not conserved, 5 internal: a non-negative predecessor cycle; may be NULL).  Does not touch the handle's own solver or round
+ * state.  INVALID on NULL required arrays; UNSUPPORTED when 2(2n + Sn + (S-1)n^2) >= 2^24. */
+gwtf_status gwtf_flow_warm_reroute(gwtf_flow_t h, int32_t* node_flow, int32_t* src_flow, int32_t* snk_flow,
+                                   int32_t* arc_flow_dense, int64_t* flow_value, int64_t* total_cost,
+                                   int64_t* stats, int32_t* inst_status);
+
 /* Work counters of the exact solve accumulated since create (host int64 out[cap], cap <= 2048):
  * [0] dense boundary relaxations, [1] backward (reverse-arc) phases, [2] augmentations,
  * [3] Bellman-Ford passes, [4] traced path nodes (cluster tier), [11] frontier relaxations (cluster

@@ -55,6 +55,7 @@ EXPORTS = {
     "gwtf_flow_kernel_times": ([P, ctypes.POINTER(ctypes.c_char_p), P, P, I32, P], I32),
     "gwtf_flow_stats": ([P, P, I32], I32),
     "gwtf_flow_greedy_baseline": ([P, P, P], I32),
+    "gwtf_flow_warm_reroute": ([P, P, P, P, P, P, P, P, P], I32),
     "gwtf_flow_destroy": ([P], I32),
     "gwtf_last_error": ([], ctypes.c_char_p),
     "gwtf_abi_version": ([], I32),

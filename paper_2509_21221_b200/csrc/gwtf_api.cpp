@@ -738,6 +738,44 @@ gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_
   return finish_out(h, maps);
 }
 
+gwtf_status gwtf_flow_warm_reroute(gwtf_flow_t h, int32_t* node_flow, int32_t* src_flow, int32_t* snk_flow,
+                                   int32_t* arc_flow_dense, int64_t* flow_value, int64_t* total_cost, int64_t* stats,
+                                   int32_t* inst_status) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!node_flow || !src_flow || !snk_flow || !flow_value || !total_cost)
+    return fail(GWTF_E_INVALID, "warm_reroute: NULL required array");
+  const Problem& P = h->P;
+  if (P.S > 1 && !arc_flow_dense) return fail(GWTF_E_INVALID, "warm_reroute: NULL arc_flow_dense");
+  const size_t B = P.B, Sn = (size_t)P.S * P.n, A = (size_t)std::max(P.S - 1, 0) * P.n * P.n;
+  if (2 * (2 * (int64_t)P.n + (int64_t)Sn + (int64_t)A) >= (1ll << 24) - 1)
+    return fail(GWTF_E_UNSUPPORTED, "warm_reroute: residual arc ids need more than 24 bits");
+  // in/out flow arrays: device mode works in place; host mode copies in and back out
+  std::vector<OutMap> maps;
+  int32_t* io[4] = {src_flow, node_flow, arc_flow_dense, snk_flow};
+  const size_t cnt[4] = {B * P.n, B * Sn, B * A, B * P.n};
+  int32_t* dev[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int k = 0; k < 4; ++k) {
+    if (!io[k] || cnt[k] == 0) { dev[k] = io[k]; continue; }
+    if ((s = map_out(h, io[k], cnt[k], 18 + k, &dev[k], maps)) != GWTF_OK) return s;
+    if (host_mode(h) && (s = copy_in(h, dev[k], io[k], cnt[k] * 4)) != GWTF_OK) return s;
+  }
+  int64_t *F = nullptr, *C = nullptr, *St = nullptr;
+  int32_t* Q = nullptr;
+  if ((s = map_out(h, flow_value, B, 22, &F, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, total_cost, B, 23, &C, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, stats, 3 * B, 24, &St, maps)) != GWTF_OK) return s;
+  if ((s = map_out(h, inst_status, B, 25, &Q, maps)) != GWTF_OK) return s;
+  void* ws = scratch(h, 26, warm_ws_bytes(P, warm_grid(P)));
+  if (!ws) return fail(GWTF_E_NOMEM, "warm_reroute workspace");
+  Timer t;
+  prof_begin(h, "warm_kernel", &t);
+  CK(h, launch_warm(P, dev[0], dev[1], dev[2], dev[3], ws, F, C, St, Q, h->stream));
+  h->kernel_launches += 1;
+  prof_end(h, &t);
+  return finish_out(h, maps);
+}
+
 gwtf_status gwtf_flow_stats(gwtf_flow_t h, int64_t* out, int32_t cap) {
   gwtf_status s = enter(h);
   if (s != GWTF_OK) return s;

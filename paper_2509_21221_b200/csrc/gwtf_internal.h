@@ -109,6 +109,10 @@ cudaError_t launch_addition_build(int32_t S, int32_t n, const int32_t* cap, cons
                                   int32_t* snk_o, int32_t* link_o, cudaStream_t st);
 cudaError_t launch_addition_select(int64_t count, const int64_t* F, const int64_t* cost, int64_t* best, cudaStream_t st);
 cudaError_t launch_greedy(const Problem& P, int32_t* rem, int64_t* F, int64_t* cost, cudaStream_t st);
+size_t warm_ws_bytes(const Problem& P, int grid);
+int warm_grid(const Problem& P);
+cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* arc, int32_t* snk_f, void* ws,
+                        int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, cudaStream_t st);
 cudaError_t launch_scan_costs(const int32_t* v, int64_t count, int32_t* out_max, int32_t* out_min,
                               cudaStream_t st);
 

@@ -1,0 +1,316 @@
+// Warm-start rerouting after churn (PAPER.md:188 reroute after a failure,
+// :274-288 crash handling).  Starting from a pre-churn assignment (dense layouts of
+// gwtf_flow_get_assignment), on the handle's current (churned) graph:
+//   1. strip the units the churned graph cannot carry (dead relay, relay over capacity, link /
+//      src / snk arc now ABSENT), one unit path at a time;
+//   2. cancel negative residual cycles: Bellman-Ford from a virtual root, a change in pass N
+//      proves a cycle, the predecessor walk extracts it and its bottleneck is pushed;
+//   3. resume successive shortest paths (Bellman-Ford from s*, signed costs) until F = M or t*
+//      is unreachable.
+// One CTA per instance (grid-stride over the batch).  A pass relaxes every residual arc of the
+// node-split stage graph in parallel; a node's label is one 64-bit word, biased distance << 24 |
+// residual-arc id, lowered with atomicMin, so a label and its predecessor are always consistent
+// (every cycle of the predecessor graph is then negative).  Labels live in a per-instance global
+// scratch row (L1/L2 resident for the shapes this serves).  The flow arrays are updated in place.
+//
+// Arc numbering (forward arc e; residual arc r = 2e forward, 2e+1 backward):
+//   e in [0, n)                      src arc     D -> in(0,i)         cap M, cost src[i]
+//   e in [n, n+Sn)                   relay arc   in(s,i) -> out(s,i)  cap alive ? cap : 0, cost 0
+//   e in [n+Sn, n+Sn+(S-1)n^2)       link arc    out(s,u) -> in(s+1,v) (dest-major s,v,u), cap M
+//   e in [n+Sn+(S-1)n^2, E)          snk arc     out(S-1,i) -> D      cap M, cost snk[i]
+// Nodes: 0 = s*, 1 = t*, in(s,i) = 2 + 2(s n + i), out(s,i) = in(s,i) + 1.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gwtf_internal.h"
+
+namespace gwtf {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kArcBits = 24;
+constexpr uint64_t kNoPred = (1ull << kArcBits) - 1;
+constexpr int64_t kBias = 1ll << 38;  // |distance| < 2^38 (checked per relaxation)
+constexpr uint64_t kLabInf = ~0ull;
+
+struct WarmCtx {
+  int S, n, ld, N;
+  int64_t E, M;
+  const int32_t* tile;   // [S-1][n][ld]
+  const int32_t* src;
+  const int32_t* snk;
+  const int32_t* cap;
+  const uint8_t* alive;
+  int32_t* src_f;        // [n]
+  int32_t* g;            // [S][n]
+  int32_t* arc;          // [S-1][n][n]
+  int32_t* snk_f;        // [n]
+};
+
+struct ArcV { int from, to; int64_t cap, cost; int32_t* x; };
+
+__device__ __forceinline__ int in_node(const WarmCtx& c, int s, int i) { return 2 + 2 * (s * c.n + i); }
+
+__device__ ArcV arc_of(const WarmCtx& c, int64_t e) {
+  ArcV a;
+  const int n = c.n, Sn = c.S * c.n;
+  if (e < n) {
+    const int32_t w = c.src[e];
+    a = {0, in_node(c, 0, (int)e), w == kAbsent ? 0 : c.M, w == kAbsent ? 0 : (int64_t)w, c.src_f + e};
+  } else if (e < n + Sn) {
+    const int k = (int)(e - n);
+    a = {2 + 2 * k, 3 + 2 * k, c.alive[k] ? (int64_t)c.cap[k] : 0, 0, c.g + k};
+  } else if (e < n + Sn + (int64_t)(c.S - 1) * n * n) {
+    const int k = (int)(e - n - Sn);  // < 2^23 (checked by the host)
+    const int q = k / n, u = k - q * n, s = q / n, v = q - s * n;
+    const int32_t w = c.tile[((size_t)s * n + v) * c.ld + u];
+    a = {in_node(c, s, u) + 1, in_node(c, s + 1, v), w == kAbsent ? 0 : c.M, w == kAbsent ? 0 : (int64_t)w, c.arc + k};
+  } else {
+    const int i = (int)(e - n - Sn - (int64_t)(c.S - 1) * n * n);
+    const int32_t w = c.snk[i];
+    a = {in_node(c, c.S - 1, i) + 1, 1, w == kAbsent ? 0 : c.M, w == kAbsent ? 0 : (int64_t)w, c.snk_f + i};
+  }
+  return a;
+}
+
+// labels are lowered by global atomics (performed at L2): read them around the L1
+__device__ __forceinline__ uint64_t ld_lab(const uint64_t* p) { return *(const volatile uint64_t*)p; }
+__device__ __forceinline__ int64_t lab_dist(uint64_t L) { return (int64_t)(L >> kArcBits) - kBias; }
+__device__ __forceinline__ int lab_pred(uint64_t L) { return (int)(L & kNoPred); }
+__device__ __forceinline__ uint64_t lab(int64_t d, uint64_t r) { return ((uint64_t)(d + kBias) << kArcBits) | r; }
+
+// residual arc r -> (from, to, rcap, rcost, x, sign)
+__device__ __forceinline__ void res_of(const WarmCtx& c, int64_t r, int& from, int& to, int64_t& rcap, int64_t& rcost,
+                                       int32_t*& x, int& sign) {
+  const ArcV a = arc_of(c, r >> 1);
+  x = a.x;
+  if (r & 1) { from = a.to; to = a.from; rcap = *a.x; rcost = -a.cost; sign = -1; }
+  else { from = a.from; to = a.to; rcap = a.cap - *a.x; rcost = a.cost; sign = 1; }
+}
+
+// One team-wide Bellman-Ford pass over every residual arc.  Returns (block-uniform) whether
+// some label changed; *last = a node lowered in this pass.
+__device__ bool bf_pass(const WarmCtx& c, uint64_t* labv, int* last, int* changed_sm, int* bad_sm) {
+  if (threadIdx.x == 0) *changed_sm = 0;
+  __syncthreads();
+  int ch = 0;
+  for (int64_t r = threadIdx.x; r < 2 * c.E; r += blockDim.x) {
+    int from, to, sign;
+    int64_t rcap, rcost;
+    int32_t* x;
+    res_of(c, r, from, to, rcap, rcost, x, sign);
+    if (rcap <= 0) continue;
+    const uint64_t Lf = ld_lab(&labv[from]);
+    if (Lf == kLabInf) continue;
+    const int64_t d = lab_dist(Lf) + rcost;
+    if (d >= kBias || d <= -kBias) { *bad_sm = 1; continue; }
+    const uint64_t cand = lab(d, (uint64_t)r);
+    if ((cand >> kArcBits) < (ld_lab(&labv[to]) >> kArcBits)) {
+      const uint64_t old = atomicMin((unsigned long long*)&labv[to], (unsigned long long)cand);
+      if ((cand >> kArcBits) < (old >> kArcBits)) { ch = 1; *last = to; }
+    }
+  }
+  if (ch) *changed_sm = 1;
+  __syncthreads();
+  const bool any = *changed_sm != 0;
+  __syncthreads();
+  return any;
+}
+
+// thread 0: remove one unit along a flow path through forward arc e (lowest index upstream and
+// downstream).  A conserved flow has a carrying arc on each side of every interior node; false
+// if the given assignment is not conserved.
+__device__ bool strip_unit(const WarmCtx& c, int64_t e) {
+  const int n = c.n, S = c.S;
+  const ArcV a = arc_of(c, e);
+  *a.x -= 1;
+  for (int node = a.from; node != 0;) {  // upstream
+    const int k = (node - 2) >> 1, s = k / n, i = k % n;
+    if (node & 1) { c.g[k] -= 1; node = node - 1; continue; }  // out(s,i) <- relay arc
+    if (s == 0) { c.src_f[i] -= 1; node = 0; continue; }
+    int u = 0;
+    while (u < n && c.arc[((size_t)(s - 1) * n + i) * n + u] <= 0) ++u;
+    if (u == n) return false;
+    c.arc[((size_t)(s - 1) * n + i) * n + u] -= 1;
+    node = in_node(c, s - 1, u) + 1;
+  }
+  for (int node = a.to; node != 1;) {  // downstream
+    const int k = (node - 2) >> 1, s = k / n, i = k % n;
+    if (!(node & 1)) { c.g[k] -= 1; node = node + 1; continue; }  // in(s,i) -> relay arc
+    if (s == S - 1) { c.snk_f[i] -= 1; node = 1; continue; }
+    int v = 0;
+    while (v < n && c.arc[((size_t)s * n + v) * n + i] <= 0) ++v;
+    if (v == n) return false;
+    c.arc[((size_t)s * n + v) * n + i] -= 1;
+    node = in_node(c, s + 1, v);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
+                                                        int32_t* arc_all, int32_t* snk_f_all, uint64_t* lab_all,
+                                                        int32_t* stamp_all, int64_t* F_out, int64_t* cost_out,
+                                                        int64_t* stats_out, int32_t* status_out) {
+  __shared__ int changed_sm, bad_sm, last_sm, cyc_sm;
+  __shared__ unsigned long long cost_sm;
+  const int S = P.S, n = P.n;
+  const int N = 2 + 2 * S * n;
+  const int64_t E = 2ll * n + (int64_t)S * n + (int64_t)(S - 1) * n * n;
+  for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
+    WarmCtx c;
+    c.S = S; c.n = n; c.ld = P.ld; c.N = N; c.E = E; c.M = P.supply[b];
+    c.tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
+    c.src = P.src + (size_t)b * n;
+    c.snk = P.snk + (size_t)b * n;
+    c.cap = P.cap + (size_t)b * S * n;
+    c.alive = P.alive + (size_t)b * S * n;
+    c.src_f = src_f_all + (size_t)b * n;
+    c.g = g_all + (size_t)b * S * n;
+    c.arc = arc_all + (size_t)b * (S - 1) * n * n;
+    c.snk_f = snk_f_all + (size_t)b * n;
+    uint64_t* labv = lab_all + (size_t)blockIdx.x * N;
+    int32_t* stamp = stamp_all + (size_t)blockIdx.x * N;
+    int64_t stripped = 0, cycles = 0, augment = 0;
+    int status = 0;
+    // ---- 1. strip (thread 0; few units) ----
+    if (threadIdx.x == 0) {
+      bad_sm = 0;
+      for (int64_t e = 0; e < E; ++e) {
+        const ArcV a = arc_of(c, e);
+        while (!bad_sm && *a.x > a.cap) {
+          if (!strip_unit(c, e)) bad_sm = 4;
+          ++stripped;
+        }
+      }
+    }
+    for (int k = threadIdx.x; k < N; k += blockDim.x) stamp[k] = -1;
+    __syncthreads();
+    // ---- 2. negative-cycle cancelling ----
+    int walk_id = 0;
+    for (;;) {
+      for (int k = threadIdx.x; k < N; k += blockDim.x) labv[k] = lab(0, kNoPred);
+      __syncthreads();
+      bool cyc = false;
+      for (int pass = 0;; ++pass) {
+        const bool ch = bf_pass(c, labv, &last_sm, &changed_sm, &bad_sm);
+        if (!ch) break;
+        // every cycle of the predecessor graph is negative: look for one after each pass that
+        // changed a label (walk from a lowered node), so a cycle is cancelled as soon as it forms
+        // instead of after the N passes that prove it
+        {
+          if (threadIdx.x == 0) {
+            cyc_sm = -1;
+            ++walk_id;
+            int x = last_sm;
+            while (stamp[x] != walk_id) {
+              stamp[x] = walk_id;
+              const int r = lab_pred(ld_lab(&labv[x]));
+              if (r == (int)kNoPred) { x = -1; break; }
+              int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+              res_of(c, r, from, to, rcap, rcost, xp, sign);
+              x = from;
+            }
+            cyc_sm = x;
+          }
+          __syncthreads();
+          if (cyc_sm >= 0) { cyc = true; break; }
+          if (pass > 4 * N + 8) { if (threadIdx.x == 0) bad_sm = 2; __syncthreads(); break; }
+        }
+      }
+      if (!cyc || bad_sm) break;
+      if (threadIdx.x == 0) {  // push the bottleneck around the cycle through cyc_sm
+        const int x0 = cyc_sm;
+        int64_t bott = INT64_MAX, ccost = 0;
+        int x = x0;
+        do {
+          int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+          res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
+          bott = rcap < bott ? rcap : bott;
+          ccost += rcost;
+          x = from;
+        } while (x != x0);
+        if (ccost >= 0) { bad_sm = 5; bott = 0; }  // cannot happen (see above); never loop on it
+        x = x0;
+        do {
+          int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+          res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
+          *xp += (int32_t)(sign * bott);
+          x = from;
+        } while (x != x0);
+      }
+      ++cycles;
+      __syncthreads();
+      if (bad_sm) break;
+    }
+    // ---- 3. successive shortest paths from the cancelled flow ----
+    int64_t F = 0;
+    for (int i = 0; i < n; ++i) F += c.src_f[i];
+    while (!bad_sm && F < c.M) {
+      for (int k = threadIdx.x; k < N; k += blockDim.x) labv[k] = k == 0 ? lab(0, kNoPred) : kLabInf;
+      __syncthreads();
+      for (int pass = 0; bf_pass(c, labv, &last_sm, &changed_sm, &bad_sm); ++pass)
+        if (pass > N) { if (threadIdx.x == 0) bad_sm = 3; __syncthreads(); break; }
+      if (bad_sm || ld_lab(&labv[1]) == kLabInf) break;
+      if (threadIdx.x == 0) {
+        int64_t bott = c.M - F;
+        for (int x = 1; x != 0;) {
+          int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+          res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
+          bott = rcap < bott ? rcap : bott;
+          x = from;
+        }
+        for (int x = 1; x != 0;) {
+          int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+          res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
+          *xp += (int32_t)(sign * bott);
+          x = from;
+        }
+        changed_sm = (int)(bott > 0x7fffffff ? 0x7fffffff : bott);
+      }
+      __syncthreads();
+      F += changed_sm;
+      ++augment;
+      __syncthreads();
+    }
+    status = bad_sm;
+    // ---- objective of the repaired assignment ----
+    if (threadIdx.x == 0) cost_sm = 0;
+    __syncthreads();
+    long long part = 0;
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      const ArcV a = arc_of(c, e);
+      part += (long long)*a.x * a.cost;
+    }
+    atomicAdd(&cost_sm, (unsigned long long)part);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      F_out[b] = F;
+      cost_out[b] = (int64_t)cost_sm;
+      if (stats_out) { stats_out[3 * b] = stripped; stats_out[3 * b + 1] = cycles; stats_out[3 * b + 2] = augment; }
+      if (status_out) status_out[b] = status;  // 5 = non-negative cycle (never expected)
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+size_t warm_ws_bytes(const Problem& P, int grid) {
+  const size_t N = 2 + 2 * (size_t)P.S * P.n;
+  return (size_t)grid * N * (8 + 4);
+}
+
+int warm_grid(const Problem& P) { return (int)std::min<int64_t>(P.B, 148 * 8); }
+
+cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* arc, int32_t* snk_f, void* ws,
+                        int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, cudaStream_t st) {
+  const int grid = warm_grid(P);
+  const size_t N = 2 + 2 * (size_t)P.S * P.n;
+  uint64_t* labv = (uint64_t*)ws;
+  int32_t* stamp = (int32_t*)(labv + (size_t)grid * N);
+  warm_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, stamp, F, cost, stats, status);
+  return cudaGetLastError();
+}
+
+}  // namespace gwtf

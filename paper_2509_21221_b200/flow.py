@@ -226,6 +226,20 @@ class Flow:
         check("gwtf_flow_greedy_baseline", lib().gwtf_flow_greedy_baseline(self.h, _ptr(F), _ptr(C)))
         return F, C
 
+    def warm_reroute(self, node_flow, src_flow, snk_flow, arc_flow):
+        """Warm-start rerouting on the current (churned) graph from a pre-churn assignment
+        (gwtf_flow_warm_reroute).  The four flow tensors (get_assignment's
+        layouts, on this handle's side: device or host) are overwritten with the repaired optimum.
+        -> (F [B], cost [B], stats [B][3] = stripped / cycles / augmentations, status [B])."""
+        F = self._out((self.B,), torch.int64)
+        C = self._out((self.B,), torch.int64)
+        St = self._out((self.B, 3), torch.int64)
+        Q = self._out((self.B,), torch.int32)
+        af = arc_flow if arc_flow is not None and arc_flow.numel() else None
+        check("gwtf_flow_warm_reroute", lib().gwtf_flow_warm_reroute(
+            self.h, _ptr(node_flow), _ptr(src_flow), _ptr(snk_flow), _ptr(af), _ptr(F), _ptr(C), _ptr(St), _ptr(Q)))
+        return F, C, St, Q
+
     def stats(self, raw: bool = False):
         """Exact-solve work counters since create (gwtf_flow_stats)."""
         import numpy as np
