@@ -187,61 +187,72 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
     for (int k = threadIdx.x; k < N; k += blockDim.x) stamp[k] = -1;
     __syncthreads();
     // ---- 2. negative-cycle cancelling ----
-    int walk_id = 0;
-    for (;;) {
+    // Labels are not reset after a cancel: whatever their history, a pass that lowers nothing
+    // leaves labels that are feasible potentials of the current residual graph, which proves that
+    // no negative cycle is left.  A predecessor cycle found on stale labels is checked (every arc
+    // still residual, negative total) before it is pushed; 2N + 8 passes without a usable cycle
+    // since the last cancel restart the labels from zero (fresh labels: every predecessor cycle is
+    // negative and residual).
+    {
+      int walk_id = 0, since = 0;
+      bool fresh = true;
       for (int k = threadIdx.x; k < N; k += blockDim.x) labv[k] = lab(0, kNoPred);
       __syncthreads();
-      bool cyc = false;
-      for (int pass = 0;; ++pass) {
+      while (!bad_sm) {
         const bool ch = bf_pass(c, labv, &last_sm, &changed_sm, &bad_sm);
         if (!ch) break;
-        // every cycle of the predecessor graph is negative: look for one after each pass that
-        // changed a label (walk from a lowered node), so a cycle is cancelled as soon as it forms
-        // instead of after the N passes that prove it
-        {
-          if (threadIdx.x == 0) {
-            cyc_sm = -1;
-            ++walk_id;
-            int x = last_sm;
-            while (stamp[x] != walk_id) {
-              stamp[x] = walk_id;
-              const int r = lab_pred(ld_lab(&labv[x]));
-              if (r == (int)kNoPred) { x = -1; break; }
-              int from, to, sign; int64_t rcap, rcost; int32_t* xp;
-              res_of(c, r, from, to, rcap, rcost, xp, sign);
-              x = from;
-            }
-            cyc_sm = x;
+        ++since;
+        if (threadIdx.x == 0) {  // walk the predecessors of a lowered node; cancel a usable cycle
+          ++walk_id;
+          int x = last_sm;
+          while (stamp[x] != walk_id) {
+            stamp[x] = walk_id;
+            const int r = lab_pred(ld_lab(&labv[x]));
+            if (r == (int)kNoPred) { x = -1; break; }
+            int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+            res_of(c, r, from, to, rcap, rcost, xp, sign);
+            x = from;
           }
-          __syncthreads();
-          if (cyc_sm >= 0) { cyc = true; break; }
-          if (pass > 4 * N + 8) { if (threadIdx.x == 0) bad_sm = 2; __syncthreads(); break; }
+          cyc_sm = 0;
+          if (x >= 0) {
+            const int x0 = x;
+            int64_t bott = INT64_MAX, ccost = 0;
+            do {
+              int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+              res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
+              bott = rcap < bott ? rcap : bott;
+              ccost += rcost;
+              x = from;
+            } while (x != x0);
+            if (bott > 0 && ccost < 0) {
+              do {
+                int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+                res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
+                *xp += (int32_t)(sign * bott);
+                x = from;
+              } while (x != x0);
+              cyc_sm = 1;
+            } else if (fresh) {
+              bad_sm = 5;  // cannot happen on fresh labels; never loop on it
+            }
+          }
         }
+        __syncthreads();
+        if (cyc_sm) {
+          ++cycles;
+          since = 0;
+          fresh = false;
+        } else if (since > (fresh ? 4 * N + 8 : 2 * N + 8)) {
+          if (fresh) {
+            if (threadIdx.x == 0) bad_sm = 2;
+          } else {
+            for (int k = threadIdx.x; k < N; k += blockDim.x) labv[k] = lab(0, kNoPred);
+            since = 0;
+            fresh = true;
+          }
+        }
+        __syncthreads();
       }
-      if (!cyc || bad_sm) break;
-      if (threadIdx.x == 0) {  // push the bottleneck around the cycle through cyc_sm
-        const int x0 = cyc_sm;
-        int64_t bott = INT64_MAX, ccost = 0;
-        int x = x0;
-        do {
-          int from, to, sign; int64_t rcap, rcost; int32_t* xp;
-          res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
-          bott = rcap < bott ? rcap : bott;
-          ccost += rcost;
-          x = from;
-        } while (x != x0);
-        if (ccost >= 0) { bad_sm = 5; bott = 0; }  // cannot happen (see above); never loop on it
-        x = x0;
-        do {
-          int from, to, sign; int64_t rcap, rcost; int32_t* xp;
-          res_of(c, lab_pred(ld_lab(&labv[x])), from, to, rcap, rcost, xp, sign);
-          *xp += (int32_t)(sign * bott);
-          x = from;
-        } while (x != x0);
-      }
-      ++cycles;
-      __syncthreads();
-      if (bad_sm) break;
     }
     // ---- 3. successive shortest paths from the cancelled flow ----
     int64_t F = 0;
