@@ -29,6 +29,7 @@ namespace gwtf {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kStripList = 256;  // over-capacity arcs listed per instance (more: thread 0 rescans all)
 constexpr int kArcBits = 24;
 constexpr uint64_t kNoPred = (1ull << kArcBits) - 1;
 constexpr int64_t kBias = 1ll << 38;  // |distance| < 2^38 (checked per relaxation)
@@ -152,7 +153,8 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
                                                         int32_t* arc_all, int32_t* snk_f_all, uint64_t* lab_all,
                                                         int32_t* stamp_all, int64_t* F_out, int64_t* cost_out,
                                                         int64_t* stats_out, int32_t* status_out) {
-  __shared__ int changed_sm, bad_sm, last_sm, cyc_sm;
+  __shared__ int changed_sm, bad_sm, last_sm, cyc_sm, strip_n;
+  __shared__ int strip_list[kStripList];
   __shared__ unsigned long long cost_sm;
   const int S = P.S, n = P.n;
   const int N = 2 + 2 * S * n;
@@ -173,10 +175,23 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
     int32_t* stamp = stamp_all + (size_t)blockIdx.x * N;
     int64_t stripped = 0, cycles = 0, augment = 0;
     int status = 0;
-    // ---- 1. strip (thread 0; few units) ----
-    if (threadIdx.x == 0) {
-      bad_sm = 0;
-      for (int64_t e = 0; e < E; ++e) {
+    // ---- 1. strip: the team finds the over-capacity arcs, thread 0 strips their units ----
+    // (stripping only lowers flows, so an arc within capacity before the strip stays so)
+    if (threadIdx.x == 0) { bad_sm = 0; strip_n = 0; }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      const ArcV a = arc_of(c, e);
+      if (*a.x > a.cap) {
+        const int slot = atomicAdd(&strip_n, 1);
+        if (slot < kStripList) strip_list[slot] = (int)e;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && strip_n > 0) {
+      const bool listed = strip_n <= kStripList;
+      const int64_t cnt = listed ? strip_n : E;
+      for (int64_t j = 0; j < cnt; ++j) {
+        const int64_t e = listed ? strip_list[j] : j;
         const ArcV a = arc_of(c, e);
         while (!bad_sm && *a.x > a.cap) {
           if (!strip_unit(c, e)) bad_sm = 4;
