@@ -6,6 +6,10 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 CXX ?= g++
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fno-fast-math --expt-relaxed-constexpr
+# make DEV=1: development build that honours GWTF_DEBUG_FLAGS (phase timers, key dumps, ...)
+ifeq ($(DEV),1)
+NVFLAGS += -DGWTF_DEV_FLAGS
+endif
 PKG := paper_2509_21221_b200
 CSRC := $(PKG)/csrc
 KERN := $(wildcard $(CSRC)/*.cu)

@@ -155,7 +155,9 @@ gwtf_status gwtf_flow_solve_and_rounds(gwtf_flow_t h, int32_t max_rounds, int64_
  * s = -1, snk_cost[b][u_src] for s = S-1 (cost may be GWTF_ABSENT: a dropped link).
  * Round-state pointers into crashed relays or across dropped links are cleared in place;
  * accepted-move counters, deny counters and quiet counters reset.  The next solve_batch
- * is a cold solve on the masked graph.  INVALID on out-of-range updates. */
+ * is a cold solve on the masked graph.  INVALID on out-of-range updates; OVERFLOW (that update
+ * rejected) when a finite cost c breaks create's key bounds, (2Sn+2)*c >= 2^42 or
+ * (2Sn+2)*c*Mmax >= 2^62.  Other valid updates are applied in both cases. */
 gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const int32_t* edge_updates,
                                   int64_t k);
 
@@ -177,6 +179,18 @@ gwtf_status gwtf_flow_get_assignment(gwtf_flow_t h, int32_t* node_flow, int32_t*
 gwtf_status gwtf_flow_export_round_state(gwtf_flow_t h, int32_t* up, int32_t* down, int32_t* src_down,
                                          int32_t* snk_up, int32_t* kacc, int32_t* deny, int32_t* quiet,
                                          int64_t* round);
+
+/* Inverse of gwtf_flow_export_round_state (checkpoint / resume of the decentralized rounds,
+ * SURVEY.md 5): installs a round state given in the export layouts (device pointers, or host
+ * pointers with GWTF_HOST_PTRS; copied, the caller keeps ownership).  up/down/src_down/snk_up are
+ * required; kacc/deny/quiet/round may be NULL (= 0).  The state is checked on the device: every
+ * pointer must be answered by its target (pairing bijectivity), cross one stage
+ * boundary (or reach the data node from stage 0 / S-1, slot index below the instance's supply),
+ * and unusable slots (dead relay, j >= cap) must be FREE.  On a violation the round
+ * state is reset to empty and GWTF_E_INVALID is returned.  Synchronizes the stream. */
+gwtf_status gwtf_flow_import_round_state(gwtf_flow_t h, const int32_t* up, const int32_t* down,
+                                         const int32_t* src_down, const int32_t* snk_up, const int32_t* kacc,
+                                         const int32_t* deny, const int32_t* quiet, const int64_t* round);
 
 /* Save / restore the handle's mutable state (masks, costs, round state) on the device,
  * e.g. to replay the same churn step several times in a benchmark. */

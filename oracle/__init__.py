@@ -56,6 +56,13 @@ def lib():
         L.orc_rounds_apply_churn.argtypes = [P, P, P, ctypes.c_int64]
         L.orc_rounds_export.argtypes = [P] + [P] * 8
         L.orc_rounds_digest.restype = ctypes.c_uint64
+        L.orc_rounds_import.argtypes = [P] + [P] * 6 + [ctypes.c_int32, ctypes.c_int64]
+        L.orc_mix64.restype = ctypes.c_uint64
+        L.orc_mix64.argtypes = [ctypes.c_uint64]
+        L.orc_rng_h.restype = ctypes.c_uint64
+        L.orc_rng_h.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]
+        L.orc_pick.restype = ctypes.c_uint32
+        L.orc_pick.argtypes = [ctypes.c_uint64, ctypes.c_uint32]
         L.orc_rounds_digest.argtypes = [P]
         L.orc_rounds_instance.argtypes = [P] + [P] * 5
         L.orc_llama_victim.restype = ctypes.c_int32
@@ -269,6 +276,15 @@ class Rounds:
         lib().orc_rounds_export(self.h, _ptr(up), _ptr(dn), _ptr(sd), _ptr(su), _ptr(k), _ptr(dw), ctypes.byref(q),
                                 ctypes.byref(r))
         return dict(up=up, down=dn, src_down=sd, snk_up=su, kacc=k, deny=dw, quiet=q.value, round=r.value)
+
+    def import_state(self, st: dict):
+        """Install a round state in export()'s layouts (checkpoint / resume); raises if it is not a
+        valid pairing."""
+        c = lambda k: np.ascontiguousarray(np.asarray(st[k], np.int32).reshape(-1))  # noqa: E731
+        arrs = [c("up"), c("down"), c("src_down"), c("snk_up"), c("kacc"), c("deny")]
+        rc = lib().orc_rounds_import(self.h, *[_ptr(a) for a in arrs], int(st.get("quiet", 0)), int(st.get("round", 0)))
+        if rc != 0:
+            raise ValueError("orc_rounds_import: not a valid pairing state")
 
     def digest(self) -> int:
         return int(lib().orc_rounds_digest(self.h))
@@ -521,3 +537,17 @@ def multi_source_ssp(I: Instance, srcs, snks, supplies):
         out.append((r.F, r.cost, r.node_flow.copy()))
         cap = cap - r.node_flow
     return out
+
+
+# ------------------------------------------------------------------ the R4 draws
+def mix64(z: int) -> int:
+    return int(lib().orc_mix64(z & (2**64 - 1)))
+
+
+def rng_h(seed: int, inst: int, rnd: int, gid: int, stream: int) -> int:
+    return int(lib().orc_rng_h(seed & (2**64 - 1), inst, rnd, gid, stream))
+
+
+def pick(x: int, m: int) -> int:
+    return int(lib().orc_pick(x & (2**64 - 1), m))
+

@@ -1267,6 +1267,51 @@ int orc_rounds_export(const orc_rounds* o, int32_t* up, int32_t* down, int32_t* 
   return 0;
 }
 
+// Inverse of orc_rounds_export (checkpoint / resume): the caller supplies a state in the
+// export layouts.  Checked here: the pairing bijectivity and capacity invariants,
+// pointers only across one stage boundary (or to the data node at the ends); -1 when violated.
+int orc_rounds_import(orc_rounds* o, const int32_t* up, const int32_t* down, const int32_t* src_down,
+                      const int32_t* snk_up, const int32_t* kacc, const int32_t* deny, int32_t quiet, int64_t round) {
+  Rounds& R = o->R;
+  const Inst& I = R.I;
+  const int S = I.S, n = I.n, MC = I.MC;
+  const int64_t ns = (int64_t)S * n * MC, M = I.M;
+  for (int64_t p = 0; p < ns; ++p) {
+    const int g = (int)(p / MC), j = (int)(p % MC), s = g / n;
+    const bool usable = R.alive(g) && j < R.capE(g);
+    if (!usable && (up[p] != NONE || down[p] != NONE)) return -1;
+    if (up[p] >= 0 && (up[p] >= ns || up[p] / MC / n != s - 1 || down[up[p]] != (int32_t)p)) return -1;
+    if (up[p] <= -2 && (s != 0 || -2 - up[p] >= M || src_down[-2 - up[p]] != (int32_t)p)) return -1;
+    if (down[p] >= 0 && (down[p] >= ns || down[p] / MC / n != s + 1 || up[down[p]] != (int32_t)p)) return -1;
+    if (down[p] <= -2 && (s != S - 1 || -2 - down[p] >= M || snk_up[-2 - down[p]] != (int32_t)p)) return -1;
+  }
+  for (int64_t k = 0; k < M; ++k) {
+    if (src_down[k] != NONE && (src_down[k] < 0 || src_down[k] >= ns || up[src_down[k]] != (int32_t)(-2 - k))) return -1;
+    if (snk_up[k] != NONE && (snk_up[k] < 0 || snk_up[k] >= ns || down[snk_up[k]] != (int32_t)(-2 - k))) return -1;
+  }
+  R.up.assign(up, up + ns);
+  R.down.assign(down, down + ns);
+  R.src_down.assign(src_down, src_down + M);
+  R.snk_up.assign(snk_up, snk_up + M);
+  R.kacc.assign(kacc, kacc + (size_t)S * n);
+  R.deny.assign(deny, deny + (size_t)S * n);
+  R.quiet = quiet;
+  R.round = round;
+  return 0;
+}
+
+// The counter-based draws of R4: h(gid, stream) of an instance/round, and
+// pick(x, m) = floor((x >> 32) * m / 2^32); exported for the known-answer tests.
+uint64_t orc_mix64(uint64_t z) { return mix64(z); }
+uint64_t orc_rng_h(uint64_t seed, int64_t inst, int64_t round, int32_t gid, int32_t stream) {
+  Rounds R;
+  R.seed = seed;
+  R.inst = inst;
+  R.round = round;
+  return R.h(gid, stream);
+}
+uint32_t orc_pick(uint64_t x, uint32_t m) { return pick(x, m); }
+
 uint64_t orc_rounds_digest(const orc_rounds* o) { return o->R.digest(); }
 
 int orc_rounds_instance(const orc_rounds* o, int32_t* cap_eff, uint8_t* alive, int32_t* src, int32_t* snk,

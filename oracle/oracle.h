@@ -94,6 +94,16 @@ int orc_rounds_apply_churn(orc_rounds* R, const uint8_t* alive_new, const int32_
 int orc_rounds_export(const orc_rounds* R, int32_t* up, int32_t* down, int32_t* src_down, int32_t* snk_up,
                       int32_t* kacc, int32_t* deny, int32_t* quiet, int64_t* round);
 uint64_t orc_rounds_digest(const orc_rounds* R);
+/* Inverse of orc_rounds_export (checkpoint / resume): install a round state given in the
+ * export layouts.  Returns -1 (state unchanged) unless the pointers are a valid pairing:
+ * bijective, within capacity, across one stage boundary or to the data node. */
+int orc_rounds_import(orc_rounds* R, const int32_t* up, const int32_t* down, const int32_t* src_down,
+                      const int32_t* snk_up, const int32_t* kacc, const int32_t* deny, int32_t quiet, int64_t round);
+/* The R4 draws: mix64 = splitmix64 finalizer, h(gid, stream) =
+ * mix(mix(mix(mix(seed) ^ inst) ^ round) ^ (gid*4 + stream)), pick(x, m) = ((x >> 32) * m) >> 32. */
+uint64_t orc_mix64(uint64_t z);
+uint64_t orc_rng_h(uint64_t seed, int64_t inst, int64_t round, int32_t gid, int32_t stream);
+uint32_t orc_pick(uint64_t x, uint32_t m);
 /* The instance as currently masked (after churn): cap_eff [S][n], src [n], snk [n], link [S-1][n][n]. */
 int orc_rounds_instance(const orc_rounds* R, int32_t* cap_eff, uint8_t* alive, int32_t* src, int32_t* snk,
                         int32_t* link);

@@ -49,6 +49,7 @@ EXPORTS = {
     "gwtf_flow_get_assignment": ([P, P, P, P, P], I32),
     "gwtf_flow_residual_caps": ([P, P], I32),
     "gwtf_flow_export_round_state": ([P, P, P, P, P, P, P, P, P], I32),
+    "gwtf_flow_import_round_state": ([P, P, P, P, P, P, P, P, P], I32),
     "gwtf_flow_snapshot": ([P], I32),
     "gwtf_flow_restore": ([P], I32),
     "gwtf_flow_set_profiling": ([P, I32], I32),

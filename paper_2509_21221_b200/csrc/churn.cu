@@ -61,6 +61,16 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
     const int b = u[0], s = u[1], v = u[2], w = u[3], c = u[4];
     const bool cost_ok = c == kAbsent || (c >= 0 && c < (1 << 30));
     if (b < 0 || b >= P.B || !cost_ok) { atomicOr(bad, 1); continue; }
+    if (c != kAbsent) {
+      // the bounds gwtf_flow_create enforces: a simple residual path's cost must
+      // fit the 64-bit key's 42-bit cost field, and M of them an int64 total; such an update is
+      // rejected (not applied), bit 4
+      const uint64_t path = (uint64_t)(2 * P.S * P.n + 2) * (uint64_t)c;  // < 2^61
+      if (path >= (1ull << 42) || (P.Mmax > 0 && path > ((1ull << 62) - 1) / (uint64_t)P.Mmax)) {
+        atomicOr(bad, 4);
+        continue;
+      }
+    }
     if (c != kAbsent) atomicMax(&P.counters[6], c);  // weight bound of the cluster tier's 32-bit keys
     if (s == -1) {
       if (v < 0 || v >= P.n) { atomicOr(bad, 1); continue; }
@@ -137,6 +147,42 @@ __global__ void churn_state_kernel(const Problem P) {
   }
   for (size_t t = gtid(); t < (size_t)P.B * Sn; t += gstride()) { P.kacc[t] = 0; P.deny[t] = 0; }
   for (size_t t = gtid(); t < (size_t)P.B; t += gstride()) P.quiet[t] = 0;
+}
+
+// Validation of an imported round state (gwtf_flow_import_round_state): every
+// pointer of a usable slot is answered by its target (pairing bijectivity), crosses
+// exactly one stage boundary or reaches the data node at the ends, data-node slots stay below
+// the instance's supply, unusable slots (dead relay, j >= cap) hold nothing.
+__global__ void import_check_kernel(const Problem P, int32_t* bad) {
+  const int Sn = P.S * P.n, MC = P.MC;
+  const int32_t ns = Sn * MC;
+  const size_t nslot = (size_t)P.B * ns;
+  int fail = 0;
+  for (size_t t = gtid(); t < nslot; t += gstride()) {
+    const int b = (int)(t / ns);
+    const int p = (int)(t % ns);
+    const int v = p / MC, j = p % MC, s = v / P.n;
+    const size_t o = (size_t)b * Sn + v;
+    const int32_t* up = P.up + (size_t)b * ns;
+    const int32_t* dn = P.down + (size_t)b * ns;
+    const int64_t M = P.supply[b];
+    const int32_t u = up[p], d = dn[p];
+    if (!(P.alive[o] && j < P.cap[o])) { fail |= u != kNone || d != kNone; continue; }
+    if (u >= 0) fail |= u >= ns || u / MC / P.n != s - 1 || dn[u] != p;
+    else if (u != kNone) fail |= s != 0 || -2 - u >= M || P.src_down[(size_t)b * P.Mmax - 2 - u] != p;
+    if (d >= 0) fail |= d >= ns || d / MC / P.n != s + 1 || up[d] != p;
+    else if (d != kNone) fail |= s != P.S - 1 || -2 - d >= M || P.snk_up[(size_t)b * P.Mmax - 2 - d] != p;
+  }
+  for (size_t t = gtid(); t < (size_t)P.B * P.Mmax; t += gstride()) {
+    const int b = (int)(t / P.Mmax);
+    const int k = (int)(t % P.Mmax);
+    const int32_t sd = P.src_down[t], su = P.snk_up[t];
+    if (k >= P.supply[b]) { fail |= sd != kNone || su != kNone; continue; }
+    if (sd != kNone) fail |= sd < 0 || sd >= ns || P.up[(size_t)b * ns + sd] != -2 - k;
+    if (su != kNone) fail |= su < 0 || su >= ns || P.down[(size_t)b * ns + su] != -2 - k;
+  }
+  for (size_t t = gtid(); t < (size_t)P.B * Sn; t += gstride()) fail |= P.kacc[t] < 0 || P.deny[t] < 0;
+  if (fail) atomicOr(bad, 1);
 }
 
 __global__ void dense_arcs_kernel(const Problem P, int32_t* dense) {
@@ -216,6 +262,11 @@ cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32
     if (e != cudaSuccess) return e;
   }
   churn_state_kernel<<<grid_for((size_t)P.B * P.S * P.n * P.MC + P.B * P.Mmax), 256, 0, st>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_import_check(const Problem& P, int32_t* bad, cudaStream_t st) {
+  import_check_kernel<<<grid_for((size_t)P.B * P.S * P.n * P.MC + (size_t)P.B * P.Mmax), 256, 0, st>>>(P, bad);
   return cudaGetLastError();
 }
 

@@ -353,7 +353,11 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   P.objective = d->objective;
   P.W = d->steady_window;
   P.deny_after = d->deny_after;
+#ifdef GWTF_DEV_FLAGS
+  // development builds only (make DEV=1): testing switches, some of which (e.g. bit 64, no tile
+  // stream) deliberately give wrong results; a product build never reads them
   if (const char* dbg = getenv("GWTF_DEBUG_FLAGS")) P.debug = atoi(dbg);
+#endif
 
   // exact-solve tiers for instances that do not fit in shared memory: the cluster tier (one
   // thread-block cluster per instance, tiles streamed from HBM) when the device can host it,
@@ -581,6 +585,7 @@ gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const
     CK(h, cudaStreamSynchronize(h->stream));
     if (bad & 2) h->P.tile16 = nullptr;  // a cost no longer fits 16 bits: stream the int32 tiles
     if (bad & 1) return fail(GWTF_E_INVALID, "edge update out of range (valid updates were applied)");
+    if (bad & 4) return fail(GWTF_E_OVERFLOW, "edge update cost breaks the key bounds (rejected; valid updates were applied)");
   }
   return GWTF_OK;
 }
@@ -650,6 +655,41 @@ gwtf_status gwtf_flow_export_round_state(gwtf_flow_t h, int32_t* up, int32_t* do
   if (quiet) CK(h, cudaMemcpyAsync(quiet, P.quiet, (size_t)P.B * 4, kind, h->stream));
   if (round) CK(h, cudaMemcpyAsync(round, P.round, (size_t)P.B * 8, kind, h->stream));
   if (host_mode(h)) CK(h, cudaStreamSynchronize(h->stream));
+  return GWTF_OK;
+}
+
+gwtf_status gwtf_flow_import_round_state(gwtf_flow_t h, const int32_t* up, const int32_t* down,
+                                         const int32_t* src_down, const int32_t* snk_up, const int32_t* kacc,
+                                         const int32_t* deny, const int32_t* quiet, const int64_t* round) {
+  gwtf_status s = enter(h);
+  if (s != GWTF_OK) return s;
+  if (!up || !down || !src_down || !snk_up) return fail(GWTF_E_INVALID, "up/down/src_down/snk_up are required");
+  const Problem& P = h->P;
+  const size_t Sn = (size_t)P.S * P.n;
+  const size_t nslot = (size_t)P.B * Sn * P.MC;
+  const cudaMemcpyKind kind = host_mode(h) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if (nslot) CK(h, cudaMemcpyAsync(P.up, up, nslot * 4, kind, h->stream));
+  if (nslot) CK(h, cudaMemcpyAsync(P.down, down, nslot * 4, kind, h->stream));
+  if (P.Mmax) CK(h, cudaMemcpyAsync(P.src_down, src_down, (size_t)P.B * P.Mmax * 4, kind, h->stream));
+  if (P.Mmax) CK(h, cudaMemcpyAsync(P.snk_up, snk_up, (size_t)P.B * P.Mmax * 4, kind, h->stream));
+  if (kacc) CK(h, cudaMemcpyAsync(P.kacc, kacc, P.B * Sn * 4, kind, h->stream));
+  else CK(h, cudaMemsetAsync(P.kacc, 0, P.B * Sn * 4, h->stream));
+  if (deny) CK(h, cudaMemcpyAsync(P.deny, deny, P.B * Sn * 4, kind, h->stream));
+  else CK(h, cudaMemsetAsync(P.deny, 0, P.B * Sn * 4, h->stream));
+  if (quiet) CK(h, cudaMemcpyAsync(P.quiet, quiet, (size_t)P.B * 4, kind, h->stream));
+  else CK(h, cudaMemsetAsync(P.quiet, 0, (size_t)P.B * 4, h->stream));
+  if (round) CK(h, cudaMemcpyAsync(P.round, round, (size_t)P.B * 8, kind, h->stream));
+  else CK(h, cudaMemsetAsync(P.round, 0, (size_t)P.B * 8, h->stream));
+  CK(h, cudaMemsetAsync(h->bad_flag, 0, 4, h->stream));
+  CK(h, launch_import_check(P, h->bad_flag, h->stream));
+  h->kernel_launches += 1;
+  int32_t bad = 0;
+  CK(h, cudaMemcpyAsync(&bad, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (bad) {
+    CK(h, launch_init_round_state(P, h->stream));  // never leave an inconsistent pairing behind
+    return fail(GWTF_E_INVALID, "imported round state is not a valid pairing (state reset to empty)");
+  }
   return GWTF_OK;
 }
 

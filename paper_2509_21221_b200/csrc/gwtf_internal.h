@@ -94,6 +94,7 @@ int ssp_cluster_size(const Problem& P);
 cudaError_t launch_ssp_cluster(const Problem& P, const SspOut& o, cudaStream_t st, int C);
 cudaError_t launch_rounds(const Problem& P, const RoundsOut& o, cudaStream_t st, int num_sms);
 cudaError_t launch_init_round_state(const Problem& P, cudaStream_t st);
+cudaError_t launch_import_check(const Problem& P, int32_t* bad, cudaStream_t st);
 cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32_t* upd, int64_t k,
                          int32_t* bad_flag, cudaStream_t st);
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st);

@@ -167,8 +167,16 @@ class Flow:
             _ptr(out_rounds.dangling)))
         return out_sol, out_rounds
 
+    def _dev(self):
+        return None if self.host else self.device
+
     def apply_churn(self, alive_new=None, edge_updates=None):
+        B, S, n = self.B, self.S, self.n
+        if alive_new is not None:
+            _need(alive_new, torch.uint8, (B, S, n), "alive_new", self._dev())
         k = 0 if edge_updates is None else int(edge_updates.shape[0])
+        if edge_updates is not None:
+            _need(edge_updates, torch.int32, (k, 5), "edge_updates", self._dev())
         check("gwtf_flow_apply_churn", lib().gwtf_flow_apply_churn(
             self.h, _ptr(alive_new), _ptr(edge_updates) if k else None, k))
 
@@ -197,6 +205,21 @@ class Flow:
         check("gwtf_flow_export_round_state", lib().gwtf_flow_export_round_state(
             self.h, *[_ptr(st[k]) for k in ("up", "down", "src_down", "snk_up", "kacc", "deny", "quiet", "round")]))
         return st
+
+    def import_round_state(self, st: dict):
+        """Install a round state in export_round_state()'s layouts (gwtf_flow_import_round_state:
+        checkpoint / resume; checked on the device, GwtfError E_INVALID if it is not a valid pairing)."""
+        B, S, n, MC, M = self.B, self.S, self.n, self.max_cap, self.Mmax
+        shapes = dict(up=(B, S, n, MC), down=(B, S, n, MC), src_down=(B, M), snk_up=(B, M), kacc=(B, S, n),
+                      deny=(B, S, n), quiet=(B,), round=(B,))
+        args = []
+        for key, shape in shapes.items():
+            t = st.get(key)
+            if t is None and key in ("kacc", "deny", "quiet", "round"):
+                args.append(None)
+                continue
+            args.append(_ptr(_need(t, torch.int64 if key == "round" else torch.int32, shape, key, self._dev())))
+        check("gwtf_flow_import_round_state", lib().gwtf_flow_import_round_state(self.h, *args))
 
     def snapshot(self):
         check("gwtf_flow_snapshot", lib().gwtf_flow_snapshot(self.h))
@@ -231,6 +254,12 @@ class Flow:
         (gwtf_flow_warm_reroute).  The four flow tensors (get_assignment's
         layouts, on this handle's side: device or host) are overwritten with the repaired optimum.
         -> (F [B], cost [B], stats [B][3] = stripped / cycles / augmentations, status [B])."""
+        B, S, n = self.B, self.S, self.n
+        _need(node_flow, torch.int32, (B, S, n), "node_flow", self._dev())
+        _need(src_flow, torch.int32, (B, n), "src_flow", self._dev())
+        _need(snk_flow, torch.int32, (B, n), "snk_flow", self._dev())
+        if arc_flow is not None and arc_flow.numel():
+            _need(arc_flow, torch.int32, (B, S - 1, n, n), "arc_flow", self._dev())
         F = self._out((self.B,), torch.int64)
         C = self._out((self.B,), torch.int64)
         St = self._out((self.B, 3), torch.int64)
