@@ -80,6 +80,12 @@ struct Inst {
   int64_t *scost, *adv_cost;
   int32_t *req_slot, *req_target, *grant, *prop, *ptouch, *capv;
   uint32_t* summ;
+  // incremental bookkeeping (K2): slots whose down pointer changed since the costs were
+  // last brought up to date (flag + list), relays whose summary / advertisement is stale (flag +
+  // list), the advertiser bitmask per stage [S][W] and its population count per stage
+  int32_t *mflag, *mlist, *rflag, *rlist, *advcnt, *lcnt;
+  uint32_t* advm;
+  int W;
   uint64_t *pkey, *res;
   const int32_t *tile, *src, *snk;
   const uint8_t* alive;
@@ -173,6 +179,30 @@ struct Inst {
     }
     return bc;
   }
+  __device__ void mark_slot(int32_t p) const {
+    if (p >= 0 && atomicExch(&mflag[p], 1) == 0) mlist[atomicAdd(&lcnt[0], 1)] = p;
+  }
+  __device__ void mark_relay(int v) const {
+    if (atomicExch(&rflag[v], 1) == 0) rlist[atomicAdd(&lcnt[1], 1)] = v;
+  }
+  // cost to sink of slot p from its down pointer (valid when scost[down p] is up to date)
+  __device__ int64_t cost_from(int32_t p) const {
+    const int32_t d1 = down[p];
+    if (d1 == kNone) return INF;
+    const int v = relay(p), s = dn.div(v), i = v - s * n;
+    if (d1 <= -2) return cst(snk[i]);
+    return sadd(c_link(s, i, relay(d1) - (s + 1) * n), scost[d1]);
+  }
+  // the advertisement of v and its bit in the stage's advertiser mask (count kept in advcnt)
+  __device__ void set_adv(int v, int64_t a) const {
+    const int64_t old = adv_cost[v];
+    adv_cost[v] = a;
+    if ((a != INF) == (old != INF)) return;
+    const int s = dn.div(v), i = v - s * n;
+    uint32_t* w = advm + (size_t)s * W + (i >> 5);
+    if (a != INF) { atomicOr(w, 1u << (i & 31)); atomicAdd(&advcnt[s], 1); }
+    else { atomicAnd(w, ~(1u << (i & 31))); atomicSub(&advcnt[s], 1); }
+  }
   __device__ int nth_paired(int v, int q) const {
     const int c = capv[v], base = v * MC;
     _Pragma("unroll 1") for (int j = 0; j < c; ++j)
@@ -242,7 +272,7 @@ __host__ __device__ inline bool rounds_tile_in_smem(const Problem& P) {
 }
 struct RoundsLayout {
   size_t res, scost, adv_cost, pkey, up, down, src_down, snk_up, kacc, deny, req_slot, req_target, grant, prop,
-      ptouch, capv, summ, tile, mbar, cells, total;
+      ptouch, capv, summ, mflag, mlist, rflag, rlist, advm, advcnt, lcnt, tile, mbar, cells, total;
 };
 // smem: everything of one instance; otherwise only the per-instance scratch (the state
 // arrays then live in the handle's global buffers)
@@ -267,6 +297,13 @@ __host__ __device__ inline RoundsLayout rounds_layout(const Problem& P, bool sme
   L.ptouch = o; o += al16r(Sn * 4 * 4);
   L.capv = o; o += al16r(Sn * 4);
   L.summ = o; o += al16r(Sn * 4);
+  L.mflag = o; o += al16r(ns * 4);
+  L.mlist = o; o += al16r((ns + 16) * 4);
+  L.rflag = o; o += al16r(Sn * 4);
+  L.rlist = o; o += al16r(Sn * 4);
+  L.advm = o; o += al16r((size_t)P.S * ((P.n + 31) / 32) * 4);
+  L.advcnt = o; o += al16r((size_t)P.S * 4);
+  L.lcnt = o; o += 16;
   L.tile = o; if (smem && rounds_tile_in_smem(P)) o += al16r((size_t)(P.S > 1 ? P.S - 1 : 0) * P.n * P.ld * 4);
   L.mbar = o; o += 16;
   L.cells = o; o += 64;  // the cluster team's reduction cells
@@ -337,6 +374,14 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     I.ptouch = (int32_t*)(base + Lr.ptouch);
     I.capv = (int32_t*)(base + Lr.capv);
     I.summ = (uint32_t*)(base + Lr.summ);
+    I.mflag = (int32_t*)(base + Lr.mflag);
+    I.mlist = (int32_t*)(base + Lr.mlist);
+    I.rflag = (int32_t*)(base + Lr.rflag);
+    I.rlist = (int32_t*)(base + Lr.rlist);
+    I.advm = (uint32_t*)(base + Lr.advm);
+    I.advcnt = (int32_t*)(base + Lr.advcnt);
+    I.lcnt = (int32_t*)(base + Lr.lcnt);
+    I.W = (n + 31) / 32;
     const int M = I.M;
     const int32_t* cap_g = P.cap + (size_t)b * Sn;
     _Pragma("unroll 1") for (int k = T.tid; k < Sn; k += TPI) I.capv[k] = I.alive[k] ? cap_g[k] : 0;
@@ -383,6 +428,53 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     const int cost_mode = P.rounds_cost_mode;
     uint64_t round = (uint64_t)P.round[b];
     int r = 0;
+    const int W = I.W;
+    const int lane_w = T.tid >> 5, nwarps = TPI / 32;  // warp index / count inside the team
+    // ---- incremental bookkeeping (K2) ----
+    // walkers: every marked slot that has no marked slot below it in its chain (chains are disjoint
+    // paths of down pointers) recomputes its own cost and every cost above it, bottom-up; below the
+    // lowest mark nothing changed, so each chain is brought up to date by exactly one walker.  The
+    // relay at the top of a chain (an OUT slot's owner) gets its advertisement refreshed.
+    auto walk_marks = [&]() {
+      const int nm = *(volatile int*)&I.lcnt[0];
+      _Pragma("unroll 1") for (int k = T.tid; k < nm; k += TPI) {
+        const int32_t p = I.mlist[k];
+        bool lowest = true;
+        _Pragma("unroll 1") for (int32_t q = I.down[p]; q >= 0; q = I.down[q])
+          if (*(volatile int32_t*)&I.mflag[q]) { lowest = false; break; }
+        if (!lowest) continue;
+        int32_t x = p;
+        int64_t c = p - I.relay(p) * MC < I.capv[I.relay(p)] ? I.cost_from(p) : INF;
+        for (;;) {
+          I.scost[x] = c;
+          const int32_t u = I.up[x];
+          if (u < 0) {
+            if (u == kNone) I.mark_relay(I.relay(x));
+            break;
+          }
+          const int vu = I.relay(u), su = I.dn.div(vu);
+          c = sadd(I.c_link(su, vu - su * n, I.relay(x) - (su + 1) * n), c);
+          x = u;
+        }
+      }
+    };
+    // after a barrier: clear the slot marks; refresh summaries (and advertisements) of the listed relays
+    // (returns the list lengths it read: the reset in the next phase uses them, not the counters)
+    auto flush_relays = [&](int& nm, int& nr) {
+      nm = *(volatile int*)&I.lcnt[0];
+      _Pragma("unroll 1") for (int k = T.tid; k < nm; k += TPI) I.mflag[I.mlist[k]] = 0;
+      nr = *(volatile int*)&I.lcnt[1];
+      _Pragma("unroll 1") for (int k = T.tid; k < nr; k += TPI) {
+        const int v = I.rlist[k];
+        I.summ[v] = I.summarize(v);
+        I.set_adv(v, I.relay_adv(v));
+      }
+    };
+    // after the next barrier: empty both lists
+    auto reset_lists = [&](int nr) {
+      _Pragma("unroll 1") for (int k = T.tid; k < nr; k += TPI) I.rflag[I.rlist[k]] = 0;
+      if (T.tid == 0) { I.lcnt[0] = 0; I.lcnt[1] = 0; }
+    };
     T.sync();
     bool prev_quiet = false;  // the last round changed nothing (the first round of a call always runs)
     while (r < o.max_rounds) {
@@ -393,20 +485,49 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       // same requests and again no grant, so the round starts at R4 (its RNG is the only input
       // that differs); scost, adv_cost and req_* still hold the previous round's values
       if (!prev_quiet) {
+      if (r == 0) {
+        // ---------- first round of the call: every cost, summary and advertisement from scratch
+        // (the state may come from a churn, an import or another call) ----------
+        _Pragma("unroll 1") for (int k = T.tid; k < Sn * MC; k += TPI) I.mflag[k] = 0;
+        _Pragma("unroll 1") for (int k = T.tid; k < Sn; k += TPI) { I.rflag[k] = 0; I.adv_cost[k] = INF; }
+        _Pragma("unroll 1") for (int k = T.tid; k < S * W; k += TPI) I.advm[k] = 0u;
+        _Pragma("unroll 1") for (int k = T.tid; k < S; k += TPI) I.advcnt[k] = 0;
+        if (T.tid == 0) { I.lcnt[0] = 0; I.lcnt[1] = 0; }
+        if (cost_mode == 1) {
+          _Pragma("unroll 1") for (int t = T.tid; t < Sn * MC; t += TPI) I.slot_cost(t);
+          T.sync();
+        } else if (cost_mode == 2) {
+          _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.relay_costs(v);
+          T.sync();
+        } else {
+          compute_costs<TT>(T, I);  // stage-synchronous back-to-front recursion (ends with a barrier)
+        }
+        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
+          I.summ[v] = I.summarize(v);
+          I.set_adv(v, I.relay_adv(v));
+        }
+        T.sync();
+      } else {
+        // ---------- bring the costs up to date with the previous round's R3 / R6 changes ----------
+        walk_marks();
+        T.sync();
+        int nm, nr;
+        flush_relays(nm, nr);
+        T.sync();
+        reset_lists(nr);
+      }
       // ---------- R0a candidates: a relay holding an IN and an OUT slot ----------
       if (T.tid == 0) { sh_i32[0] = INT_MAX; sh_i32[1] = 0; }
       int cand = 0;
       _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
-        const uint32_t w = I.summarize(v);
+        const uint32_t w = I.summ[v];
         cand |= (w & 63u) != 63u && ((w >> 18) & 1u);
       }
       if (T.sync_or(cand)) {
-        // ---------- R0a self-pairing, costs of the round-start state ----------
-        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.relay_costs(v);
-        T.sync();
+        // ---------- R0a self-pairing, costs of the round-start state (scost is up to date) ----------
         _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
-          const Summ sm{I.summarize(v)};
-          if (!sm.has_in() || !sm.has_out()) continue;
+          const Summ sm{I.summ[v]};
+          if (!sm.has_in() || !sm.has_out() || !I.alive[v]) continue;
           const int x = v * MC + sm.first_in();
           int oo = -1;
           for (int j = 0; j < I.capv[v]; ++j) {
@@ -417,21 +538,20 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           I.down[x] = cdn;
           I.set_up_of(cdn, x);
           I.down[oo] = kNone;
+          I.mark_slot(x);
+          I.mark_slot(oo);
+          I.mark_relay(v);
           changed = 1;
         }
         T.sync();
-      }
-      // ---------- R0 cost to sink + advertisements; data-node slots ----------
-      if (cost_mode == 0) {  // stage-synchronous back-to-front recursion, then advertisements
-        compute_costs<TT>(T, I);
-        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
-      } else if (cost_mode == 1) {  // one chain walk per slot, then advertisements
-        _Pragma("unroll 1") for (int t = T.tid; t < Sn * MC; t += TPI) I.slot_cost(t);
+        walk_marks();
         T.sync();
-        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_adv(v);
-      } else {  // one chain walk per relay (fused advertisement)
-        _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) I.adv_cost[v] = I.relay_costs(v);
+        int nm, nr;
+        flush_relays(nm, nr);
+        T.sync();
+        reset_lists(nr);
       }
+      // ---------- data-node slots ----------
       {
         int fs = INT_MAX, anyfree = 0;
         _Pragma("unroll 1") for (int k = T.tid; k < M; k += TPI) {
@@ -444,21 +564,28 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       T.sync();
       const int d_rslot = *(volatile int*)&sh_i32[0];
       const int dsink_free = *(volatile int*)&sh_i32[1];
-      // ---------- R1 requests (one per node) ----------
+      // ---------- R1 requests (one per node): argmin over the next stage's advertisers only
+      // (the advertiser bitmask, in ascending position: the same lowest-j tie-break as a full scan
+      // that skips INF advertisements) ----------
       _Pragma("unroll 1") for (int rr = T.tid; rr <= Sn; rr += TPI) {
         int32_t rs = kNone, tg = -2;
         if (rr == Sn) {  // the data node requests for its lowest unpaired SRC slot
-          if (d_rslot != INT_MAX) {
+          if (d_rslot != INT_MAX && *(volatile int32_t*)&I.advcnt[0] > 0) {
             int64_t bc = INF;
-            _Pragma("unroll 1") for (int j = 0; j < n; ++j) {
-              const int64_t dj = cst(I.src[j]), aj = I.adv_cost[j];
-              if (dj == INF || aj == INF || !I.alive[j]) continue;
-              if (dj + aj < bc) { bc = dj + aj; tg = j; }
+            _Pragma("unroll 1") for (int w = 0; w < W; ++w) {
+              uint32_t bits = I.advm[w];
+              while (bits) {
+                const int j = w * 32 + __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int64_t dj = cst(I.src[j]), aj = I.adv_cost[j];
+                if (dj == INF || !I.alive[j]) continue;
+                if (dj + aj < bc) { bc = dj + aj; tg = j; }
+              }
             }
             if (tg != -2) rs = -2 - d_rslot;
           }
         } else if (I.alive[rr]) {
-          const Summ sm{I.summarize(rr)};
+          const Summ sm{I.summ[rr]};
           int32_t x = kNone;
           if (sm.has_in()) x = rr * MC + sm.first_in();                                   // (a)
           else if (!sm.has_out() && sm.first_free() != 63) x = rr * MC + sm.first_free();  // (b)
@@ -466,16 +593,21 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
             const int s = I.dn.div(rr), i = rr - s * n;
             if (s == S - 1) {
               if (I.snk[i] != kAbsent && dsink_free) tg = -1;
-            } else {
+            } else if (*(volatile int32_t*)&I.advcnt[s + 1] > 0) {
               int64_t bc = INF;
               const int32_t* col = I.tile + (size_t)s * n * I.ld + i;  // C[s][v][i], v = 0..n-1
               const int64_t* av = I.adv_cost + (s + 1) * n;
-              _Pragma("unroll 1") for (int jj = 0; jj < n; ++jj) {
-                const int64_t aj = av[jj];
-                if (aj == INF) continue;  // dead relays advertise INF
-                const int32_t c = col[(size_t)jj * I.ld];
-                if (c == kAbsent) continue;
-                if (c + aj < bc) { bc = c + aj; tg = (s + 1) * n + jj; }
+              const uint32_t* am = I.advm + (size_t)(s + 1) * W;
+              _Pragma("unroll 1") for (int w = 0; w < W; ++w) {
+                uint32_t bits = am[w];
+                while (bits) {
+                  const int jj = w * 32 + __ffs(bits) - 1;
+                  bits &= bits - 1;
+                  const int32_t c = col[(size_t)jj * I.ld];
+                  if (c == kAbsent) continue;
+                  const int64_t aj = av[jj];
+                  if (c + aj < bc) { bc = c + aj; tg = (s + 1) * n + jj; }
+                }
               }
             }
             if (tg != -2) rs = x;
@@ -488,28 +620,14 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       // ---------- R2 + R3: each target serves its requesters in ascending gid and commits ----------
       // (a target's eligibility only reads its own OUT slots, which only it modifies; requester
       // slots are IN/FREE slots written by exactly one target, so the fused commit equals
-      // "all grants on the pre-R3 state, then all commits")
-      _Pragma("unroll 1") for (int j = T.tid; j <= Sn; j += TPI) {
-        if (j == Sn) {  // D-sink: free SNK slots in index order to last-stage requesters in gid order
-          int k = 0;
-          _Pragma("unroll 1") for (int q = (S - 1) * n; q < Sn; ++q) {
-            if (I.req_target[q] != -1) continue;
-            while (k < M && I.snk_up[k] != kNone) ++k;
-            if (k >= M) break;
-            const int32_t rs = I.req_slot[q];
-            I.down[rs] = -2 - k;
-            I.snk_up[k] = rs;
-            I.deny[q] = 0;
-            changed = 1;
-            ++k;
-          }
-          continue;
-        }
+      // "all grants on the pre-R3 state, then all commits").  One warp per advertiser: the
+      // requesters of its stage are scanned 32 at a time with a ballot, in ascending gid.
+      _Pragma("unroll 1") for (int j = lane_w; j < Sn; j += nwarps) {
         const int64_t ac = I.adv_cost[j];
-        if (ac == INF) continue;  // no OUT slot: nothing to grant
+        if (ac == INF) continue;  // no OUT slot: nothing to grant (warp-uniform)
         const int s = I.dn.div(j);
         const int c = I.capv[j];
-        int cur = 0;
+        int cur = 0;  // lane 0's cursor over j's slots
         auto next_slot = [&]() -> int {
           while (cur < c) {
             const int p = j * MC + cur++;
@@ -518,27 +636,72 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           return -1;
         };
         if (s == 0) {  // the data node is the only requester of stage-0 relays
-          if (I.req_target[Sn] == j) {
+          if (lane == 0 && I.req_target[Sn] == j) {
             const int p = next_slot();
             if (p >= 0) {
               const int32_t rs = I.req_slot[Sn];
               I.src_down[-2 - rs] = p;
               I.up[p] = rs;
+              I.mark_relay(j);
               changed = 1;
             }
           }
-        } else {
-          _Pragma("unroll 1") for (int q = (s - 1) * n; q < s * n; ++q) {
-            if (I.req_target[q] != j) continue;
-            const int p = next_slot();
-            if (p < 0) break;
-            const int32_t rs = I.req_slot[q];
-            I.down[rs] = p;
-            I.up[p] = rs;
-            I.deny[q] = 0;
-            changed = 1;
-          }
+          continue;
         }
+        bool done = false;
+        _Pragma("unroll 1") for (int q0 = (s - 1) * n; q0 < s * n && !done; q0 += 32) {
+          const int q = q0 + lane;
+          uint32_t m = __ballot_sync(0xffffffffu, q < s * n && I.req_target[q] == j);
+          if (lane == 0) {
+            while (m) {
+              const int qq = q0 + __ffs(m) - 1;
+              m &= m - 1;
+              const int p = next_slot();
+              if (p < 0) { done = true; break; }
+              const int32_t rs = I.req_slot[qq];
+              I.down[rs] = p;
+              I.up[p] = rs;
+              I.deny[qq] = 0;
+              I.mark_slot(rs);
+              I.mark_relay(qq);
+              changed = 1;
+            }
+          }
+          done = __shfl_sync(0xffffffffu, done, 0);
+        }
+        if (lane == 0 && cur > 0) I.mark_relay(j);
+      }
+      // D-sink: free SNK slots in index order to last-stage requesters in gid order (last warp)
+      if (dsink_free && lane_w == nwarps - 1) {
+        int k = 0;  // lane 0's cursor over SNK slots
+        bool full = false;
+        _Pragma("unroll 1") for (int q0 = (S - 1) * n; q0 < Sn && !full; q0 += 32) {
+          const int q = q0 + lane;
+          uint32_t m = __ballot_sync(0xffffffffu, q < Sn && I.req_target[q] == -1);
+          if (lane == 0) {
+            while (m) {
+              const int qq = q0 + __ffs(m) - 1;
+              m &= m - 1;
+              while (k < M && I.snk_up[k] != kNone) ++k;
+              if (k >= M) { full = true; break; }
+              const int32_t rs = I.req_slot[qq];
+              I.down[rs] = -2 - k;
+              I.snk_up[k] = rs;
+              I.deny[qq] = 0;
+              I.mark_slot(rs);
+              I.mark_relay(qq);
+              changed = 1;
+              ++k;
+            }
+          }
+          full = __shfl_sync(0xffffffffu, full, 0);
+        }
+      }
+      T.sync();
+      // ---------- summaries of the relays R3 touched (R4 reads the post-R3 state) ----------
+      {
+        const int nr = *(volatile int*)&I.lcnt[1];
+        _Pragma("unroll 1") for (int k = T.tid; k < nr; k += TPI) I.summ[I.rlist[k]] = I.summarize(I.rlist[k]);
       }
       T.sync();
       }  // !prev_quiet
@@ -549,7 +712,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         int32_t t0 = -1, t1 = -1, t2 = -1, t3 = -1;
         uint64_t key = RES_NONE;
         if (I.alive[p] && I.req_target[p] == -2) {
-          const Summ sm{I.summarize(p)};
+          const Summ sm{I.summ[p]};
           const int s = I.dn.div(p), i = p - s * n;
           if (sm.has_in()) {  // DENY after deny_after idle rounds holding unpaired inflow
             const int dw = I.deny[p] + 1;
@@ -565,7 +728,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
             uint32_t qi = pick(I.h(p, 0), (uint32_t)(n - 1));
             if ((int)qi >= i) qi += 1;
             const int q = s * n + (int)qi;
-            const int nq = I.alive[q] ? Summ{I.summarize(q)}.npaired() : 0;
+            const int nq = I.alive[q] ? Summ{I.summ[q]}.npaired() : 0;
             if (nq > 0) {
               int64_t delta = 0;
               bool ok = false;
@@ -638,6 +801,8 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         }
         if (!win) continue;
         const int32_t x = I.prop[p * 4 + 1], y = I.prop[p * 4 + 2], z = I.prop[p * 4 + 3];
+        // every slot whose down pointer changes is marked (its cost and the costs above it are
+        // brought up to date at the next round's start); relays whose slot states change are listed
         if (kind == K_CHANGE) {
           const int32_t dx = I.down[x], dy = I.down[y];
           I.down[x] = dy;
@@ -645,6 +810,8 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           I.set_up_of(dy, x);
           I.set_up_of(dx, y);
           I.kacc[p] += 1;
+          I.mark_slot(x);
+          I.mark_slot(y);
         } else if (kind == K_REDIRECT) {
           const int32_t a = I.up[y], c = I.down[y];
           I.up[z] = a;
@@ -654,11 +821,19 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           I.up[y] = kNone;
           I.down[y] = kNone;
           I.kacc[p] += 1;
+          I.mark_slot(z);
+          I.mark_slot(y);
+          I.mark_slot(a);
+          I.mark_relay(p);
+          I.mark_relay(I.relay(y));
         } else {
           const int32_t a = I.up[x];
           I.up[x] = kNone;
           I.set_down_of(a, kNone);
           I.deny[p] = 0;
+          I.mark_slot(a);
+          I.mark_relay(p);
+          if (a >= 0) I.mark_relay(I.relay(a));
         }
         changed = 1;
       }
