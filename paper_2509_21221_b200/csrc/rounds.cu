@@ -85,6 +85,9 @@ struct Inst {
   // list), the advertiser bitmask per stage [S][W] and its population count per stage
   int32_t *mflag, *mlist, *rflag, *rlist, *advcnt, *lcnt;
   uint32_t* advm;
+  uint32_t* pmask;  // per relay: bit j = slot j is PAIRED (max_cap <= 32), maintained with summ
+  uint32_t* omask;  // per relay: bit j = slot j is OUT
+  int32_t* first_req;  // per target relay: lowest requester gid of the round (INT_MAX: none)
   int W;
   uint64_t *pkey, *res;
   const int32_t *tile, *src, *snk;
@@ -170,6 +173,15 @@ struct Inst {
     }
     scost[p0] = cc;
   }
+  // adv(v) from the maintained OUT-slot mask (refresh() first)
+  __device__ int64_t adv_of(int v) const {
+    int64_t bc = INF;
+    for (uint32_t t = omask[v]; t; t &= t - 1) {
+      const int64_t c = scost[v * MC + __ffs(t) - 1];
+      if (c < bc) bc = c;
+    }
+    return bc;
+  }
   __device__ int64_t relay_adv(int v) const {
     int64_t bc = INF;
     const int c = capv[v];
@@ -178,6 +190,29 @@ struct Inst {
       if (up[p] == kNone && down[p] != kNone && scost[p] < bc) bc = scost[p];
     }
     return bc;
+  }
+  // summary and PAIRED-slot mask of relay v, stored
+  __device__ void refresh(int v) const {
+    uint32_t fi = 63, ff = 63, np = 0, ho = 0, pm = 0, om = 0;
+    const int c = capv[v], base = v * MC;
+    _Pragma("unroll 1") for (int j = 0; j < c; ++j) {
+      const int t = st(base + j);
+      if (t == ST_IN && fi == 63) fi = j;
+      if (t == ST_FREE && ff == 63) ff = j;
+      np += t == ST_PAIRED;
+      pm |= (uint32_t)(t == ST_PAIRED) << j;
+      om |= (uint32_t)(t == ST_OUT) << j;
+      ho |= t == ST_OUT;
+    }
+    summ[v] = fi | (ff << 6) | (np << 12) | (ho << 18);
+    pmask[v] = pm;
+    omask[v] = om;
+  }
+  // the q-th PAIRED slot of relay v (slot order), from the maintained mask
+  __device__ int nth_paired_m(int v, int q) const {
+    uint32_t m = pmask[v];
+    for (; q > 0; --q) m &= m - 1;
+    return m ? v * MC + __ffs(m) - 1 : -1;
   }
   __device__ void mark_slot(int32_t p) const {
     if (p >= 0 && atomicExch(&mflag[p], 1) == 0) mlist[atomicAdd(&lcnt[0], 1)] = p;
@@ -272,7 +307,7 @@ __host__ __device__ inline bool rounds_tile_in_smem(const Problem& P) {
 }
 struct RoundsLayout {
   size_t res, scost, adv_cost, pkey, up, down, src_down, snk_up, kacc, deny, req_slot, req_target, grant, prop,
-      ptouch, capv, summ, mflag, mlist, rflag, rlist, advm, advcnt, lcnt, tile, mbar, cells, total;
+      ptouch, capv, summ, mflag, mlist, rflag, rlist, advm, advcnt, pmask, omask, first_req, lcnt, tile, mbar, cells, total;
 };
 // smem: everything of one instance; otherwise only the per-instance scratch (the state
 // arrays then live in the handle's global buffers)
@@ -303,6 +338,9 @@ __host__ __device__ inline RoundsLayout rounds_layout(const Problem& P, bool sme
   L.rlist = o; o += al16r(Sn * 4);
   L.advm = o; o += al16r((size_t)P.S * ((P.n + 31) / 32) * 4);
   L.advcnt = o; o += al16r((size_t)P.S * 4);
+  L.pmask = o; o += al16r(Sn * 4);
+  L.omask = o; o += al16r(Sn * 4);
+  L.first_req = o; o += al16r(Sn * 4);
   L.lcnt = o; o += 16;
   L.tile = o; if (smem && rounds_tile_in_smem(P)) o += al16r((size_t)(P.S > 1 ? P.S - 1 : 0) * P.n * P.ld * 4);
   L.mbar = o; o += 16;
@@ -381,6 +419,9 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     I.advm = (uint32_t*)(base + Lr.advm);
     I.advcnt = (int32_t*)(base + Lr.advcnt);
     I.lcnt = (int32_t*)(base + Lr.lcnt);
+    I.pmask = (uint32_t*)(base + Lr.pmask);
+    I.omask = (uint32_t*)(base + Lr.omask);
+    I.first_req = (int32_t*)(base + Lr.first_req);
     I.W = (n + 31) / 32;
     const int M = I.M;
     const int32_t* cap_g = P.cap + (size_t)b * Sn;
@@ -430,6 +471,23 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     int r = 0;
     const int W = I.W;
     const int lane_w = T.tid >> 5, nwarps = TPI / 32;  // warp index / count inside the team
+#ifdef GWTF_DEV_FLAGS
+    // development builds (GWTF_DEBUG_FLAGS & 16): leader-thread cycles per phase into stats[1200 + k]
+    const bool prof = (P.debug & 16) && T.tid == 0 && T.id == 0 && blockIdx.x == 0;
+    unsigned long long tl = clock64();
+#define RMARK(k)                                                                       \
+  do {                                                                                 \
+    if (prof) {                                                                        \
+      const unsigned long long t_ = clock64();                                         \
+      atomicAdd(&P.stats[1200 + (k)], t_ - tl);                                        \
+      tl = t_;                                                                         \
+    }                                                                                  \
+  } while (0)
+#define WSTAT(k, v) do { if (P.debug & 16) atomicAdd(&P.stats[1220 + (k)], (unsigned long long)(v)); } while (0)
+#else
+#define RMARK(k) do {} while (0)
+#define WSTAT(k, v) do {} while (0)
+#endif
     // ---- incremental bookkeeping (K2) ----
     // walkers: every marked slot that has no marked slot below it in its chain (chains are disjoint
     // paths of down pointers) recomputes its own cost and every cost above it, bottom-up; below the
@@ -440,21 +498,33 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       _Pragma("unroll 1") for (int k = T.tid; k < nm; k += TPI) {
         const int32_t p = I.mlist[k];
         bool lowest = true;
-        _Pragma("unroll 1") for (int32_t q = I.down[p]; q >= 0; q = I.down[q])
+        _Pragma("unroll 1") for (int32_t q = I.down[p]; q >= 0;) {
+          const int32_t qn = I.down[q];  // issued together with the flag load: one latency per step
+          WSTAT(3, 1);
           if (*(volatile int32_t*)&I.mflag[q]) { lowest = false; break; }
+          q = qn;
+        }
+        WSTAT(0, 1);
         if (!lowest) continue;
+        WSTAT(1, 1);
         int32_t x = p;
         int64_t c = p - I.relay(p) * MC < I.capv[I.relay(p)] ? I.cost_from(p) : INF;
-        for (;;) {
-          I.scost[x] = c;
-          const int32_t u = I.up[x];
+        int32_t u = I.up[x];
+        // software-pipelined: the next up pointer and this hop's link cost are loaded together
+        _Pragma("unroll 1") for (;;) {
           if (u < 0) {
+            I.scost[x] = c;
             if (u == kNone) I.mark_relay(I.relay(x));
             break;
           }
+          const int32_t un = I.up[u];
+          WSTAT(2, 1);
           const int vu = I.relay(u), su = I.dn.div(vu);
-          c = sadd(I.c_link(su, vu - su * n, I.relay(x) - (su + 1) * n), c);
+          const int32_t w = I.tile[((size_t)su * n + (I.relay(x) - (su + 1) * n)) * I.ld + (vu - su * n)];
+          I.scost[x] = c;
+          c = sadd(cst(w), c);
           x = u;
+          u = un;
         }
       }
     };
@@ -466,8 +536,8 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       nr = *(volatile int*)&I.lcnt[1];
       _Pragma("unroll 1") for (int k = T.tid; k < nr; k += TPI) {
         const int v = I.rlist[k];
-        I.summ[v] = I.summarize(v);
-        I.set_adv(v, I.relay_adv(v));
+        I.refresh(v);
+        I.set_adv(v, I.adv_of(v));
       }
     };
     // after the next barrier: empty both lists
@@ -489,7 +559,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         // ---------- first round of the call: every cost, summary and advertisement from scratch
         // (the state may come from a churn, an import or another call) ----------
         _Pragma("unroll 1") for (int k = T.tid; k < Sn * MC; k += TPI) I.mflag[k] = 0;
-        _Pragma("unroll 1") for (int k = T.tid; k < Sn; k += TPI) { I.rflag[k] = 0; I.adv_cost[k] = INF; }
+        _Pragma("unroll 1") for (int k = T.tid; k < Sn; k += TPI) { I.rflag[k] = 0; I.adv_cost[k] = INF; I.first_req[k] = INT_MAX; }
         _Pragma("unroll 1") for (int k = T.tid; k < S * W; k += TPI) I.advm[k] = 0u;
         _Pragma("unroll 1") for (int k = T.tid; k < S; k += TPI) I.advcnt[k] = 0;
         if (T.tid == 0) { I.lcnt[0] = 0; I.lcnt[1] = 0; }
@@ -503,8 +573,8 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           compute_costs<TT>(T, I);  // stage-synchronous back-to-front recursion (ends with a barrier)
         }
         _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
-          I.summ[v] = I.summarize(v);
-          I.set_adv(v, I.relay_adv(v));
+          I.refresh(v);
+          I.set_adv(v, I.adv_of(v));
         }
         T.sync();
       } else {
@@ -516,6 +586,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         T.sync();
         reset_lists(nr);
       }
+      RMARK(0);
       // ---------- R0a candidates: a relay holding an IN and an OUT slot ----------
       if (T.tid == 0) { sh_i32[0] = INT_MAX; sh_i32[1] = 0; }
       int cand = 0;
@@ -523,7 +594,9 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         const uint32_t w = I.summ[v];
         cand |= (w & 63u) != 63u && ((w >> 18) & 1u);
       }
-      if (T.sync_or(cand)) {
+      const int any_cand = T.sync_or(cand);
+      RMARK(1);
+      if (any_cand) {
         // ---------- R0a self-pairing, costs of the round-start state (scost is up to date) ----------
         _Pragma("unroll 1") for (int v = T.tid; v < Sn; v += TPI) {
           const Summ sm{I.summ[v]};
@@ -550,6 +623,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         flush_relays(nm, nr);
         T.sync();
         reset_lists(nr);
+        RMARK(2);
       }
       // ---------- data-node slots ----------
       {
@@ -562,128 +636,178 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         if (anyfree) atomicOr(&sh_i32[1], 1);
       }
       T.sync();
+      RMARK(3);
       const int d_rslot = *(volatile int*)&sh_i32[0];
       const int dsink_free = *(volatile int*)&sh_i32[1];
       // ---------- R1 requests (one per node): argmin over the next stage's advertisers only
       // (the advertiser bitmask, in ascending position: the same lowest-j tie-break as a full scan
       // that skips INF advertisements) ----------
-      _Pragma("unroll 1") for (int rr = T.tid; rr <= Sn; rr += TPI) {
+      // warp-uniform iteration (the warp operations below need every lane); the last warp also
+      // carries the data node (rr == Sn)
+      _Pragma("unroll 1") for (int rb = T.tid - lane; rb <= Sn; rb += TPI) {
+        const int rr = rb + lane;
         int32_t rs = kNone, tg = -2;
-        if (rr == Sn) {  // the data node requests for its lowest unpaired SRC slot
-          if (d_rslot != INT_MAX && *(volatile int32_t*)&I.advcnt[0] > 0) {
-            int64_t bc = INF;
-            _Pragma("unroll 1") for (int w = 0; w < W; ++w) {
-              uint32_t bits = I.advm[w];
-              while (bits) {
-                const int j = w * 32 + __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int64_t dj = cst(I.src[j]), aj = I.adv_cost[j];
-                if (dj == INF || !I.alive[j]) continue;
-                if (dj + aj < bc) { bc = dj + aj; tg = j; }
-              }
-            }
-            if (tg != -2) rs = -2 - d_rslot;
-          }
-        } else if (I.alive[rr]) {
-          const Summ sm{I.summ[rr]};
-          int32_t x = kNone;
-          if (sm.has_in()) x = rr * MC + sm.first_in();                                   // (a)
-          else if (!sm.has_out() && sm.first_free() != 63) x = rr * MC + sm.first_free();  // (b)
-          if (x != kNone) {
-            const int s = I.dn.div(rr), i = rr - s * n;
-            if (s == S - 1) {
-              if (I.snk[i] != kAbsent && dsink_free) tg = -1;
-            } else if (*(volatile int32_t*)&I.advcnt[s + 1] > 0) {
-              int64_t bc = INF;
-              const int32_t* col = I.tile + (size_t)s * n * I.ld + i;  // C[s][v][i], v = 0..n-1
-              const int64_t* av = I.adv_cost + (s + 1) * n;
-              const uint32_t* am = I.advm + (size_t)(s + 1) * W;
-              _Pragma("unroll 1") for (int w = 0; w < W; ++w) {
-                uint32_t bits = am[w];
-                while (bits) {
-                  const int jj = w * 32 + __ffs(bits) - 1;
-                  bits &= bits - 1;
-                  const int32_t c = col[(size_t)jj * I.ld];
-                  if (c == kAbsent) continue;
-                  const int64_t aj = av[jj];
-                  if (c + aj < bc) { bc = c + aj; tg = (s + 1) * n + jj; }
-                }
-              }
-            }
-            if (tg != -2) rs = x;
+        // requester slot: (a) the lowest IN slot, (b) the lowest FREE slot of a stable relay
+        int32_t x = kNone;
+        int s = 0, i = 0;
+        if (rr < Sn) {
+          s = I.dn.div(rr);
+          i = rr - s * n;
+          if (I.alive[rr]) {
+            const Summ sm{I.summ[rr]};
+            if (sm.has_in()) x = rr * MC + sm.first_in();                                   // (a)
+            else if (!sm.has_out() && sm.first_free() != 63) x = rr * MC + sm.first_free();  // (b)
           }
         }
-        I.req_slot[rr] = rs;
-        I.req_target[rr] = tg;
+        const bool want = x != kNone && s < S - 1;
+        // a warp whose lanes all sit in one stage walks that stage's advertisers together
+        // (coalesced link loads, 4 advertisers in flight); otherwise every lane walks alone
+        const int s0 = __shfl_sync(0xffffffffu, s, 0);
+        const bool uni = __all_sync(0xffffffffu, rr < Sn && s == s0);
+        const bool anyw = __any_sync(0xffffffffu, want);
+        int64_t bc = INF;
+        int tgw = -2;
+        if (uni) {
+          if (anyw && s0 < S - 1 && *(volatile int32_t*)&I.advcnt[s0 + 1] > 0) {
+            const int32_t* col = I.tile + (size_t)s0 * n * I.ld + i;  // C[s][v][i], v = 0..n-1
+            const int64_t* av = I.adv_cost + (s0 + 1) * n;
+            const uint32_t* am = I.advm + (size_t)(s0 + 1) * W;
+            _Pragma("unroll 1") for (int w = 0; w < W; ++w) {
+              uint32_t bits = am[w];
+              while (bits) {
+                int jv[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  jv[t] = bits ? w * 32 + __ffs(bits) - 1 : -1;
+                  bits &= bits - 1;
+                }
+                int32_t cv[4];
+                int64_t avv[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                  if (jv[t] >= 0) { cv[t] = col[(size_t)jv[t] * I.ld]; avv[t] = av[jv[t]]; }
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                  if (jv[t] >= 0 && cv[t] != kAbsent && cv[t] + avv[t] < bc) { bc = cv[t] + avv[t]; tgw = (s0 + 1) * n + jv[t]; }
+              }
+            }
+          }
+        } else if (want && *(volatile int32_t*)&I.advcnt[s + 1] > 0) {
+          const int32_t* col = I.tile + (size_t)s * n * I.ld + i;
+          const int64_t* av = I.adv_cost + (s + 1) * n;
+          const uint32_t* am = I.advm + (size_t)(s + 1) * W;
+          _Pragma("unroll 1") for (int w = 0; w < W; ++w) {
+            uint32_t bits = am[w];
+            while (bits) {
+              const int jj = w * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int32_t c = col[(size_t)jj * I.ld];
+              if (c == kAbsent) continue;
+              const int64_t aj = av[jj];
+              if (c + aj < bc) { bc = c + aj; tgw = (s + 1) * n + jj; }
+            }
+          }
+        }
+        if (want) tg = tgw;
+        else if (x != kNone && s == S - 1 && I.snk[i] != kAbsent && dsink_free) tg = -1;
+        if (tg != -2) rs = x;
+        if (rr == Sn && d_rslot != INT_MAX && *(volatile int32_t*)&I.advcnt[0] > 0) {
+          // the data node requests for its lowest unpaired SRC slot (stage-0 advertisers)
+          int64_t bd = INF;
+          _Pragma("unroll 1") for (int w = 0; w < W; ++w) {
+            uint32_t bits = I.advm[w];
+            while (bits) {
+              const int j = w * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              const int64_t dj = cst(I.src[j]), aj = I.adv_cost[j];
+              if (dj == INF || !I.alive[j]) continue;
+              if (dj + aj < bd) { bd = dj + aj; tg = j; }
+            }
+          }
+          if (tg != -2) rs = -2 - d_rslot;
+        }
+        if (rr <= Sn) {
+          I.req_slot[rr] = rs;
+          I.req_target[rr] = tg;
+          if (tg >= 0) atomicMin(&I.first_req[tg], rr);
+        }
       }
       T.sync();
+      RMARK(4);
       // ---------- R2 + R3: each target serves its requesters in ascending gid and commits ----------
       // (a target's eligibility only reads its own OUT slots, which only it modifies; requester
       // slots are IN/FREE slots written by exactly one target, so the fused commit equals
-      // "all grants on the pre-R3 state, then all commits").  One warp per advertiser: the
-      // requesters of its stage are scanned 32 at a time with a ballot, in ascending gid.
-      _Pragma("unroll 1") for (int j = lane_w; j < Sn; j += nwarps) {
-        const int64_t ac = I.adv_cost[j];
-        if (ac == INF) continue;  // no OUT slot: nothing to grant (warp-uniform)
-        const int s = I.dn.div(j);
-        const int c = I.capv[j];
-        int cur = 0;  // lane 0's cursor over j's slots
-        auto next_slot = [&]() -> int {
-          while (cur < c) {
-            const int p = j * MC + cur++;
-            if (I.st(p) == ST_OUT && I.scost[p] == ac) return p;
+      // "all grants on the pre-R3 state, then all commits").  One thread per advertiser (the
+      // bitmask): with one eligible slot -- the usual case -- the lowest-gid requester (first_req,
+      // an atomicMin of R1) takes it; with several, the requesters are walked in gid order.
+      auto commit_grant = [&](int qq, int32_t pslot) {
+        const int32_t rs = I.req_slot[qq];
+        I.down[rs] = pslot;
+        I.up[pslot] = rs;
+        I.deny[qq] = 0;
+        I.mark_slot(rs);
+        I.mark_relay(qq);
+        changed = 1;
+      };
+      _Pragma("unroll 1") for (int w = T.tid; w < S * W; w += TPI) {
+        uint32_t bits = I.advm[w];
+        const int s = w / W, wb = (w - s * W) * 32;
+        while (bits) {
+          const int i = wb + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int j = s * n + i;
+          const int q1 = I.first_req[j];
+          if (q1 == INT_MAX) continue;  // nobody asked
+          I.first_req[j] = INT_MAX;     // ready for the next round
+          const int64_t ac = I.adv_cost[j];
+          uint32_t el = 0;  // eligible: OUT slots with cost == adv(j), in slot order
+          for (uint32_t t = I.omask[j]; t; t &= t - 1) {
+            const int jj = __ffs(t) - 1;
+            if (I.scost[j * MC + jj] == ac) el |= 1u << jj;
           }
-          return -1;
-        };
-        if (s == 0) {  // the data node is the only requester of stage-0 relays
-          if (lane == 0 && I.req_target[Sn] == j) {
-            const int p = next_slot();
-            if (p >= 0) {
-              const int32_t rs = I.req_slot[Sn];
-              I.src_down[-2 - rs] = p;
-              I.up[p] = rs;
-              I.mark_relay(j);
-              changed = 1;
+          if (!el) continue;
+          I.mark_relay(j);
+          if (s == 0) {  // the data node is the only requester of stage-0 relays
+            const int32_t pslot = j * MC + __ffs(el) - 1;
+            const int32_t rs = I.req_slot[Sn];
+            I.src_down[-2 - rs] = pslot;
+            I.up[pslot] = rs;
+            changed = 1;
+            continue;
+          }
+          if (__popc(el) == 1) {
+            commit_grant(q1, j * MC + __ffs(el) - 1);
+          } else {
+            _Pragma("unroll 1") for (int qq = q1; qq < s * n && el; ++qq) {
+              if (I.req_target[qq] != j) continue;
+              commit_grant(qq, j * MC + __ffs(el) - 1);
+              el &= el - 1;
             }
           }
-          continue;
         }
-        bool done = false;
-        _Pragma("unroll 1") for (int q0 = (s - 1) * n; q0 < s * n && !done; q0 += 32) {
-          const int q = q0 + lane;
-          uint32_t m = __ballot_sync(0xffffffffu, q < s * n && I.req_target[q] == j);
-          if (lane == 0) {
-            while (m) {
-              const int qq = q0 + __ffs(m) - 1;
-              m &= m - 1;
-              const int p = next_slot();
-              if (p < 0) { done = true; break; }
-              const int32_t rs = I.req_slot[qq];
-              I.down[rs] = p;
-              I.up[p] = rs;
-              I.deny[qq] = 0;
-              I.mark_slot(rs);
-              I.mark_relay(qq);
-              changed = 1;
-            }
-          }
-          done = __shfl_sync(0xffffffffu, done, 0);
-        }
-        if (lane == 0 && cur > 0) I.mark_relay(j);
       }
-      // D-sink: free SNK slots in index order to last-stage requesters in gid order (last warp)
+      // D-sink: free SNK slots in index order to last-stage requesters in gid order (last warp:
+      // the requesters and the free SNK slots are both taken 32 at a time with ballots)
       if (dsink_free && lane_w == nwarps - 1) {
-        int k = 0;  // lane 0's cursor over SNK slots
+        int next = 0, fcb = 0;
+        uint32_t fm = 0;
         bool full = false;
         _Pragma("unroll 1") for (int q0 = (S - 1) * n; q0 < Sn && !full; q0 += 32) {
           const int q = q0 + lane;
           uint32_t m = __ballot_sync(0xffffffffu, q < Sn && I.req_target[q] == -1);
-          if (lane == 0) {
-            while (m) {
-              const int qq = q0 + __ffs(m) - 1;
-              m &= m - 1;
-              while (k < M && I.snk_up[k] != kNone) ++k;
-              if (k >= M) { full = true; break; }
+          while (m) {
+            const int qq = q0 + __ffs(m) - 1;
+            m &= m - 1;
+            while (fm == 0u && next < M) {
+              const int k = next + lane;
+              fm = __ballot_sync(0xffffffffu, k < M && I.snk_up[k] == kNone);
+              fcb = next;
+              next += 32;
+            }
+            if (fm == 0u) { full = true; break; }
+            const int k = fcb + __ffs(fm) - 1;
+            fm &= fm - 1;
+            if (lane == 0) {
               const int32_t rs = I.req_slot[qq];
               I.down[rs] = -2 - k;
               I.snk_up[k] = rs;
@@ -691,19 +815,19 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
               I.mark_slot(rs);
               I.mark_relay(qq);
               changed = 1;
-              ++k;
             }
           }
-          full = __shfl_sync(0xffffffffu, full, 0);
         }
       }
       T.sync();
+      RMARK(5);
       // ---------- summaries of the relays R3 touched (R4 reads the post-R3 state) ----------
       {
         const int nr = *(volatile int*)&I.lcnt[1];
-        _Pragma("unroll 1") for (int k = T.tid; k < nr; k += TPI) I.summ[I.rlist[k]] = I.summarize(I.rlist[k]);
+        _Pragma("unroll 1") for (int k = T.tid; k < nr; k += TPI) I.refresh(I.rlist[k]);
       }
       T.sync();
+      RMARK(6);
       }  // !prev_quiet
       // ---------- R4 proposals by idle relays (post-R3 state) + R5 reservations ----------
       _Pragma("unroll 1") for (int p = T.tid; p < Sn; p += TPI) {
@@ -733,7 +857,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
               int64_t delta = 0;
               bool ok = false;
               if (sm.first_free() != 63 && !sm.has_out()) {  // Request Redirect
-                y = I.nth_paired(q, (int)pick(I.h(p, 2), (uint32_t)nq));
+                y = I.nth_paired_m(q, (int)pick(I.h(p, 2), (uint32_t)nq));
                 const int a = I.up[y] >= 0 ? I.relay(I.up[y]) : -1;
                 const int c = I.down[y] >= 0 ? I.relay(I.down[y]) : -1;
                 const int64_t dax = I.d(a, p), dxc = I.d(p, c), dab = I.d(a, q), dbc = I.d(q, c);
@@ -745,8 +869,8 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
                   ok = true;
                 }
               } else if (sm.npaired() > 0) {  // Request Change
-                x = I.nth_paired(p, (int)pick(I.h(p, 1), (uint32_t)sm.npaired()));
-                y = I.nth_paired(q, (int)pick(I.h(p, 2), (uint32_t)nq));
+                x = I.nth_paired_m(p, (int)pick(I.h(p, 1), (uint32_t)sm.npaired()));
+                y = I.nth_paired_m(q, (int)pick(I.h(p, 2), (uint32_t)nq));
                 const int j1 = I.down[x] >= 0 ? I.relay(I.down[x]) : -1;
                 const int j2 = I.down[y] >= 0 ? I.relay(I.down[y]) : -1;
                 if (j1 != j2) {
@@ -789,6 +913,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         }
       }
       T.sync();
+      RMARK(7);
       // ---------- R6 commit the proposals that hold every slot they touch ----------
       _Pragma("unroll 1") for (int p = T.tid; p < Sn; p += TPI) {
         const int kind = I.prop[p * 4 + 0];
@@ -838,6 +963,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         changed = 1;
       }
       T.sync();
+      RMARK(8);
       _Pragma("unroll 1") for (int p = T.tid; p < Sn; p += TPI) {  // release the reservations for the next round
         if (I.prop[p * 4 + 0] == K_NONE) continue;
         _Pragma("unroll 1") for (int q = 0; q < 4; ++q) {
@@ -847,6 +973,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       }
       // ---------- R7 ----------
       const int any = T.sync_or(changed);
+      RMARK(9);
       quiet = any ? 0 : quiet + 1;
       prev_quiet = !any;
       round += 1;
@@ -881,6 +1008,8 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
       ++r;
       if (quiet >= P.W) break;
     }
+#undef RMARK
+#undef WSTAT
     if (o.digests)
       _Pragma("unroll 1") for (int k = r + T.tid; k < o.max_rounds; k += TPI) o.digests[(size_t)b * o.max_rounds + k] = 0;
     // ---------- results: complete SRC -> SNK chains and dangling outflows ----------

@@ -27,6 +27,8 @@ ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 ev[0].record(fl.stream)
 r0 = fl.decentralized_rounds(max(a.skip, 1))
 ev[1].record(fl.stream)
+torch.cuda.synchronize()
+raw0 = fl.stats(raw=True)
 r1 = fl.decentralized_rounds(a.rounds)
 ev[2].record(fl.stream)
 torch.cuda.synchronize()
@@ -34,3 +36,14 @@ t0, t1 = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
 print(json.dumps({"skip_rounds": max(a.skip, 1), "skip_ms": t0, "rounds": r1.rounds_run.tolist(), "ms": t1,
                   "ms_per_round": t1 / max(1, int(r1.rounds_run.max())), "F_dec": r1.dec_flow.tolist(),
                   "cost_dec": r1.dec_cost.tolist(), "dangling": r1.dangling.tolist()}))
+if int(os.environ.get("GWTF_DEBUG_FLAGS", "0")) & 16:  # dev build: rounds phase cycles (leader thread)
+    raw = fl.stats(raw=True) - raw0  # the second launch only
+    names = ["start:walk+flush", "r0a-vote", "r0a", "d-scan", "R1", "R2R3", "summ", "R4R5", "R6", "R7"]
+    cyc = raw[1200:1210].astype(float)
+    tot = cyc.sum() or 1.0
+    print("rounds phase cycles (second launch):")
+    for nm, c in zip(names, cyc):
+        print(f"  {nm:18s} {c:14.0f} {100 * c / tot:5.1f}%")
+    w = raw[1220:1224]
+    R = max(1, int(r1.rounds_run.max()))
+    print(f"per round (all instances): marks {w[0] / R:.0f}, lowest walkers {w[1] / R:.0f}, up steps {w[2] / R:.0f}, down steps {w[3] / R:.0f}")
