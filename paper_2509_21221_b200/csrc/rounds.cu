@@ -88,6 +88,7 @@ struct Inst {
   uint32_t* pmask;  // per relay: bit j = slot j is PAIRED (max_cap <= 32), maintained with summ
   uint32_t* omask;  // per relay: bit j = slot j is OUT
   int32_t* first_req;  // per target relay: lowest requester gid of the round (INT_MAX: none)
+  int32_t* lcd;        // per slot: cost of the link to its down pointer's node (kAbsent: none / absent)
   int W;
   uint64_t *pkey, *res;
   const int32_t *tile, *src, *snk;
@@ -195,7 +196,7 @@ struct Inst {
   __device__ void refresh(int v) const {
     uint32_t fi = 63, ff = 63, np = 0, ho = 0, pm = 0, om = 0;
     const int c = capv[v], base = v * MC;
-    _Pragma("unroll 1") for (int j = 0; j < c; ++j) {
+    _Pragma("unroll 4") for (int j = 0; j < c; ++j) {  // 4 slots' loads in flight
       const int t = st(base + j);
       if (t == ST_IN && fi == 63) fi = j;
       if (t == ST_FREE && ff == 63) ff = j;
@@ -214,8 +215,20 @@ struct Inst {
     for (; q > 0; --q) m &= m - 1;
     return m ? v * MC + __ffs(m) - 1 : -1;
   }
+  // link cost from slot p's node to its down pointer's node (an SNK pointer: the sink cost)
+  __device__ int32_t link_down(int32_t p) const {
+    const int32_t d1 = down[p];
+    if (d1 == kNone) return kAbsent;
+    const int v = relay(p), s = dn.div(v), i = v - s * n;
+    if (d1 <= -2) return snk[i];
+    return tile[((size_t)s * n + (relay(d1) - (s + 1) * n)) * ld + i];
+  }
+  // a slot whose down pointer just changed: its link cost is refreshed and it is listed for the
+  // next cost update (walk_marks)
   __device__ void mark_slot(int32_t p) const {
-    if (p >= 0 && atomicExch(&mflag[p], 1) == 0) mlist[atomicAdd(&lcnt[0], 1)] = p;
+    if (p < 0) return;
+    lcd[p] = link_down(p);
+    if (atomicExch(&mflag[p], 1) == 0) mlist[atomicAdd(&lcnt[0], 1)] = p;
   }
   __device__ void mark_relay(int v) const {
     if (atomicExch(&rflag[v], 1) == 0) rlist[atomicAdd(&lcnt[1], 1)] = v;
@@ -224,9 +237,7 @@ struct Inst {
   __device__ int64_t cost_from(int32_t p) const {
     const int32_t d1 = down[p];
     if (d1 == kNone) return INF;
-    const int v = relay(p), s = dn.div(v), i = v - s * n;
-    if (d1 <= -2) return cst(snk[i]);
-    return sadd(c_link(s, i, relay(d1) - (s + 1) * n), scost[d1]);
+    return d1 <= -2 ? cst(lcd[p]) : sadd(cst(lcd[p]), scost[d1]);
   }
   // the advertisement of v and its bit in the stage's advertiser mask (count kept in advcnt)
   __device__ void set_adv(int v, int64_t a) const {
@@ -307,7 +318,7 @@ __host__ __device__ inline bool rounds_tile_in_smem(const Problem& P) {
 }
 struct RoundsLayout {
   size_t res, scost, adv_cost, pkey, up, down, src_down, snk_up, kacc, deny, req_slot, req_target, grant, prop,
-      ptouch, capv, summ, mflag, mlist, rflag, rlist, advm, advcnt, pmask, omask, first_req, lcnt, tile, mbar, cells, total;
+      ptouch, capv, summ, mflag, mlist, rflag, rlist, advm, advcnt, pmask, omask, first_req, lcd, lcnt, tile, mbar, cells, total;
 };
 // smem: everything of one instance; otherwise only the per-instance scratch (the state
 // arrays then live in the handle's global buffers)
@@ -341,6 +352,7 @@ __host__ __device__ inline RoundsLayout rounds_layout(const Problem& P, bool sme
   L.pmask = o; o += al16r(Sn * 4);
   L.omask = o; o += al16r(Sn * 4);
   L.first_req = o; o += al16r(Sn * 4);
+  L.lcd = o; o += al16r(ns * 4);
   L.lcnt = o; o += 16;
   L.tile = o; if (smem && rounds_tile_in_smem(P)) o += al16r((size_t)(P.S > 1 ? P.S - 1 : 0) * P.n * P.ld * 4);
   L.mbar = o; o += 16;
@@ -422,6 +434,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     I.pmask = (uint32_t*)(base + Lr.pmask);
     I.omask = (uint32_t*)(base + Lr.omask);
     I.first_req = (int32_t*)(base + Lr.first_req);
+    I.lcd = (int32_t*)(base + Lr.lcd);
     I.W = (n + 31) / 32;
     const int M = I.M;
     const int32_t* cap_g = P.cap + (size_t)b * Sn;
@@ -519,8 +532,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
           }
           const int32_t un = I.up[u];
           WSTAT(2, 1);
-          const int vu = I.relay(u), su = I.dn.div(vu);
-          const int32_t w = I.tile[((size_t)su * n + (I.relay(x) - (su + 1) * n)) * I.ld + (vu - su * n)];
+          const int32_t w = I.lcd[u];  // u's down link is the link u -> x
           I.scost[x] = c;
           c = sadd(cst(w), c);
           x = u;
@@ -563,6 +575,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
         _Pragma("unroll 1") for (int k = T.tid; k < S * W; k += TPI) I.advm[k] = 0u;
         _Pragma("unroll 1") for (int k = T.tid; k < S; k += TPI) I.advcnt[k] = 0;
         if (T.tid == 0) { I.lcnt[0] = 0; I.lcnt[1] = 0; }
+        _Pragma("unroll 1") for (int k = T.tid; k < Sn * MC; k += TPI) I.lcd[k] = I.link_down(k);
         if (cost_mode == 1) {
           _Pragma("unroll 1") for (int t = T.tid; t < Sn * MC; t += TPI) I.slot_cost(t);
           T.sync();
@@ -860,7 +873,9 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
                 y = I.nth_paired_m(q, (int)pick(I.h(p, 2), (uint32_t)nq));
                 const int a = I.up[y] >= 0 ? I.relay(I.up[y]) : -1;
                 const int c = I.down[y] >= 0 ? I.relay(I.down[y]) : -1;
-                const int64_t dax = I.d(a, p), dxc = I.d(p, c), dab = I.d(a, q), dbc = I.d(q, c);
+                // the existing links a -> q and q -> c are y's up / down links (stored costs)
+                const int64_t dax = I.d(a, p), dxc = I.d(p, c);
+                const int64_t dab = I.up[y] >= 0 ? cst(I.lcd[I.up[y]]) : I.d(a, q), dbc = cst(I.lcd[y]);
                 if (dax != INF && dxc != INF && dab != INF && dbc != INF) {
                   delta = P.objective == 0 ? (dax + dxc) - (dab + dbc) : max(dax, dxc) - max(dab, dbc);
                   kind = K_REDIRECT;
@@ -874,7 +889,8 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
                 const int j1 = I.down[x] >= 0 ? I.relay(I.down[x]) : -1;
                 const int j2 = I.down[y] >= 0 ? I.relay(I.down[y]) : -1;
                 if (j1 != j2) {
-                  const int64_t a1 = I.d(p, j2), a2 = I.d(q, j1), b1 = I.d(p, j1), b2 = I.d(q, j2);
+                  // p -> j1 and q -> j2 are the existing links of x and y (stored costs)
+                  const int64_t a1 = I.d(p, j2), a2 = I.d(q, j1), b1 = cst(I.lcd[x]), b2 = cst(I.lcd[y]);
                   if (a1 != INF && a2 != INF && b1 != INF && b2 != INF) {
                     delta = P.objective == 0 ? (a1 + a2) - (b1 + b2) : max(a1, a2) - max(b1, b2);
                     kind = K_CHANGE;
