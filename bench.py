@@ -1,14 +1,16 @@
 """bench.py -- instances/sec of the GWTF routing hot path (BASELINE.json metric) on N B200s.
 
-One step = one pass of the whole hot path over this GPU's batch of the churn protocol
-(SURVEY.md 8(d)): apply_churn (crash/rejoin masks) -> cold exact SSP solve on the masked
-graph -> decentralized repair rounds to steady state -> (N>1) NCCL all_gather of the
-per-instance results.  The pre-churn converged state is built once (untimed) and restored
-before every step (untimed, like the L2 flush).  Workload: configs[1] of BASELINE.json
-(GPT-like 300M: 6 stages x 16 clients, 64 microbatches, 10% churn), B instances per GPU
-(weak scaling).
+Headline workload (N=1 line): the largest single-GPU configuration of BASELINE.json, `stress`:
+8 instances per GPU of 64 stages x 1,024 clients with dense inter-stage links, M = 4,096
+microbatches, caps U{1..20}, costs U{1..100}.  One step = one pass of the whole
+hot path over this GPU's batch: the cold exact SSP solve (solve_batch) and the decentralized rounds
+from the empty state to steady state or max_rounds = 120 + 2M (decentralized_rounds) -- issued
+together through gwtf_flow_solve_and_rounds (the two read the same graph and write disjoint
+state, and their cluster grids fit side by side on the 148 SMs) -- then, for N > 1, the NCCL
+gather of the per-instance results.  The churn-protocol configs (gpt, llama, churn) and tiny are
+reported beside it (`configs`), each with SSP-only, rounds-only and combined rates.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config gpt]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config stress|gpt|...]
   torchrun --nproc-per-node N bench.py --gpus N ...
 """
 from __future__ import annotations
@@ -16,6 +18,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -32,17 +35,17 @@ import gen  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gwtf", choices=["gwtf", "reference"])
-    ap.add_argument("--config", default="gpt")
+    ap.add_argument("--config", default="stress")
     ap.add_argument("--batch", type=int, default=0, help="instances per GPU (default: the config's B)")
-    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle instances for cpu_baseline (0 = auto)")
+    ap.add_argument("--serial", action="store_true", help="solve then rounds on one stream (no overlap)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline and stress tier (profiling runs)")
-    ap.add_argument("--no-stress-tier", action="store_true", help="skip the stress-config exact-solve measurement")
-    ap.add_argument("--no-addition", action="store_true", help="skip the node-addition optimizer measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the secondary config lines")
+    ap.add_argument("--no-extras", action="store_true", help="skip node addition / flow quality / multi source / warm")
+    ap.add_argument("--quick", action="store_true", help="headline only (profiling runs)")
     return ap.parse_args()
 
 
@@ -52,16 +55,19 @@ def workload_name(cfg):
             + f", churn={cfg.churn}")
 
 
+def arcs_E(cfg):
+    return (cfg.S - 1) * cfg.n * cfg.n + 2 * cfg.n
+
+
 def algorithmic_bytes_ssp(cfg, A_total):
     """an SSP shortest-path step examines every forward arc once:
-    bytes/augmentation = E x sizeof(cost), E = (S-1) n^2 + 2n, int32 costs."""
-    E = (cfg.S - 1) * cfg.n * cfg.n + 2 * cfg.n
-    return float(A_total) * E * 4
+    bytes/augmentation = E x sizeof(cost), E = (S-1) n^2 + 2n, the C-ABI's int32 costs."""
+    return float(A_total) * arcs_E(cfg) * 4
 
 
 def load_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture of this bench
-    command (profiles/<round>/traffic.json, written by scripts/ncu_traffic.py), else None."""
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (the newest
+    profiles/r*/traffic.json holding it, written by scripts/ncu_traffic.py), else None."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
         try:
@@ -74,51 +80,116 @@ def load_traffic(kernel):
     return None, None
 
 
-def stress_tier(dev):
-    """The HBM-streaming tier on the stress config (SURVEY.md 8(d) tier G): 8 instances of 64
-    stages x 1,024 clients, M = 4,096, one cold exact solve through the cluster-tier kernel.
-    Algorithmic bytes = sum_b A_b x E x 4 (E = (S-1) n^2 + 2n int32 arc costs per augmentation)."""
-    import torch
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
 
-    from paper_2509_21221_b200 import Flow
-    from tests import harness
-    cfg = gen.CONFIGS["stress"]
-    bt, src, snk, link = harness.device_inputs(cfg, 0, cfg.B, device=dev)
-    fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0)
-    del link
+
+class Setup:
+    """One config's handle with its step inputs resident in HBM: for the churn-protocol configs the
+    pre-churn converged state and the churn events (SURVEY.md 8(d) protocol); for the cold configs
+    the empty state.  snapshot() holds the state every step starts from."""
+
+    def __init__(self, cfg, dev, inst0, B):
+        import torch
+
+        from paper_2509_21221_b200 import Flow
+        from tests import harness
+        self.cfg, self.B, self.inst0 = cfg, B, inst0
+        bt, src, snk, link = harness.device_inputs(cfg, inst0, B, device=dev)
+        self.fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0,
+                       inst_base=inst0)
+        del link
+        self.an = self.upd = None
+        if cfg.churn != "none":
+            self.fl.decentralized_rounds(cfg.max_rounds)  # untimed: the pre-churn converged state
+            if cfg.churn == "random":
+                self.an, self.upd = harness.churn_inputs(cfg, inst0, bt.alive, device=dev)
+            else:
+                st = self.fl.export_round_state()
+                self.an = torch.from_numpy(gen.llama_victims(st["up"].cpu().numpy(), st["down"].cpu().numpy(),
+                                                             bt.alive.cpu().numpy(), gen.victim_draws(cfg, inst0, B))).to(dev)
+        self.fl.snapshot()
+        self.sol = self.fl.solve_batch()
+        self.rr = self.fl.decentralized_rounds(cfg.max_rounds)
+        torch.cuda.synchronize()
+
+    def churn(self):
+        if self.an is not None or self.upd is not None:
+            self.fl.apply_churn(self.an, self.upd)
+
+
+def time_loop(fl, steps, warmup, prep, body, flush, world=1, clocks=None):
+    """W untimed + K timed steps; each timed step bracketed by a barrier and synchronizes, CUDA
+    events on the handle's stream; prep() (restore, L2 flush) is untimed."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        prep()
+        body()
     torch.cuda.synchronize()
-    fl.set_profiling(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(fl.stream)
-    sol = fl.solve_batch()
-    ev1.record(fl.stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    kt = fl.kernel_times()
-    ev0.record(fl.stream)
-    rr = fl.decentralized_rounds(cfg.max_rounds)  # cold, to steady state (W = 5) or max_rounds
-    ev1.record(fl.stream)
-    torch.cuda.synchronize()
-    rms = ev0.elapsed_time(ev1)
-    fl.set_profiling(False)
-    A = int(sol.augmentations.sum().item())
-    alg = algorithmic_bytes_ssp(cfg, A)
-    kname = "ssp_cluster_kernel" if "ssp_cluster_kernel" in kt else max(kt, key=lambda k: kt[k][0])
-    kms = kt[kname][0]
-    peak, peak_src = load_peaks()
-    tr, tsrc = load_traffic("stress:" + kname)
-    # the capture ran a supply-capped solve: its DRAM bytes per augmentation x this launch's A
-    traffic = tr["dram_bytes_per_aug"] * A if tr and "dram_bytes_per_aug" in tr else None
-    out = {"workload": workload_name(cfg), "instances": cfg.B, "solve_ms": ms, "rounds_ms": rms,
-           "instances_per_s": cfg.B / ((ms + rms) / 1e3), "ssp_instances_per_s": cfg.B / (ms / 1e3),
-           "rounds_instances_per_s": cfg.B / (rms / 1e3), "augmentations": A,
-           "rounds_run": [int(x) for x in rr.rounds_run.tolist()], "max_rounds": cfg.max_rounds,
-           "F": int(sol.flow_value.sum().item()), "cost": int(sol.total_cost.sum().item()),
-           "F_dec": int(rr.dec_flow.sum().item()), "cost_dec": int(rr.dec_cost.sum().item()),
-           "status_ok": bool((sol.status == 0).all().item()),
-           "roofline": {"kernel": kname, "bound": "hbm", "achieved": alg / (kms / 1e3) / 1e9, "peak": peak,
-                        "unit": "GB/s", "frac": alg / (kms / 1e3) / 1e9 / peak, "peak_source": peak_src,
-                        "algorithmic_bytes_per_launch": alg, "traffic": traffic, "traffic_source": tsrc}}
+    total = 0.0
+    for _ in range(steps):
+        prep()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(fl.stream)
+        body()
+        ev1.record(fl.stream)
+        torch.cuda.synchronize()
+        total += ev0.elapsed_time(ev1)
+    return total
+
+
+
+def config_rates(name, dev, steps=3, warmup=3):
+    """A secondary config on this GPU (SURVEY.md 8(d) "SSP-only, rounds-only and combined rates"):
+    each timed step restores the step's start state (untimed), applies the churn events (timed in
+    the SSP-only and the combined step), then runs the cold solve, the rounds, or both."""
+    import torch
+    cfg = gen.CONFIGS[name]
+    su = Setup(cfg, dev, 0, cfg.B)
+    fl, mr = su.fl, cfg.max_rounds
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def prep():
+        fl.restore()
+        flush.random_(0, 255)
+
+    def ssp():
+        su.churn()
+        fl.solve_batch(out=su.sol)
+
+    def rounds():
+        fl.decentralized_rounds(mr, out=su.rr)
+
+    def comb():
+        su.churn()
+        fl.solve_batch(out=su.sol)
+        fl.decentralized_rounds(mr, out=su.rr)
+
+    t_s = time_loop(fl, steps, warmup, prep, ssp, flush)
+
+    def prep_r():  # the rounds-only step starts after the churn (applied untimed)
+        prep()
+        su.churn()
+    t_r = time_loop(fl, steps, warmup, prep_r, rounds, flush)
+    t_c = time_loop(fl, steps, warmup, prep, comb, flush)
+    B = cfg.B
+    out = {"workload": workload_name(cfg), "instances": B, "max_rounds": mr,
+           "ssp_instances_per_s": B * steps / (t_s / 1e3), "rounds_instances_per_s": B * steps / (t_r / 1e3),
+           "combined_instances_per_s": B * steps / (t_c / 1e3), "ms_per_step": t_c / steps,
+           "augmentations_mean": float(su.sol.augmentations.double().mean()),
+           "rounds_mean": float(su.rr.rounds_run.double().mean()),
+           "F_mean": float(su.sol.flow_value.double().mean()), "F_dec_mean": float(su.rr.dec_flow.double().mean())}
     fl.close()
     return out
 
@@ -192,56 +263,6 @@ def flow_quality(dev, B=256):
                      "gwtf_vs_swarm_improvement_mean": float(imp.mean()) if imp.numel() else None,
                      "gwtf_vs_swarm_improvement_max": float(imp.max()) if imp.numel() else None,
                      "same_flow_instances": int(same.sum())}
-        fl.close()
-    return out
-
-
-def other_configs(dev, steps=5, warmup=3):
-    """The other churn-protocol configs of SURVEY.md 8(d) on this GPU, same step and timing as the
-    main line (device events, L2 flushed, restore untimed): tiny (cold, no churn), llama (victim
-    crash), churn (random crash/rejoin + link drops)."""
-    import torch
-
-    from paper_2509_21221_b200 import Flow
-    from tests import harness
-    out = {}
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    for name in ("tiny", "llama", "churn"):
-        cfg = gen.CONFIGS[name]
-        B, mr = cfg.B, cfg.max_rounds
-        bt, src, snk, link = harness.device_inputs(cfg, 0, B, device=dev)
-        fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0)
-        an = upd = None
-        if cfg.churn != "none":
-            fl.decentralized_rounds(mr)
-            if cfg.churn == "random":
-                an, upd = harness.churn_inputs(cfg, 0, bt.alive, device=dev)
-            else:
-                st = fl.export_round_state()
-                an = torch.from_numpy(gen.llama_victims(st["up"].cpu().numpy(), st["down"].cpu().numpy(),
-                                                        bt.alive.cpu().numpy(), gen.victim_draws(cfg, 0, B))).to(dev)
-        fl.snapshot()
-        sol = fl.solve_batch()
-        rr = fl.decentralized_rounds(mr)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        total = 0.0
-        for it in range(warmup + steps):
-            fl.restore()
-            flush.random_(0, 255)
-            torch.cuda.synchronize()
-            ev0.record(fl.stream)
-            if an is not None or upd is not None:
-                fl.apply_churn(an, upd)
-            fl.solve_batch(out=sol)
-            fl.decentralized_rounds(mr, out=rr)
-            ev1.record(fl.stream)
-            torch.cuda.synchronize()
-            if it >= warmup:
-                total += ev0.elapsed_time(ev1)
-        out[name] = {"workload": workload_name(cfg), "instances": B, "ms_per_step": total / steps,
-                     "instances_per_s": B * steps / (total / 1e3),
-                     "augmentations_mean": float(sol.augmentations.double().mean()),
-                     "rounds_mean": float(rr.rounds_run.double().mean())}
         fl.close()
     return out
 
@@ -389,47 +410,185 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(cfg, target_s=15.0, inst0=0):
-    """The oracle (as it stands) on the host cores, on a bounded sample of the same workload,
-    sized for about target_s seconds of CPU work (calibrated on a small first sample)."""
+
+def oracle_stress_sample(cfg, ninst, ssp_augs=2, nrounds=3, threads=None, inst0=0):
+    """The oracle (as it stands) on a bounded sample of the stress workload, one instance per host
+    thread: the canonical SSP with the supply capped at `ssp_augs` (the first augmentations of the
+    full solve: same graph, same Dijkstra over every arc) and `nrounds` decentralized rounds from the
+    empty state.  Returns per-instance seconds per augmentation and per round (medians)."""
+    import oracle
+    from tests import harness
+    threads = threads or os.cpu_count() or 1
+    ninst = max(1, min(ninst, threads))
+    res = [None] * ninst
+
+    def work(k):
+        bt, src, snk, link = harness.host_inputs(cfg, inst0 + k, 1)
+        I = oracle.instance_from_batch(bt, 0, link[0], src[0], snk[0])
+        Ic = oracle.Instance(I.S, I.n, I.max_cap, min(I.M, ssp_augs), I.cap, I.src, I.snk, I.link, I.alive)
+        t = time.perf_counter()
+        s = oracle.ssp(Ic)
+        t_ssp = time.perf_counter() - t
+        R = oracle.Rounds(I, seed=0, inst_id=inst0 + k)
+        t = time.perf_counter()
+        R.run(nrounds)
+        t_r = time.perf_counter() - t
+        res[k] = (t_ssp / max(s.A, 1), t_r / nrounds)
+
+    ths = [threading.Thread(target=work, args=(k,)) for k in range(ninst)]
+    t0 = time.perf_counter()
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    wall = time.perf_counter() - t0
+    return (float(np.median([r[0] for r in res])), float(np.median([r[1] for r in res])), ninst, wall)
+
+
+def cpu_baseline(cfg, A_per_inst=None, rounds_per_inst=None, target_s=15.0, inst0=0):
+    """The oracle (as it stands) on the box's host cores on a bounded sample of the same workload
+    and the same per-instance work as the GPU step."""
     from tests import harness
     threads = os.cpu_count() or 1
+    if cfg.name == "stress":
+        t_aug, t_round, nin, wall = oracle_stress_sample(cfg, min(threads, 8), threads=threads, inst0=inst0)
+        per_inst = A_per_inst * t_aug + rounds_per_inst * t_round
+        used = min(threads, nin)
+        return {"value": used / per_inst, "unit": "instances/s", "cores": used, "kind": "oracle",
+                "cpu_model": cpu_model(), "extrapolated": True,
+                "sample": (f"{nin} stress instances, one per host thread, {wall:.1f} s: the oracle's canonical SSP for the "
+                           f"first 2 augmentations ({t_aug:.2f} s each) and 3 rounds from the empty state "
+                           f"({t_round:.3f} s each); per-instance time extrapolated to the GPU step's work "
+                           f"({A_per_inst:.0f} augmentations + {rounds_per_inst:.0f} rounds = {per_inst / 3600:.2f} h)")}
     cal = max(threads * 4, 32)
     t = time.perf_counter()
     harness.oracle_pipeline(cfg, inst0, cal, seed=0, threads=threads)
     rate = cal / max(time.perf_counter() - t, 1e-6)
     sample = int(min(max(rate * target_s, cal), 200000))
-    t = time.perf_counter()
-    harness.oracle_pipeline(cfg, inst0 + cal, sample, seed=0, threads=threads)
-    dt = time.perf_counter() - t
-    return {"value": sample / dt, "unit": "instances/s", "cores": threads, "kind": "oracle",
-            "sample": f"{sample} instances of the same workload (full step: pre-churn rounds + churn + SSP + "
-                      f"repair rounds), {dt:.1f} s on {threads} threads, one instance per thread"}
+    r = harness.oracle_pipeline(cfg, inst0 + cal, sample, seed=0, threads=threads)
+    step_s = float(np.sum(r["step_ns"])) / 1e9 if "step_ns" in r else None
+    if step_s:
+        value = sample * threads / step_s
+        what = "the step's work only (churn + cold SSP + repair rounds, timed per instance inside the oracle)"
+    else:
+        value = rate
+        what = "whole pipeline"
+    return {"value": value, "unit": "instances/s", "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": f"{sample} instances of the same workload, {what}, one instance per thread on {threads} threads"}
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the oracle as it stands on the host cores, same metric/config."""
+    """--impl reference: the oracle as it stands on the host cores, same metric / config / unit
+    (PAPER.md has no code to install: the reference arm is the CPU oracle)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample or max(64, threads * 48)
-    from tests import harness
-    for w in range(max(args.warmup, 0)):
-        harness.oracle_pipeline(cfg, w * sample, min(sample, 64), seed=0, threads=threads)
-    t = time.perf_counter()
-    for k in range(args.steps):
-        harness.oracle_pipeline(cfg, k * sample, sample, seed=0, threads=threads)
-    dt = time.perf_counter() - t
-    value = args.steps * sample / dt
+    A_full, R_full = 4072.0, float(cfg.max_rounds)  # stress instance 0: the oracle's stored values (tests/golden)
+    if cfg.name == "stress":
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", "stress_ssp.json")) as f:
+                A_full = float(json.load(f)["A"])
+        except Exception:
+            pass
+    vals = []
+    t_all = time.perf_counter()
+    for k in range(args.warmup + args.steps):
+        if cfg.name == "stress":
+            t_aug, t_round, nin, wall = oracle_stress_sample(cfg, min(threads, 8), ssp_augs=1, nrounds=1,
+                                                             threads=threads, inst0=k)
+            per_inst = A_full * t_aug + R_full * t_round
+            v, ms = min(threads, nin) / per_inst, wall * 1e3
+        else:
+            from tests import harness
+            sample = max(64, threads * 16)
+            t = time.perf_counter()
+            r = harness.oracle_pipeline(cfg, k * sample, sample, seed=0, threads=threads)
+            ms = (time.perf_counter() - t) * 1e3
+            # the step's work only (churn + SSP + repair rounds, timed per instance inside the oracle;
+            # the pre-churn rounds are setup, untimed on the GPU arm too), aggregated over the threads
+            v = sample * threads / (float(np.sum(r["step_ns"])) / 1e9)
+        if k >= args.warmup:
+            vals.append((v, ms))
+    value = float(np.median([v for v, _ in vals]))
+    sample = ("per step: 8 stress instances (one per host thread), the oracle's first SSP augmentation and one "
+              "round each, extrapolated to the full instance (" + f"{A_full:.0f} augmentations + {R_full:.0f} rounds)"
+              if cfg.name == "stress" else "per step: a batch of the workload through the oracle pipeline; the rate "
+              "counts the step's work (churn + SSP + repair rounds) timed per instance, over the host threads")
     line = {"impl": "reference", "metric": "min-cost-flow instances solved/sec", "value": value,
             "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "int64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "instances_per_step": sample, "parallelism": "host threads"},
-            "cpu_baseline": {"value": value, "unit": "instances/s", "cores": threads, "kind": "oracle",
-                             "sample": f"{sample} instances per step (bounded sample of the workload)"},
-            "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "ms_per_step": float(np.mean([m for _, m in vals])), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+            "config": {"workload": workload_name(cfg), "instances_per_gpu": cfg.B, "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": "instances/s", "cores": min(threads, 8) if cfg.name == "stress" else threads,
+                             "kind": "oracle", "cpu_model": cpu_model(), "sample": sample, "extrapolated": cfg.name == "stress"},
+            "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_all}
     print(json.dumps(line), flush=True)
+
+
+
+def e2e(cfg, B, inst0, dev, steps):
+    """The same metric end to end through the public API in host-pointer mode (GWTF_HOST_PTRS).
+    Cold configs (stress): every step creates the handle from pinned host buffers (the whole graph
+    H2D), runs the exact solve and the rounds, reads every per-instance result back to pinned host
+    memory and destroys the handle.  Churn-protocol configs: the graph and its pre-churn state are
+    resident; each step passes the churn events from pinned host memory, solves, runs the repair
+    rounds and reads the results back.  Wall clock per step, median."""
+    import torch
+
+    from paper_2509_21221_b200 import Flow
+    from tests import harness
+    bt, src, snk, link = harness.device_inputs(cfg, inst0, B, device=dev)
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    h = {k: pin(v) for k, v in dict(cap=bt.cap, alive=bt.alive, src=src, snk=snk, link=link, supply=bt.supply).items()}
+    del link, src, snk
+    mr = cfg.max_rounds
+    d2h = B * (8 + 8 + 4 + 4) + B * (4 + 8 + 8 + 4)
+    times = []
+    if cfg.churn == "none":
+        h2d = sum(v.numel() * v.element_size() for v in h.values())
+        for it in range(1 + max(1, steps)):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            fl = Flow(h["cap"], h["src"], h["snk"], h["link"], h["supply"], max_cap=cfg.max_cap, alive=h["alive"],
+                      seed=0, inst_base=inst0, host=True)
+            fl.solve_and_rounds(mr)
+            fl.close()
+            torch.cuda.synchronize()
+            if it >= 1:
+                times.append(time.perf_counter() - t)
+        what = ("per step: create from pinned host buffers (the whole graph H2D) + cold exact solve + rounds to "
+                "steady state + every per-instance result D2H + destroy")
+    else:
+        fl = Flow(h["cap"], h["src"], h["snk"], h["link"], h["supply"], max_cap=cfg.max_cap, alive=h["alive"],
+                  seed=0, inst_base=inst0, host=True)
+        fl.decentralized_rounds(mr)
+        an = upd = None
+        if cfg.churn == "random":
+            a, u = harness.churn_inputs(cfg, inst0, bt.alive, device=dev)
+            an, upd = pin(a), (pin(u) if u is not None else None)
+        else:
+            st = fl.export_round_state()
+            an = torch.from_numpy(gen.llama_victims(st["up"].numpy(), st["down"].numpy(), h["alive"].numpy(),
+                                                    gen.victim_draws(cfg, inst0, B))).pin_memory()
+        fl.snapshot()
+        h2d = (an.numel() if an is not None else 0) + (upd.numel() * 4 if upd is not None else 0)
+        for it in range(3 + max(3, min(steps, 20))):
+            fl.restore()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            fl.apply_churn(an, upd)
+            fl.solve_batch()
+            fl.decentralized_rounds(mr)
+            torch.cuda.synchronize()
+            if it >= 3:
+                times.append(time.perf_counter() - t)
+        fl.close()
+        what = ("per step from pinned host memory: churn events H2D (apply_churn) + cold exact solve + repair rounds + "
+                "every per-instance result D2H; resident graph and pre-churn state (restored, untimed)")
+    tm = float(np.median(times))
+    return {"value": B / tm, "unit": "instances/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": tm * 1e3, "what": what}
 
 
 def main():
@@ -446,42 +605,24 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2509_21221_b200 import Flow
     from paper_2509_21221_b200.dist import gather_results
-    from tests import harness
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     B = cfg.B
-    inst0 = rank * B  # weak scaling: every rank owns B instances
+    inst0 = rank * B  # weak scaling: every rank owns B instances (global ids keyed into the RNG)
     mr = cfg.max_rounds
 
-    # ---------------- untimed setup: inputs resident in HBM, pre-churn converged state ----------
-    bt, src, snk, link = harness.device_inputs(cfg, inst0, B, device=dev)
-    fl = Flow(bt.cap, src, snk, link, bt.supply, max_cap=cfg.max_cap, alive=bt.alive, seed=0, inst_base=inst0)
-    fl.decentralized_rounds(mr)
-    an, upd = None, None
-    if cfg.churn == "random":
-        an, upd = harness.churn_inputs(cfg, inst0, bt.alive, device=dev)
-    elif cfg.churn == "victim":
-        st = fl.export_round_state()
-        an = torch.from_numpy(gen.llama_victims(st["up"].cpu().numpy(), st["down"].cpu().numpy(),
-                                                bt.alive.cpu().numpy(), gen.victim_draws(cfg, inst0, B))).to(dev)
-    fl.snapshot()
+    su = Setup(cfg, dev, inst0, B)  # untimed: inputs resident in HBM, the step's start state snapshotted
+    fl, sol, rr = su.fl, su.sol, su.rr
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    sol = fl.solve_batch()
-    rr = fl.decentralized_rounds(mr)
-    stream = fl.stream
-
-    # GWTF_BENCH_CONCURRENT=1: the step's solve and rounds through gwtf_flow_solve_and_rounds (two
-    # streams; measured ~3% shorter steps, but the per-kernel times then overlap)
-    concurrent = os.environ.get("GWTF_BENCH_CONCURRENT", "0") == "1"
+    concurrent = not args.serial
 
     def step():
-        fl.apply_churn(an, upd)
-        if concurrent:  # exact solve and repair rounds of the step on two streams (independent work)
+        su.churn()
+        if concurrent:  # exact solve and rounds on two streams (independent work on the same graph)
             fl.solve_and_rounds(mr, out_sol=sol, out_rounds=rr)
         else:
             fl.solve_batch(out=sol)
@@ -496,29 +637,28 @@ def main():
         prep()
         step()
     torch.cuda.synchronize()
-
     fl.set_profiling(True)
-    total_ms = 0.0
-    A_total = 0
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     launches0 = int(fl.stats(raw=True)[15])
+    A_total = 0
+    rounds_total = 0
+    total_ms = 0.0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             prep()
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-            ev0.record(stream)
-            g = step()
-            ev1.record(stream)
+            ev0.record(fl.stream)
+            step()
+            ev1.record(fl.stream)
             torch.cuda.synchronize()
             total_ms += ev0.elapsed_time(ev1)
             A_total += int(sol.augmentations.sum().item())
+            rounds_total += int(rr.rounds_run.sum().item())
     ktimes = fl.kernel_times()
     fl.set_profiling(False)
-    # restore() between steps launches no kernels (device memcpys), so the difference is the steps'
-    launches_timed = int(fl.stats(raw=True)[15]) - launches0
+    launches_timed = int(fl.stats(raw=True)[15]) - launches0  # restore() launches no kernels
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -529,23 +669,31 @@ def main():
     peak, peak_src = load_peaks()
     dom = max(ktimes, key=lambda k: ktimes[k][0])
     dom_ms, dom_launches = ktimes[dom]
-    tr, tsrc = load_traffic(dom)
-    roof = {"kernel": dom, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src,
-            "traffic": tr["dram_bytes_per_launch"] if tr else None, "traffic_source": tsrc}
-    if dom == "ssp_kernel":
+    ssp_name = next((k for k in ktimes if k.startswith("ssp")), None)
+
+    def ssp_roof(kname):
+        ms, nl = ktimes[kname]
         alg = algorithmic_bytes_ssp(cfg, A_total)
-        roof["achieved"] = alg / (dom_ms / 1e3) / 1e9
-        roof["algorithmic_bytes_per_launch"] = alg / max(dom_launches, 1)
+        tr, tsrc = load_traffic(f"{cfg.name}:{kname}")
+        return {"kernel": kname, "bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": alg / (ms / 1e3) / 1e9 / peak, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": alg / max(nl, 1),
+                "algorithmic_model": "E x 4 B per augmentation (SURVEY.md 8(d)), E = (S-1) n^2 + 2n; "
+                                     f"{A_total} augmentations in {nl} launches",
+                "traffic": tr.get("dram_bytes_per_launch") if tr else None, "traffic_source": tsrc,
+                "traffic_note": tr.get("note") if tr else None}
+
+    if dom == ssp_name:
+        roof = ssp_roof(dom)
     else:
-        # rounds: per round every slot's (up, down) state and every relay's advertiser row of the
-        # next stage is read once; units from the rounds actually run
-        rounds_total = int(rr.rounds_run.sum().item()) * args.steps
-        per_round = cfg.S * cfg.n * cfg.max_cap * 8 + cfg.S * cfg.n * cfg.n * 4 + 2 * cfg.M * 4
-        alg = float(rounds_total) * per_round
-        roof["achieved"] = alg / (dom_ms / 1e3) / 1e9
-        roof["algorithmic_bytes_per_launch"] = alg / max(dom_launches, 1)
-    roof["frac"] = roof["achieved"] / peak
-    kshare = {k: {"ms_total": v[0], "launches": v[1], "share": v[0] / total_ms if total_ms else None}
+        # the rounds (latency-bound) dominate: HBM use from the ncu DRAM bytes of the committed capture
+        tr, tsrc = load_traffic(f"{cfg.name}:{dom}")
+        bpl = tr.get("dram_bytes_per_launch") if tr else None
+        ach = (bpl * dom_launches / (dom_ms / 1e3) / 1e9) if bpl else None
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak if ach else None, "peak_source": peak_src, "traffic": bpl, "traffic_source": tsrc,
+                "note": "rounds kernel: achieved = ncu DRAM bytes per launch / live launch time (latency-bound)"}
+    kshare = {k: {"ms_total": v[0], "launches": v[1], "share_of_step": v[0] / total_ms if total_ms else None}
               for k, v in ktimes.items()}
 
     line = {"metric": "min-cost-flow instances solved/sec", "value": value, "unit": "instances/s", "n_gpus": world,
@@ -553,97 +701,32 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded generator, SURVEY.md 8(d))",
             "config": {"workload": workload_name(cfg), "instances_per_gpu": B, "global_instances": world * B,
-                       "max_rounds": mr, "l2": "flushed (256 MiB write) between timed steps; state restore untimed",
+                       "max_rounds": mr, "step": ("cold exact solve + rounds from the empty state" if cfg.churn == "none"
+                                                  else "churn + cold exact solve + repair rounds"),
+                       "streams": "solve and rounds concurrent (gwtf_flow_solve_and_rounds)" if concurrent else "serial",
+                       "l2": "flushed (256 MiB write) between timed steps; state restore untimed",
                        "parallelism": f"instance-sharded x{world}"},
-            "roofline": roof, "kernels": kshare, "clocks": clk.summary(),
-            "gpu_launches": None}
-    # our kernels launched inside the timed steps, counted by the library (gwtf_flow_stats[15])
-    line["gpu_launches"] = launches_timed
+            "roofline": roof, "kernels": kshare, "clocks": clk.summary(), "gpu_launches": launches_timed,
+            "augmentations_per_step": A_total / max(args.steps, 1), "rounds_per_step": rounds_total / max(args.steps, 1)}
+    if ssp_name and dom != ssp_name:
+        line["min_plus_roofline"] = ssp_roof(ssp_name)
 
     if rank == 0 and not (args.quick or args.no_e2e):
-        line["e2e"] = e2e(cfg, B, inst0, dev, args)
+        line["e2e"] = e2e(cfg, B, inst0, dev, min(args.steps, 3) if cfg.churn == "none" else args.steps)
     if rank == 0 and not (args.quick or args.no_cpu_baseline):
-        line["cpu_baseline"] = cpu_baseline(cfg)
-    if rank == 0 and world == 1 and not (args.quick or args.no_stress_tier):
-        line["stress_tier"] = stress_tier(dev)
-    if rank == 0 and world == 1 and not (args.quick or args.no_addition):
+        line["cpu_baseline"] = cpu_baseline(cfg, A_per_inst=A_total / max(args.steps * B, 1),
+                                            rounds_per_inst=rounds_total / max(args.steps * B, 1))
+    if rank == 0 and world == 1 and not (args.quick or args.no_configs):
+        line["configs"] = {nm: config_rates(nm, dev) for nm in ("tiny", "gpt", "llama", "churn") if nm != cfg.name}
+    if rank == 0 and world == 1 and not (args.quick or args.no_extras):
         line["node_addition"] = node_addition(dev)
         line["flow_quality"] = flow_quality(dev)
-        line["other_configs"] = other_configs(dev)
         line["multi_source"] = multi_source(dev)
         line["warm_reroute"] = warm_reroute(dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def e2e(cfg, B, inst0, dev, args):
-    """The same metric end to end through the public API in host-pointer mode (GWTF_HOST_PTRS):
-    the graph and its pre-churn converged state are resident (created once from pinned host buffers,
-    untimed, like the device-timed value's setup); every timed step passes that step's inputs -- the
-    churn events (alive mask, link updates) -- from pinned host memory (apply_churn), runs the cold
-    exact solve and the repair rounds, and reads every per-instance result back to pinned host
-    memory.  Wall clock per step, median; the state restore between steps is untimed.  The
-    from-scratch pipeline (create + base rounds + churn + solve + repair) is reported as e2e_cold."""
-    import torch
-
-    from paper_2509_21221_b200 import Flow
-    from tests import harness
-    bt, src, snk, link = harness.device_inputs(cfg, inst0, B, device=dev)
-    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
-    h = {k: pin(v) for k, v in dict(cap=bt.cap, alive=bt.alive, src=src, snk=snk, link=link, supply=bt.supply).items()}
-    mr = cfg.max_rounds
-    fl = Flow(h["cap"], h["src"], h["snk"], h["link"], h["supply"], max_cap=cfg.max_cap, alive=h["alive"],
-              seed=0, inst_base=inst0, host=True)
-    fl.decentralized_rounds(mr)
-    an = upd = None
-    if cfg.churn == "random":
-        a, u = harness.churn_inputs(cfg, inst0, bt.alive, device=dev)
-        an, upd = pin(a), (pin(u) if u is not None else None)
-    elif cfg.churn == "victim":
-        st = fl.export_round_state()
-        an = torch.from_numpy(gen.llama_victims(st["up"].numpy(), st["down"].numpy(), h["alive"].numpy(),
-                                                gen.victim_draws(cfg, inst0, B))).pin_memory()
-    fl.snapshot()
-    h2d = (an.numel() if an is not None else 0) + (upd.numel() * 4 if upd is not None else 0)
-    d2h = B * (8 + 8 + 4 + 4) + B * (4 + 8 + 8 + 4)
-    times = []
-    for it in range(3 + max(3, min(args.steps, 20))):
-        fl.restore()
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        if an is not None or upd is not None:
-            fl.apply_churn(an, upd)
-        fl.solve_batch()
-        fl.decentralized_rounds(mr)
-        torch.cuda.synchronize()
-        if it >= 3:
-            times.append(time.perf_counter() - t)
-    fl.close()
-    tm = float(np.median(times))
-    cold = []
-    for it in range(3):
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        f2 = Flow(h["cap"], h["src"], h["snk"], h["link"], h["supply"], max_cap=cfg.max_cap, alive=h["alive"],
-                  seed=0, inst_base=inst0, host=True)
-        f2.decentralized_rounds(mr)
-        if an is not None or upd is not None:
-            f2.apply_churn(an, upd)
-        f2.solve_batch()
-        f2.decentralized_rounds(mr)
-        f2.close()
-        torch.cuda.synchronize()
-        if it >= 1:
-            cold.append(time.perf_counter() - t)
-    cold_h2d = sum(v.numel() * v.element_size() for v in h.values()) + h2d
-    return {"value": B / tm, "unit": "instances/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "what": "per step from pinned host memory: churn events H2D (apply_churn) + cold exact solve + repair "
-                    "rounds + every per-instance result D2H; resident graph and pre-churn state (restored, untimed)",
-            "e2e_cold": {"value": B / float(np.median(cold)), "unit": "instances/s", "h2d_bytes_per_step": int(cold_h2d),
-                         "d2h_bytes_per_step": int(d2h) * 2,
-                         "what": "create from pinned host buffers + base rounds + churn + solve + repair rounds + D2H"}}
 
 
 if __name__ == "__main__":

@@ -30,7 +30,8 @@ class OrcInstance(ctypes.Structure):
 class OrcResult(ctypes.Structure):
     _fields_ = [("F", ctypes.c_int64), ("cost", ctypes.c_int64), ("A", ctypes.c_int32),
                 ("rounds", ctypes.c_int32), ("F_dec", ctypes.c_int64), ("cost_dec", ctypes.c_int64),
-                ("dangling", ctypes.c_int32), ("pre_rounds", ctypes.c_int32), ("digest", ctypes.c_uint64)]
+                ("dangling", ctypes.c_int32), ("pre_rounds", ctypes.c_int32), ("digest", ctypes.c_uint64),
+                ("step_ns", ctypes.c_int64)]
 
 
 def lib():
@@ -321,7 +322,8 @@ def pipeline_batch(cfg, cap, alive, src, snk, link, supply, churn_kind=0, alive_
                                   out)
     if rc != 0:
         raise RuntimeError(f"oracle pipeline failed rc={rc}")
-    dt = {"digest": np.uint64, "F": np.int64, "cost": np.int64, "F_dec": np.int64, "cost_dec": np.int64}
+    dt = {"digest": np.uint64, "F": np.int64, "cost": np.int64, "F_dec": np.int64, "cost_dec": np.int64,
+          "step_ns": np.int64}
     return {k: np.array([getattr(out[b], k) for b in range(B)], dtype=dt.get(k, np.int32))
             for k, _ in OrcResult._fields_}
 

@@ -6,6 +6,7 @@
 // beyond what the definitions state.  Shares no code with the CUDA path.
 #include "oracle.h"
 
+#include <chrono>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -1369,6 +1370,8 @@ int orc_pipeline_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const i
     int64_t fd, cd;
     int32_t dg, pre = 0;
     orc_rounds_run(R, max_rounds, &pre, &fd, &cd, &dg, nullptr);
+    // the bench step's work starts here (the pre-churn rounds are its untimed setup)
+    const auto t_step = std::chrono::steady_clock::now();
     if (churn_kind == 1) {
       orc_rounds_apply_churn(R, alive_new ? alive_new + b * S * n : nullptr,
                              updates ? updates + 5 * ubeg[b] : nullptr, ubeg[b + 1] - ubeg[b]);
@@ -1387,6 +1390,7 @@ int orc_pipeline_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const i
     orc_rounds_run(R, max_rounds, &rr, &r.F_dec, &r.cost_dec, &r.dangling, nullptr);
     r.rounds = rr;
     r.pre_rounds = pre;
+    r.step_ns = (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_step).count();
     r.digest = orc_rounds_digest(R);
     orc_rounds_destroy(R);
   });

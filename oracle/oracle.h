@@ -117,6 +117,7 @@ int32_t orc_llama_victim(const orc_rounds* R, uint64_t draw_stage, uint64_t draw
 typedef struct {
   int64_t F, cost; int32_t A, rounds; int64_t F_dec, cost_dec; int32_t dangling, pre_rounds;
   uint64_t digest;
+  int64_t step_ns;  /* wall time of the step's work (churn + SSP + repair rounds), this instance */
 } orc_result;
 int orc_pipeline_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const int32_t* cap,
                        const uint8_t* alive, const int32_t* src, const int32_t* snk, const int32_t* link,
