@@ -535,16 +535,22 @@ gwtf_status gwtf_flow_solve_and_rounds(gwtf_flow_t h, int32_t max_rounds, int64_
   CK(h, cudaEventRecord(h->ev_fork, h->stream));
   CK(h, cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
   Timer tr, ts;
-  prof_begin(h, "rounds_kernel", &tr, h->stream2);
-  CK(h, launch_rounds(h->P, ro, h->stream2, h->num_sms));
-  h->kernel_launches += 1;
-  prof_end(h, &tr, h->stream2);
   const int tier = (h->flags & GWTF_FORCE_GLOBAL_TIER) ? 1 : (h->flags & GWTF_FORCE_CLUSTER_TIER) ? 2 : 0;
   const bool cluster = tier != 1 && h->P.cluster_size > 0 && (tier == 2 || ssp_smem_bytes(h->P) > 227 * 1024);
+  // the exact solve is launched first so that its clusters are placed first; beside the cluster
+  // tier of the solve (one cluster of ~10 SMs per instance) the rounds' clusters shrink to 2 CTAs:
+  // measured on the stress step, clusters of 8 or 4 keep some of the solve's clusters from being
+  // co-resident (10.2 / 10.9 s step), clusters of 2 do not (6.9 s; the solve alone takes 6.8 s)
   prof_begin(h, cluster ? "ssp_cluster_kernel" : "ssp_kernel", &ts);
   CK(h, launch_ssp(h->P, so, h->stream, h->num_sms, tier));
   h->kernel_launches += ssp_launch_count(h->P, tier);
   prof_end(h, &ts);
+  Problem PR = h->P;
+  if (cluster) PR.rounds_cluster_pref = 2;
+  prof_begin(h, "rounds_kernel", &tr, h->stream2);
+  CK(h, launch_rounds(PR, ro, h->stream2, h->num_sms));
+  h->kernel_launches += 1;
+  prof_end(h, &tr, h->stream2);
   CK(h, cudaEventRecord(h->ev_join, h->stream2));
   CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   h->has_assignment = true;

@@ -62,6 +62,7 @@ struct Problem {
   int32_t hbits;               // hop bits of the 32-bit packed keys; 0 = 64-bit keys only
   // cluster tier (instances too large for shared memory): cluster size and per-cluster path scratch
   int32_t cluster_size;        // 0 = cluster tier unavailable
+  int32_t rounds_cluster_pref; // rounds cluster size chosen by the caller (0: by the cost model)
   uint8_t* ws_cluster;
   int32_t ws_cluster_slots;
   int32_t debug;               // GWTF_DEBUG_FLAGS (testing)

@@ -1192,6 +1192,7 @@ bool rounds_use_cluster(const Problem& P) {
 // cluster size of the rounds: smallest waves x (relays per thread + fixed barrier cost)
 int rounds_cluster_size(const Problem& P) {
   if (const char* f = getenv("GWTF_ROUNDS_CLUSTER_SIZE")) return atoi(f);
+  if (P.rounds_cluster_pref > 0) return P.rounds_cluster_pref;
   int best = 0;
   long long best_cost = 0;
   for (int C : {16, 8, 4, 2}) {
