@@ -40,6 +40,22 @@ __global__ void pack_tile16_kernel(const Problem P) {
   }
 }
 
+// 8-bit copy of the padded tiles (the cluster tier streams a quarter of the int32 bytes): valid
+// only when every arc within n is present with a cost < 255 (bit 0 of bad otherwise); padding = 255
+__global__ void pack_tile8_kernel(const Problem P, int32_t* bad) {
+  const size_t rows = (size_t)P.B * (P.S - 1) * P.n;
+  const size_t total = rows * P.ld8;
+  int fail = 0;
+  for (size_t t = gtid(); t < total; t += gstride()) {
+    const size_t row = t / P.ld8;
+    const int c = (int)(t % P.ld8);
+    const int32_t v = c < P.n ? P.tile[row * P.ld + c] : 255;
+    if (c < P.n && (v == kAbsent || v >= 255)) fail = 1;
+    P.tile8[t] = (uint8_t)(v == kAbsent || v >= 255 ? 255 : v);
+  }
+  if (fail) atomicOr(bad, 1);
+}
+
 // max finite value and min value of an int32 array (validation of costs / capacities)
 __global__ void scan_kernel(const int32_t* __restrict__ v, int64_t count, int32_t* out_max, int32_t* out_min) {
   int mx = INT_MIN, mn = INT_MAX;
@@ -80,6 +96,10 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
       P.snk[(size_t)b * P.n + w] = c;
     } else if (s >= 0 && s < P.S - 1 && v >= 0 && v < P.n && w >= 0 && w < P.n) {
       P.tile[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld + w] = c;
+      if (P.tile8) {  // the 8-bit copy: an absent link or a cost >= 255 retires it (bit 8)
+        if (c == kAbsent || c >= 255) atomicOr(bad, 8);
+        P.tile8[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld8 + w] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
+      }
       if (P.tile16) {  // the cluster tier's 16-bit copy; a finite cost >= t16code retires it (bit 2)
         if (c != kAbsent && c >= P.t16code) atomicOr(bad, 2);
         P.tile16[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld16 + w] =
@@ -246,6 +266,12 @@ cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t
 cudaError_t launch_pack_tile16(const Problem& P, cudaStream_t st) {
   const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld16;
   if (total && P.tile16) pack_tile16_kernel<<<grid_for(total), 256, 0, st>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_tile8(const Problem& P, int32_t* bad, cudaStream_t st) {
+  const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld8;
+  if (total && P.tile8) pack_tile8_kernel<<<grid_for(total), 256, 0, st>>>(P, bad);
   return cudaGetLastError();
 }
 

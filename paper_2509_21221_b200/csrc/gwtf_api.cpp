@@ -448,6 +448,16 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     P.ld16 = (int32_t)((n + 7) / 8 * 8);
     if ((s = alloc(h, &P.tile16, B * nb * n * P.ld16, true)) != GWTF_OK) return bail(s);
     CK(h, launch_pack_tile16(P, h->stream));
+    if (maxc < 255 && !getenv("GWTF_NO_TILE8")) {  // and the 8-bit copy when every arc is present
+      P.ld8 = (int32_t)((n + 15) / 16 * 16);
+      if ((s = alloc(h, &P.tile8, B * nb * n * P.ld8, true)) != GWTF_OK) return bail(s);
+      int32_t bad8 = 0;
+      CK(h, cudaMemsetAsync(h->bad_flag, 0, 4, h->stream));
+      CK(h, launch_pack_tile8(P, h->bad_flag, h->stream));
+      CK(h, cudaMemcpyAsync(&bad8, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
+      CK(h, cudaStreamSynchronize(h->stream));
+      if (bad8) P.tile8 = nullptr;  // an absent link: stream the 16-bit copy
+    }
   }
   {  // counters[6]: bound on the largest finite arc weight (raised by apply_churn's edge updates)
     const int32_t mw = (int32_t)maxc;
@@ -537,20 +547,20 @@ gwtf_status gwtf_flow_solve_and_rounds(gwtf_flow_t h, int32_t max_rounds, int64_
   Timer tr, ts;
   const int tier = (h->flags & GWTF_FORCE_GLOBAL_TIER) ? 1 : (h->flags & GWTF_FORCE_CLUSTER_TIER) ? 2 : 0;
   const bool cluster = tier != 1 && h->P.cluster_size > 0 && (tier == 2 || ssp_smem_bytes(h->P) > 227 * 1024);
-  // the exact solve is launched first so that its clusters are placed first; beside the cluster
-  // tier of the solve (one cluster of ~10 SMs per instance) the rounds' clusters shrink to 2 CTAs:
-  // measured on the stress step, clusters of 8 or 4 keep some of the solve's clusters from being
-  // co-resident (10.2 / 10.9 s step), clusters of 2 do not (6.9 s; the solve alone takes 6.8 s)
-  prof_begin(h, cluster ? "ssp_cluster_kernel" : "ssp_kernel", &ts);
-  CK(h, launch_ssp(h->P, so, h->stream, h->num_sms, tier));
-  h->kernel_launches += ssp_launch_count(h->P, tier);
-  prof_end(h, &ts);
+  // beside the cluster tier of the solve (one cluster of ~10 SMs per instance) the rounds' clusters
+  // shrink to 2 CTAs: measured on the stress step, clusters of 8 or 4 keep some of the solve's
+  // clusters from being co-resident (10.2 / 10.9 s step), clusters of 2 do not (6.9 s; the solve
+  // alone takes 6.8 s).  The rounds are launched first (launching the solve first measured 12.4 s).
   Problem PR = h->P;
   if (cluster) PR.rounds_cluster_pref = 2;
   prof_begin(h, "rounds_kernel", &tr, h->stream2);
   CK(h, launch_rounds(PR, ro, h->stream2, h->num_sms));
   h->kernel_launches += 1;
   prof_end(h, &tr, h->stream2);
+  prof_begin(h, cluster ? "ssp_cluster_kernel" : "ssp_kernel", &ts);
+  CK(h, launch_ssp(h->P, so, h->stream, h->num_sms, tier));
+  h->kernel_launches += ssp_launch_count(h->P, tier);
+  prof_end(h, &ts);
   CK(h, cudaEventRecord(h->ev_join, h->stream2));
   CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   h->has_assignment = true;
@@ -590,6 +600,7 @@ gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const
     CK(h, cudaMemcpyAsync(&bad, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     if (bad & 2) h->P.tile16 = nullptr;  // a cost no longer fits 16 bits: stream the int32 tiles
+    if (bad & (2 | 8)) h->P.tile8 = nullptr;  // an absent link or a cost >= 255: no 8-bit stream
     if (bad & 1) return fail(GWTF_E_INVALID, "edge update out of range (valid updates were applied)");
     if (bad & 4) return fail(GWTF_E_OVERFLOW, "edge update cost breaks the key bounds (rejected; valid updates were applied)");
   }

@@ -21,6 +21,9 @@ struct Problem {
   uint16_t* tile16;            // cluster tier: [B][S-1][n][ld16] copy of tile, t16code = absent/padding
                                // (nullptr when some cost >= t16code or the tier is unused)
   int32_t ld16;                // n rounded up to 8
+  uint8_t* tile8;              // cluster tier: [B][S-1][n][ld8] 8-bit copy when every arc is present and
+                               // every cost < 255 (255 = padding); nullptr otherwise (or once retired)
+  int32_t ld8;                 // n rounded up to 16
   int32_t t16code;             // T32 of the cluster tier's 32-bit keys (ssp_cluster.cu), < 2^16
   int32_t* src;                // [B][n]
   int32_t* snk;                // [B][n]
@@ -100,6 +103,7 @@ cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32
                          int32_t* bad_flag, cudaStream_t st);
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st);
 cudaError_t launch_pack_tile16(const Problem& P, cudaStream_t st);
+cudaError_t launch_pack_tile8(const Problem& P, int32_t* bad, cudaStream_t st);
 cudaError_t launch_dense_arcs(const Problem& P, int32_t* dense, cudaStream_t st);
 cudaError_t launch_residual_caps(const Problem& P, int32_t* out, cudaStream_t st);
 cudaError_t launch_eq1(int32_t B, int32_t S, int32_t n, int32_t L, const int32_t* comp, const int32_t* loc,

@@ -66,12 +66,12 @@ __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   L.mbar = o; o += al16c(NBMAX * 8 + NBMAX * 4);  // full barriers + consumed-row counters
   L.kin = o; o += al16c(SR * 8);
   L.kout = o; o += al16c(SR * 8);
-  L.g = o; o += al16c(SR * 2);
-  L.capE = o; o += al16c(SR * 2);
+  L.g = o; o += al16c(SR);     // node flows and capacities fit int8 (max_cap <= 32)
+  L.capE = o; o += al16c(SR);
   L.srcf = o; o += al16c(R * 4);
   L.snkf = o; o += al16c(R * 4);
-  const size_t ldk = P.tile16 ? P.ld16 : P.ld;                     // key-vector length
-  const size_t slot = P.tile16 ? (size_t)P.ld16 * 2 : (size_t)P.ld * 4;  // bytes per streamed row
+  const size_t ldk = P.tile8 ? P.ld8 : P.tile16 ? P.ld16 : P.ld;  // key-vector length
+  const size_t slot = P.tile8 ? (size_t)P.ld8 : P.tile16 ? (size_t)P.ld16 * 2 : (size_t)P.ld * 4;  // bytes per row
   L.kbuf = o; o += al16c(ldk * 8);
   L.kb32 = o; o += al16c(ldk * 4);
   L.aq = o; o += al16c((size_t)CT * 12);
@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const ClLayout L = cl_layout(P, C);
   Misc* misc = (Misc*)(sm + L.misc);
   uint64_t* mbar = (uint64_t*)(sm + L.mbar);
-  int16_t* g = (int16_t*)(sm + L.g);
-  int16_t* capE = (int16_t*)(sm + L.capE);
+  int8_t* g = (int8_t*)(sm + L.g);
+  int8_t* capE = (int8_t*)(sm + L.capE);
   int32_t* srcf = (int32_t*)(sm + L.srcf);
   int32_t* snkf = (int32_t*)(sm + L.snkf);
   uint64_t* kbuf = (uint64_t*)(sm + L.kbuf);
@@ -120,9 +120,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const int nbc = L.nbc;
   uint32_t* ecnt = (uint32_t*)(mbar + NBMAX);  // per chunk slot: rows consumed (monotonic)
   // streamed rows: the 16-bit tile copy when present (half the bytes), else the int32 tiles
-  const bool t16 = P.tile16 != nullptr;
-  const int ldk = t16 ? P.ld16 : ld;  // weights per streamed row
-  const uint32_t rowbytes = t16 ? (uint32_t)P.ld16 * 2 : (uint32_t)ld * 4;
+  const bool t8 = P.tile8 != nullptr;  // 8-bit rows (every arc present, costs < 255): a quarter of int32
+  const bool t16 = !t8 && P.tile16 != nullptr;
+  const int ldk = t8 ? P.ld8 : t16 ? P.ld16 : ld;  // weights per streamed row
+  const uint32_t rowbytes = t8 ? (uint32_t)P.ld8 : t16 ? (uint32_t)P.ld16 * 2 : (uint32_t)ld * 4;
   Misc* M0 = cl.map_shared_rank(misc, 0);
   // per-cluster global scratch: path (t* -> s*) and found (gwtf_api.cpp sizes it)
   uint32_t* path = (uint32_t*)(P.ws_cluster + (size_t)cid * 2 * (2 * (size_t)S * n + 4) * 4);
@@ -138,11 +139,11 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   // below T32, and absent weights / INF keys are clamped to T32 (never a minimum).
   const int H32 = 32 - __clz(2 * S * n + 2);
   const int CB32 = 32 - H32;
-  const uint32_t T32 = CB32 >= 4 ? min((1u << (CB32 - 1)) - 1u, t16 ? 0xFFFFu : 0xFFFFFFFFu) : 0u;
+  const uint32_t T32 = CB32 >= 4 ? min((1u << (CB32 - 1)) - 1u, (t16 || t8) ? 0xFFFFu : 0xFFFFFFFFu) : 0u;
   auto ldk_in = [&](int s, int v) -> uint64_t { const int q = own(v); return *(cl.map_shared_rank(kin, q) + s * R + (v - q * R)); };
   auto ldk_out = [&](int s, int v) -> uint64_t { const int q = own(v); return *(cl.map_shared_rank(kout, q) + s * R + (v - q * R)); };
-  auto rg = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
-  auto rcap = [&](int s, int v) -> int16_t* { const int q = own(v); return cl.map_shared_rank(capE, q) + s * R + (v - q * R); };
+  auto rg = [&](int s, int v) -> int8_t* { const int q = own(v); return cl.map_shared_rank(g, q) + s * R + (v - q * R); };
+  auto rcap = [&](int s, int v) -> int8_t* { const int q = own(v); return cl.map_shared_rank(capE, q) + s * R + (v - q * R); };
   auto rsrcf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(srcf, q) + (v - q * R); };
   auto rsnkf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(snkf, q) + (v - q * R); };
 
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
     for (int k = tid; k < S * R; k += CT) {
       const int s = k / R, v = v0 + k % R;
       g[k] = 0;
-      capE[k] = (v < n && P.alive[((size_t)inst * S + s) * n + v]) ? (int16_t)P.cap[((size_t)inst * S + s) * n + v] : 0;
+      capE[k] = (v < n && P.alive[((size_t)inst * S + s) * n + v]) ? (int8_t)P.cap[((size_t)inst * S + s) * n + v] : 0;
     }
     for (int k = tid; k < R; k += CT) { srcf[k] = 0; snkf[k] = 0; }
     if (r == 0) {
@@ -291,10 +292,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 }
               }
               if (r == 0 && tid == 0) atomicAdd(&P.stats[11], 1ull);
-              TMARK(1);
+              TMARK(10);  // frontier relaxation
               const bool vfs = vote(chs);
               for (int k = tid; k < DW; k += CT) dmask[s * DW + k] = 0u;  // every CTA has read it
-              TMARK(2);
+              TMARK(11);  // frontier vote
               if (vfs) {
                 if (s + 1 < S - 1) fwd |= 1ull << (s + 1);
                 else tdirty = true;
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           const int nch = (nr + NW - 1) / NW;
           const uint32_t cbytes = (uint32_t)NW * rowbytes;
           auto rows_of = [&](int sb) -> const uint8_t* {
+            if (t8) return P.tile8 + (((size_t)inst * (S - 1) + sb) * n + v0) * P.ld8;
             return t16 ? (const uint8_t*)(P.tile16 + (((size_t)inst * (S - 1) + sb) * n + v0) * P.ld16)
                        : (const uint8_t*)(tile + ((size_t)sb * n + v0) * ld);
           };
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             pres = g[(s + 1) * R + jr] < capE[(s + 1) * R + jr];
           }
           const uint32_t lim = T32 > (uint32_t)maxw ? T32 - (uint32_t)maxw : 0u;
-          int wide = lim == 0u || (P.debug & 32);  // testing: force the 64-bit path
+          int wide = lim == 0u || (P.debug & 32) || (t8 && T32 < 255u);  // testing (32): force the 64-bit path
           for (int u0 = 0; u0 < ldk; u0 += 4 * CT) {  // gather out_s from L2 (4 loads in flight)
             uint64_t kk[4];
 #pragma unroll
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           // 16-bit rows of up to 1,024 weights: every lane keeps the 32-bit keys of its own
           // columns (chunks c = lane + 32q, 8 weights each) in registers for the whole step
           const bool kreg = t16 && ldk <= 8 * 32 * KQ;
+          const bool kreg8 = t8 && ldk == 16 * 32 * 2;  // 8-bit rows of 1,024 weights
           uint4 kr[2 * KQ];
           if (kreg && !wide) {
             const uint4* kv4 = (const uint4*)kb32;
@@ -379,6 +382,12 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               kr[2 * q] = c < ldk / 8 ? kv4[2 * c] : make_uint4(0u, 0u, 0u, 0u);
               kr[2 * q + 1] = c < ldk / 8 ? kv4[2 * c + 1] : make_uint4(0u, 0u, 0u, 0u);
             }
+          } else if (kreg8 && !wide) {  // lane chunk c = lane + 32q holds columns 16c .. 16c+15
+            const uint4* kv4 = (const uint4*)kb32;
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) kr[4 * q + t] = kv4[4 * (lane + 32 * q) + t];
           }
           TMARK(0);
           int ch = 0;
@@ -411,7 +420,32 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             }
           };
           const uint32_t p2 = *(volatile const uint32_t*)&misc->p2;  // 2^H32, opaque to ptxas (below)
-          if (t16 && kreg && H32 >= 16 && ldk == 8 * 32 * KQ && !wide && !nostream) {
+          if (kreg8 && !wide && !nostream) {
+            // 8-bit rows of 1,024 weights (stress): two 16-byte loads per lane, 32 register keys;
+            // every byte is masked out (BFE-like LOP / SHF) before the IMAD by 2^H32
+            for (int k = 0, b = slot0; k < nch; ++k, b = b + 1 == nbc ? 0 : b + 1) {
+              const int j = k * NW + warp;
+              if (j < nr) {
+                mbar_wait(&mbar[b], (uint32_t)(php >> b) & 1u);
+                if (k == 0) TMARK(12);  // first chunk landed
+                const uint4* row = (const uint4*)(ring + (size_t)b * cbytes + (size_t)warp * rowbytes) + lane;
+                const uint4 w0 = row[0], w1 = row[32];
+                uint32_t a0 = 0xFFFFFFFFu, a1 = a0, a2 = a0, a3 = a0;
+                auto word = [&](uint32_t wd, const uint4& kk) {
+                  a0 = min(a0, (wd & 0xFFu) * p2 + kk.x);
+                  a1 = min(a1, ((wd >> 8) & 0xFFu) * p2 + kk.y);
+                  a2 = min(a2, ((wd >> 16) & 0xFFu) * p2 + kk.z);
+                  a3 = min(a3, (wd >> 24) * p2 + kk.w);
+                };
+                word(w0.x, kr[0]); word(w0.y, kr[1]); word(w0.z, kr[2]); word(w0.w, kr[3]);
+                word(w1.x, kr[4]); word(w1.y, kr[5]); word(w1.z, kr[6]); word(w1.w, kr[7]);
+                const uint32_t acc = __reduce_min_sync(0xffffffffu, min(min(a0, a1), min(a2, a3)));
+                apply(k, j, (acc >> H32) >= T32 ? INF
+                                                : ((uint64_t)(acc >> H32) << kHopBits) | (uint64_t)(acc & ((1u << H32) - 1u)));
+              }
+              release(k, b);
+            }
+          } else if (t16 && kreg && H32 >= 16 && ldk == 8 * 32 * KQ && !wide && !nostream) {
             // the stress fast path: 1,024-weight 16-bit rows, register-resident 32-bit keys, no
             // predicates.  (w << H32) + key is one IMAD by p2 (ptxas would otherwise fuse a shift's
             // add with the min into the quarter-rate DPX VIADDMNMX); the low half-word needs no
@@ -455,7 +489,21 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               // independent accumulators keep the add-min chains short
               const uint4* kv4 = (const uint4*)kb32;
               uint32_t a0 = 0xFFFFFFFFu, a1 = a0, a2 = a0, a3 = a0;
-              if (t16) {
+              if (t8) {  // 8-bit rows (any n): 16 weights per 16-byte load, keys from shared memory
+                const uint4* row = (const uint4*)rowb;
+                for (int c = lane; c < ldk / 16; c += 32) {
+                  const uint4 w = row[c];
+                  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) {
+                    const uint4 kk = kv4[4 * c + t];
+                    a0 = min(a0, (ws[t] & 0xFFu) * p2 + kk.x);
+                    a1 = min(a1, ((ws[t] >> 8) & 0xFFu) * p2 + kk.y);
+                    a2 = min(a2, ((ws[t] >> 16) & 0xFFu) * p2 + kk.z);
+                    a3 = min(a3, (ws[t] >> 24) * p2 + kk.w);
+                  }
+                }
+              } else if (t16) {
                 // 16-bit rows, pre-clamped (absent = T32): two weights per word, shifted into the
                 // cost field; with H32 >= 16 the low weight is one shift, the high one shift + mask
                 const uint4* row = (const uint4*)rowb;
@@ -510,7 +558,18 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               // 2^62 stands for INF in kbuf; absent weights (INT32_MAX, or 0xFFFF -> 2^42 in the
               // 16-bit rows) push a candidate to >= 2^62; nothing overflows 64 bits
               uint64_t acc = kBig, acc2 = kBig;
-              if (t16) {
+              if (t8) {  // 8-bit rows hold no absent arc; padding columns carry kBig keys
+                const uint32_t* row = (const uint32_t*)rowb;
+                for (int c = lane; c < ldk / 4; c += 32) {
+                  const uint32_t wd = row[c];  // 4 weights
+                  const ulonglong2 k01 = *(const ulonglong2*)(kbuf + 4 * c);
+                  const ulonglong2 k23 = *(const ulonglong2*)(kbuf + 4 * c + 2);
+                  acc = umin64(acc, k01.x + ((uint64_t)(wd & 0xFFu) << kHopBits) + 1ull);
+                  acc2 = umin64(acc2, k01.y + ((uint64_t)((wd >> 8) & 0xFFu) << kHopBits) + 1ull);
+                  acc = umin64(acc, k23.x + ((uint64_t)((wd >> 16) & 0xFFu) << kHopBits) + 1ull);
+                  acc2 = umin64(acc2, k23.y + ((uint64_t)(wd >> 24) << kHopBits) + 1ull);
+                }
+              } else if (t16) {
                 const uint2* row = (const uint2*)rowb;
                 auto w64 = [&](uint32_t h) -> uint64_t { return h == T32 ? (1ull << 42) : (uint64_t)h; };
 #pragma unroll 2
@@ -844,9 +903,9 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               } else if (lv == Lt) {
                 *rsnkf(pu) += (int32_t)d;
               } else if ((lu & 1) && lv == lu + 1) {
-                *rg((lu - 1) >> 1, pu) += (int16_t)d;
+                *rg((lu - 1) >> 1, pu) += (int8_t)d;
               } else if (!(lu & 1) && lv == lu - 1) {
-                *rg((lu >> 1) - 1, pu) -= (int16_t)d;
+                *rg((lu >> 1) - 1, pu) -= (int8_t)d;
               } else {
                 const bool fwdarc = !(lu & 1);
                 const int sb = fwdarc ? (lu >> 1) - 1 : (lv >> 1) - 1;
