@@ -711,8 +711,20 @@ def main():
     if ssp_name and dom != ssp_name:
         line["min_plus_roofline"] = ssp_roof(ssp_name)
 
-    if rank == 0 and not (args.quick or args.no_e2e):
-        line["e2e"] = e2e(cfg, B, inst0, dev, min(args.steps, 3) if cfg.churn == "none" else args.steps)
+    if not (args.quick or args.no_e2e):  # every rank, whole-job value from the slowest rank
+        if world > 1:
+            dist.barrier()
+        ee = e2e(cfg, B, inst0, dev, min(args.steps, 3) if cfg.churn == "none" else args.steps)
+        tm = torch.tensor([ee["ms_per_step"]], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ee["ms_per_step"] = float(tm.item())
+        ee["value"] = world * B / (ee["ms_per_step"] / 1e3)
+        if world > 1:
+            ee["h2d_bytes_per_step"] *= world
+            ee["d2h_bytes_per_step"] *= world
+            ee["what"] += f"; every rank, max over the {world} ranks, bytes summed over them"
+        line["e2e"] = ee
     if rank == 0 and not (args.quick or args.no_cpu_baseline):
         line["cpu_baseline"] = cpu_baseline(cfg, A_per_inst=A_total / max(args.steps * B, 1),
                                             rounds_per_inst=rounds_total / max(args.steps * B, 1))

@@ -54,11 +54,19 @@ if rank == 0:
     # sampled instances against the oracle (whole churn step, one instance at a time)
     ids = sorted({0, total - 1, total // 2, *np.random.default_rng(1).integers(0, total, 5).tolist()})
     ok = 0
+    import oracle
     for i in ids:
-        o = harness.oracle_pipeline(cfg, i, 1, seed=0)
         row = g[i].cpu().numpy()
-        want = [int(o["F"][0]), int(o["cost"][0]), int(o["A"][0]), 0, int(o["rounds"][0]), int(o["F_dec"][0]),
-                int(o["cost_dec"][0]), int(o["dangling"][0])]
+        if cfg.churn == "none":  # cold: exact solve + rounds from the empty state
+            bt, src, snk, link = harness.host_inputs(cfg, i, 1)
+            I = oracle.instance_from_batch(bt, 0, link[0], src[0], snk[0])
+            s = oracle.ssp(I)
+            r = oracle.Rounds(I, seed=0, inst_id=i).run(cfg.max_rounds)
+            want = [s.F, s.cost, s.A, 0, r["rounds"], r["F_dec"], r["cost_dec"], r["dangling"]]
+        else:  # the churn protocol: pre-churn rounds, churn, cold solve, repair rounds
+            o = harness.oracle_pipeline(cfg, i, 1, seed=0)
+            want = [int(o["F"][0]), int(o["cost"][0]), int(o["A"][0]), 0, int(o["rounds"][0]), int(o["F_dec"][0]),
+                    int(o["cost_dec"][0]), int(o["dangling"][0])]
         ok += [int(x) for x in row] == want
     res = {"config": name, "world": world, "total": total, "shards": [gdist.shard_range(total, world, r) for r in range(world)],
            "gathered_equals_single_gpu": same, "oracle_sampled": len(ids), "oracle_equal": ok,
