@@ -267,7 +267,7 @@ def flow_quality(dev, B=256):
     return out
 
 
-def warm_reroute(dev, names=("gpt", "llama"), steps=5, warmup=3):
+def warm_reroute(dev, names=("gpt", "llama", "churn"), steps=3, warmup=2):
     """warm-start rerouting (gwtf_flow_warm_reroute) after the config's churn event,
     from the pre-churn optimum, against the cold exact solve of the same churned graph (device events,
     L2 flushed, restore and the assignment copy untimed).  (F, cost) must agree on every instance."""

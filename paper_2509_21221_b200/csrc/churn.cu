@@ -283,6 +283,10 @@ cudaError_t launch_scan_costs(const int32_t* v, int64_t count, int32_t* out_max,
 cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32_t* upd, int64_t k, int32_t* bad,
                          cudaStream_t st) {
   if (upd && k > 0) edge_update_kernel<<<grid_for((size_t)k), 256, 0, st>>>(P, upd, k, bad);
+  {  // the mask before this churn (warm reroute tells rejoined relays from unused ones)
+    cudaError_t e = cudaMemcpyAsync(P.alive_prev, P.alive, (size_t)P.B * P.S * P.n, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
   if (alive_new) {
     cudaError_t e = cudaMemcpyAsync(P.alive, alive_new, (size_t)P.B * P.S * P.n, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;

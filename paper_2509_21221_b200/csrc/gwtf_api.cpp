@@ -321,6 +321,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
   AL(P.snk, B * n, true);
   AL(P.cap, B * Sn, false);
   AL(P.alive, B * Sn, true);
+  AL(P.alive_prev, B * Sn, true);
   AL(P.supply, B, false);
   AL(P.g, B * Sn, false);
   AL(P.src_f, B * n, false);
@@ -464,6 +465,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     CK(h, cudaMemcpyAsync(P.counters + 6, &mw, 4, cudaMemcpyHostToDevice, h->stream));
   }
   CK(h, launch_init_round_state(P, h->stream));
+  CK(h, cudaMemcpyAsync(P.alive_prev, P.alive, B * Sn, cudaMemcpyDeviceToDevice, h->stream));
   CK(h, cudaMemsetAsync(P.stats, 0, 2048 * sizeof(unsigned long long), h->stream));
   CK(h, cudaMemsetAsync(P.arc_cnt, 0, B * std::max<size_t>(nb, 1) * 4, h->stream));
   *out = h;
@@ -823,13 +825,22 @@ gwtf_status gwtf_flow_warm_reroute(gwtf_flow_t h, int32_t* node_flow, int32_t* s
   if ((s = map_out(h, total_cost, B, 23, &C, maps)) != GWTF_OK) return s;
   if ((s = map_out(h, stats, 3 * B, 24, &St, maps)) != GWTF_OK) return s;
   if ((s = map_out(h, inst_status, B, 25, &Q, maps)) != GWTF_OK) return s;
+  int32_t* Qd = Q;  // the kernels always write a status (the fallback pass reads it)
+  if (!Qd && !(Qd = (int32_t*)scratch(h, 27, B * 4))) return fail(GWTF_E_NOMEM, "warm_reroute status");
   void* ws = scratch(h, 26, warm_ws_bytes(P, warm_grid(P)));
   if (!ws) return fail(GWTF_E_NOMEM, "warm_reroute workspace");
   Timer t;
   prof_begin(h, "warm_kernel", &t);
-  CK(h, launch_warm(P, dev[0], dev[1], dev[2], dev[3], ws, F, C, St, Q, h->stream));
-  h->kernel_launches += 1;
+  CK(h, launch_warm(P, dev[0], dev[1], dev[2], dev[3], ws, F, C, St, Qd, h->stream));
+  h->kernel_launches += 2;
   prof_end(h, &t);
+  if (!inst_status) {  // no status array from the caller: a failed instance fails the call
+    std::vector<int32_t> q(B);
+    CK(h, cudaMemcpyAsync(q.data(), Qd, B * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    for (size_t b = 0; b < B; ++b)
+      if (q[b] != 0) return fail(GWTF_E_STATE, "warm_reroute: an instance did not reach the optimum (status != 0)");
+  }
   return finish_out(h, maps);
 }
 

@@ -29,6 +29,7 @@ struct Problem {
   int32_t* snk;                // [B][n]
   int32_t* cap;                // [B][S][n]
   uint8_t* alive;              // [B][S][n]
+  uint8_t* alive_prev;         // [B][S][n] the mask before the last apply_churn (warm reroute: rejoined relays)
   int64_t* supply;             // [B]
   // exact-solve state (persistent for get_assignment)
   int32_t* g;                  // [B][S][n]

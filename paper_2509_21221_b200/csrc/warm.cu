@@ -43,6 +43,7 @@ struct WarmCtx {
   const int32_t* snk;
   const int32_t* cap;
   const uint8_t* alive;
+  const uint8_t* alive_prev;  // before the last churn: a node arc of a relay alive now and dead then is new
   int32_t* src_f;        // [n]
   int32_t* g;            // [S][n]
   int32_t* arc;          // [S-1][n][n]
@@ -149,10 +150,13 @@ __device__ bool strip_unit(const WarmCtx& c, int64_t e) {
   return true;
 }
 
-__global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
-                                                        int32_t* arc_all, int32_t* snk_f_all, uint64_t* lab_all,
-                                                        int32_t* stamp_all, int64_t* F_out, int64_t* cost_out,
-                                                        int64_t* stats_out, int32_t* status_out) {
+// The general fallback (instances the potential-carrying repair cannot take: a negative residual
+// cycle on the kept flow, i.e. some link got cheaper; status 7 from warm_kernel): strip, cancel
+// negative cycles (Klein), resume SSP.
+__global__ void __launch_bounds__(kThreads) klein_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
+                                                         int32_t* arc_all, int32_t* snk_f_all, uint64_t* lab_all,
+                                                         int32_t* stamp_all, int64_t* F_out, int64_t* cost_out,
+                                                         int64_t* stats_out, int32_t* status_out) {
   __shared__ int changed_sm, bad_sm, last_sm, cyc_sm, strip_n;
   __shared__ int strip_list[kStripList];
   __shared__ unsigned long long cost_sm;
@@ -160,6 +164,7 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
   const int N = 2 + 2 * S * n;
   const int64_t E = 2ll * n + (int64_t)S * n + (int64_t)(S - 1) * n * n;
   for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
+    if (status_out[b] != 7) continue;  // solved by warm_kernel
     WarmCtx c;
     c.S = S; c.n = n; c.ld = P.ld; c.N = N; c.E = E; c.M = P.supply[b];
     c.tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
@@ -314,7 +319,293 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
       F_out[b] = F;
       cost_out[b] = (int64_t)cost_sm;
       if (stats_out) { stats_out[3 * b] = stripped; stats_out[3 * b + 1] = cycles; stats_out[3 * b + 2] = augment; }
-      if (status_out) status_out[b] = status;  // 5 = non-negative cycle (never expected)
+      status_out[b] = status;  // 5 = non-negative cycle (never expected)
+    }
+    __syncthreads();
+  }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Potential-carrying repair (the default path).  The pre-churn assignment is optimal for the old
+// graph, so its residual graph has no negative cycle; a crash, a dropped link or a raised cost
+// only removes residual arcs or lowers flows on removed arcs, so the kept part has none either.
+//   P. potentials pi: Bellman-Ford from a virtual root over the residual arcs of the kept flow
+//      (x' = min(x, cap) on every arc), leaving out the node arcs of rejoined relays (new arcs;
+//      alive now, dead before the churn) and the bypass; no convergence within N + 2 passes = a
+//      negative cycle (some cost was lowered): status 7, the instance goes to klein_kernel untouched;
+//   C. cut: every arc carrying more than its new capacity (dead relay, absent link / src / snk)
+//      drops the excess units, which leaves imbalances at its two ends -- the flow is not
+//      stripped along whole paths, it is rerouted around the cut ("reroute");
+//   V. a rejoined relay's node arc with a negative reduced cost (a shortcut) is saturated;
+//   A. successive shortest paths on reduced costs (all >= 0) from the excess nodes to the deficit
+//      nodes (multi-source Bellman-Ford, nearest deficit node, bottleneck augment, pi += min(d,
+//      d_target)), until balanced; a unit that cannot be rerouted goes back through the bypass
+//      s* -> t* (cost BIG > any simple path: the lexicographic max-flow device of SURVEY C3 i);
+//   B. successive shortest paths s* -> t* on the real arcs while the bypass still carries units.
+//   The result is a min-cost flow of maximum value on the churned graph: (F, cost) equal the cold
+//   solve's.  Without churn nothing is cut or saturated and B finds no path: the identity.
+// Bypass residual arcs: r = 2E (s* -> t*, cap M - byp, cost BIG) and 2E + 1 (t* -> s*, cap byp).
+__device__ __forceinline__ void res2(const WarmCtx& c, int64_t r, int64_t byp, int64_t big, int& from, int& to,
+                                     int64_t& rcap, int64_t& rcost, int32_t*& x, int& sign) {
+  if (r >= 2 * c.E) {
+    x = nullptr;
+    if (r == 2 * c.E) { from = 0; to = 1; rcap = c.M - byp; rcost = big; sign = 1; }
+    else { from = 1; to = 0; rcap = byp; rcost = -big; sign = -1; }
+    return;
+  }
+  res_of(c, r, from, to, rcap, rcost, x, sign);
+}
+
+__global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
+                                                        int32_t* arc_all, int32_t* snk_f_all, uint64_t* lab_all,
+                                                        int64_t* pi_all, int32_t* imb_all, int64_t* F_out,
+                                                        int64_t* cost_out, int64_t* stats_out, int32_t* status_out) {
+  __shared__ int changed_sm, bad_sm, last_sm;
+  __shared__ unsigned long long best_sm, cost_sm;
+  __shared__ long long byp_sm, delta_sm;
+  __shared__ int any_sm;
+  const int S = P.S, n = P.n;
+  const int N = 2 + 2 * S * n;
+  const int64_t E = 2ll * n + (int64_t)S * n + (int64_t)(S - 1) * n * n;
+  const int64_t NR = 2 * E + 2;  // residual arcs incl. the bypass pair
+  for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
+    WarmCtx c;
+    c.S = S; c.n = n; c.ld = P.ld; c.N = N; c.E = E; c.M = P.supply[b];
+    c.tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
+    c.src = P.src + (size_t)b * n;
+    c.snk = P.snk + (size_t)b * n;
+    c.cap = P.cap + (size_t)b * S * n;
+    c.alive = P.alive + (size_t)b * S * n;
+    c.alive_prev = P.alive_prev + (size_t)b * S * n;
+    c.src_f = src_f_all + (size_t)b * n;
+    c.g = g_all + (size_t)b * S * n;
+    c.arc = arc_all + (size_t)b * (S - 1) * n * n;
+    c.snk_f = snk_f_all + (size_t)b * n;
+    uint64_t* labv = lab_all + (size_t)blockIdx.x * N;
+    int64_t* pi = pi_all + (size_t)blockIdx.x * N;
+    int32_t* imb = imb_all + (size_t)blockIdx.x * N;
+    // BIG exceeds any simple residual path cost: (2Sn+2) x the largest finite arc cost, + 1
+    int64_t maxc = 0;
+    if (threadIdx.x == 0) { bad_sm = 0; best_sm = 0; byp_sm = 0; }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      const ArcV a = arc_of(c, e);
+      if (a.cost > maxc) maxc = a.cost;
+    }
+    atomicMax(&best_sm, (unsigned long long)maxc);
+    if (threadIdx.x == 0) {
+      int64_t F0 = 0;
+      for (int i = 0; i < n; ++i) F0 += c.src_f[i];
+      byp_sm = c.M - F0;
+    }
+    __syncthreads();
+    const int64_t big = (int64_t)(2 * (int64_t)S * n + 2) * (int64_t)best_sm + 1;
+    if (big >= (1ll << 36) || byp_sm < 0) {  // labels hold |distance| < 2^38: leave it to the fallback
+      if (threadIdx.x == 0) status_out[b] = 7;
+      __syncthreads();
+      continue;
+    }
+    // ---- P. potentials of the kept flow (x' = min(x, cap)), zero-flow node arcs and bypass left out ----
+    for (int k = threadIdx.x; k < N; k += blockDim.x) labv[k] = lab(0, kNoPred);
+    __syncthreads();
+    int passes = 0;
+    for (;;) {
+      if (threadIdx.x == 0) changed_sm = 0;
+      __syncthreads();
+      int ch = 0;
+      for (int64_t r = threadIdx.x; r < 2 * E; r += blockDim.x) {
+        const ArcV a = arc_of(c, r >> 1);
+        const int64_t xk = *a.x < a.cap ? *a.x : a.cap;  // the kept flow
+        int from, to;
+        int64_t rcap, rcost;
+        if (r & 1) { from = a.to; to = a.from; rcap = xk; rcost = -a.cost; }
+        else {
+          from = a.from; to = a.to; rcap = a.cap - xk; rcost = a.cost;
+          if ((r >> 1) >= n && (r >> 1) < n + (int64_t)S * n) {  // a rejoined relay's node arc is new
+            const int k = (int)((r >> 1) - n);
+            if (c.alive[k] && !c.alive_prev[k]) rcap = 0;
+          }
+        }
+        if (rcap <= 0) continue;
+        const int64_t d = lab_dist(ld_lab(&labv[from])) + rcost;
+        if (d >= kBias || d <= -kBias) { bad_sm = 1; continue; }
+        const uint64_t cand = lab(d, (uint64_t)r);
+        if ((cand >> kArcBits) < (ld_lab(&labv[to]) >> kArcBits)) {
+          const uint64_t old = atomicMin((unsigned long long*)&labv[to], (unsigned long long)cand);
+          if ((cand >> kArcBits) < (old >> kArcBits)) ch = 1;
+        }
+      }
+      if (ch) changed_sm = 1;
+      __syncthreads();
+      const bool any = changed_sm != 0;
+      __syncthreads();
+      if (!any || bad_sm) break;
+      if (++passes > N + 2) { if (threadIdx.x == 0) bad_sm = 7; __syncthreads(); break; }
+    }
+    if (bad_sm) {  // a negative cycle on the kept flow (or label overflow): the general fallback
+      if (threadIdx.x == 0) status_out[b] = 7;
+      __syncthreads();
+      continue;
+    }
+    for (int k = threadIdx.x; k < N; k += blockDim.x) { pi[k] = lab_dist(ld_lab(&labv[k])); imb[k] = 0; }
+    __syncthreads();
+    // ---- C. cut the units the churned graph cannot carry ----
+    long long cut = 0, sat = 0;
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      const ArcV a = arc_of(c, e);
+      if (*a.x > a.cap) {
+        const int32_t dlt = *a.x - (int32_t)a.cap;
+        *a.x = (int32_t)a.cap;
+        atomicAdd(&imb[a.from], dlt);
+        atomicSub(&imb[a.to], dlt);
+        cut += dlt;
+      }
+    }
+    __syncthreads();
+    // ---- V. saturate the residual arcs with a negative reduced cost ----
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      if (e < n || e >= n + (int64_t)S * n) continue;  // node arcs only (the rest are certified by P)
+      const ArcV a = arc_of(c, e);
+      const int k = (int)(e - n);
+      if (c.alive[k] && !c.alive_prev[k] && *a.x == 0 && a.cap > 0 && pi[a.from] - pi[a.to] < 0) {
+        *a.x = (int32_t)a.cap;
+        atomicSub(&imb[a.from], (int)a.cap);
+        atomicAdd(&imb[a.to], (int)a.cap);
+        ++sat;
+      }
+    }
+    __syncthreads();
+
+    // ---- S. successive shortest paths on reduced costs, excess -> deficit ----
+    long long iters = 0;
+    bool phaseB = false;
+    for (;;) {
+      if (threadIdx.x == 0) { any_sm = 0; best_sm = ~0ull; }
+      __syncthreads();
+      for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        const bool src = imb[k] > 0;
+        labv[k] = src ? lab(0, kNoPred) : kLabInf;
+        if (src) any_sm = 1;
+      }
+      __syncthreads();
+      if (!any_sm) {
+        if (phaseB || byp_sm == 0) break;
+        // B: the bypass's units become s*'s excess and t*'s deficit; real arcs only from here
+        phaseB = true;
+        if (threadIdx.x == 0) { imb[0] += (int32_t)byp_sm; imb[1] -= (int32_t)byp_sm; }
+        __syncthreads();
+        continue;
+      }
+      const int64_t byp = byp_sm;
+      const int64_t nr_now = phaseB ? 2 * E : NR;
+      int sp = 0;
+      for (;;) {  // Bellman-Ford on reduced costs (non-negative: converges within N passes)
+        if (threadIdx.x == 0) changed_sm = 0;
+        __syncthreads();
+        int ch = 0;
+        for (int64_t r = threadIdx.x; r < nr_now; r += blockDim.x) {
+          int from, to, sign;
+          int64_t rcap, rcost;
+          int32_t* xp;
+          res2(c, r, byp, big, from, to, rcap, rcost, xp, sign);
+          if (r == 2 * E + 1) continue;  // the reverse bypass is never used (B moves its units)
+          if (rcap <= 0) continue;
+          const uint64_t Lf = ld_lab(&labv[from]);
+          if (Lf == kLabInf) continue;
+          const int64_t d = lab_dist(Lf) + rcost + pi[from] - pi[to];
+          if (d >= kBias) { bad_sm = 1; continue; }
+          const uint64_t cand = lab(d, (uint64_t)r);
+          if ((cand >> kArcBits) < (ld_lab(&labv[to]) >> kArcBits)) {
+            const uint64_t old = atomicMin((unsigned long long*)&labv[to], (unsigned long long)cand);
+            if ((cand >> kArcBits) < (old >> kArcBits)) ch = 1;
+          }
+        }
+        if (ch) changed_sm = 1;
+        __syncthreads();
+        const bool anych = changed_sm != 0;
+        __syncthreads();
+        if (!anych || bad_sm) break;
+        if (++sp > N + 2) { if (threadIdx.x == 0) bad_sm = 3; __syncthreads(); break; }
+      }
+      if (bad_sm) break;
+      // nearest deficit node (distance, node) -- lowest node on ties
+      for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        if (imb[k] >= 0) continue;
+        const uint64_t L = ld_lab(&labv[k]);
+        if (L == kLabInf) continue;
+        atomicMin(&best_sm, ((unsigned long long)(lab_dist(L) + kBias) << 24) | (unsigned long long)k);
+      }
+      __syncthreads();
+      if (best_sm == ~0ull) {
+        if (phaseB) {  // t* unreachable: the units left at s* stay on the bypass (F is maximal)
+          if (threadIdx.x == 0) { byp_sm = imb[0]; imb[1] += imb[0]; imb[0] = 0; }
+          __syncthreads();
+          break;
+        }
+        if (threadIdx.x == 0) bad_sm = 6;
+        __syncthreads();
+        break;
+      }
+      const int tgt = (int)(best_sm & 0xFFFFFF);
+      const int64_t dt = (int64_t)(best_sm >> 24) - kBias;
+      if (threadIdx.x == 0) {  // trace to the source excess node, bottleneck, augment
+        int64_t bott = -(int64_t)imb[tgt];
+        int x = tgt, guard = 0;
+        while (lab_pred(ld_lab(&labv[x])) != (int)kNoPred && ++guard <= N + 2) {
+          int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+          res2(c, lab_pred(ld_lab(&labv[x])), byp_sm, big, from, to, rcap, rcost, xp, sign);
+          bott = rcap < bott ? rcap : bott;
+          x = from;
+        }
+        const int s0 = x;
+        if (guard > N + 2 || imb[s0] <= 0) { bad_sm = 5; }
+        else {
+          bott = imb[s0] < bott ? imb[s0] : bott;
+          for (x = tgt; x != s0;) {
+            int from, to, sign; int64_t rcap, rcost; int32_t* xp;
+            const int r = lab_pred(ld_lab(&labv[x]));
+            res2(c, r, byp_sm, big, from, to, rcap, rcost, xp, sign);
+            if (xp) *xp += (int32_t)(sign * bott);
+            else byp_sm += sign * bott;
+            x = from;
+          }
+          imb[s0] -= (int32_t)bott;
+          imb[tgt] += (int32_t)bott;
+          if (phaseB) byp_sm -= bott;  // an s* -> t* path on real arcs takes units off the bypass
+        }
+        delta_sm = bott;
+      }
+      __syncthreads();
+      if (bad_sm) break;
+      for (int k = threadIdx.x; k < N; k += blockDim.x) {  // pi += min(d, d_target)
+        const uint64_t L = ld_lab(&labv[k]);
+        const int64_t d = L == kLabInf ? dt : lab_dist(L);
+        pi[k] += d < dt ? d : dt;
+      }
+      ++iters;
+      __syncthreads();
+    }
+    // ---- objective of the repaired assignment ----
+    if (threadIdx.x == 0) cost_sm = 0;
+    __syncthreads();
+    long long part = 0;
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      const ArcV a = arc_of(c, e);
+      part += (long long)*a.x * a.cost;
+    }
+    atomicAdd(&cost_sm, (unsigned long long)part);
+    __shared__ unsigned long long cut_sm, sat_sm;
+    if (threadIdx.x == 0) { cut_sm = 0; sat_sm = 0; }
+    __syncthreads();
+    atomicAdd(&cut_sm, (unsigned long long)cut);
+    atomicAdd(&sat_sm, (unsigned long long)sat);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      F_out[b] = c.M - byp_sm;
+      cost_out[b] = (int64_t)cost_sm;
+      if (stats_out) { stats_out[3 * b] = (int64_t)cut_sm; stats_out[3 * b + 1] = (int64_t)sat_sm; stats_out[3 * b + 2] = iters; }
+      status_out[b] = bad_sm;
     }
     __syncthreads();
   }
@@ -324,18 +615,23 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
 
 size_t warm_ws_bytes(const Problem& P, int grid) {
   const size_t N = 2 + 2 * (size_t)P.S * P.n;
-  return (size_t)grid * N * (8 + 4);
+  return (size_t)grid * N * (8 + 4 + 8 + 4);
 }
 
 int warm_grid(const Problem& P) { return (int)std::min<int64_t>(P.B, 148 * 8); }
 
+// status must be a device array of B entries: the repair kernel runs every instance, the fallback
+// kernel the ones it marked 7
 cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* arc, int32_t* snk_f, void* ws,
                         int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, cudaStream_t st) {
   const int grid = warm_grid(P);
   const size_t N = 2 + 2 * (size_t)P.S * P.n;
   uint64_t* labv = (uint64_t*)ws;
-  int32_t* stamp = (int32_t*)(labv + (size_t)grid * N);
-  warm_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, stamp, F, cost, stats, status);
+  int64_t* pi = (int64_t*)(labv + (size_t)grid * N);
+  int32_t* imb = (int32_t*)(pi + (size_t)grid * N);
+  int32_t* stamp = imb + (size_t)grid * N;
+  warm_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, pi, imb, F, cost, stats, status);
+  klein_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, stamp, F, cost, stats, status);
   return cudaGetLastError();
 }
 
