@@ -354,6 +354,21 @@ def multi_source(dev, B=8192, reps=1):
                      "cost_per_data_node": [float(r[1].double().mean()) for r in res],
                      "what": "wall clock per batch, one microbatch per data node per turn (a supply-1 solve "
                              "and a handle create per turn)"}
+        # the multi-data-node decentralized rounds (gwtf_mc_rounds, MC-SYNC): M / K microbatches per data
+        # node, 120 rounds (the paper's budget), device time
+        from paper_2509_21221_b200.multisource import mc_rounds
+        sups = [d(np.full(B, cfg.M // K, np.int64)) for _ in range(K)]
+        mc = mc_rounds(d(bt.cap), d(bt.alive), d(bt.link), srcs, snks, sups, max_cap=cfg.max_cap, max_rounds=120)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        mc = mc_rounds(d(bt.cap), d(bt.alive), d(bt.link), srcs, snks, sups, max_cap=cfg.max_cap, max_rounds=120)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        out[name]["mc_rounds"] = {"instances_per_s": B / (ms / 1e3), "ms": ms, "rounds_mean": float(mc["rounds"].double().mean()),
+                                  "F_dec_per_data_node": [float(x) for x in mc["F_dec"].double().mean(dim=1)],
+                                  "cost_dec_per_data_node": [float(x) for x in mc["cost_dec"].double().mean(dim=1)],
+                                  "what": "MC-SYNC rounds from the empty state, M/K microbatches per data node, 120 rounds"}
     return out
 
 

@@ -192,6 +192,27 @@ gwtf_status gwtf_flow_import_round_state(gwtf_flow_t h, const int32_t* up, const
                                          const int32_t* src_down, const int32_t* snk_up, const int32_t* kacc,
                                          const int32_t* deny, const int32_t* quiet, const int64_t* round);
 
+/* Multi-data-node decentralized rounds, MC-SYNC (PAPER.md:203
+ * "each data node ... must receive its own flow back", :249 "unpaired outflow", settings 5-6 of
+ * :501-502).  Stateless: B instances sharing the relays and links of the single-commodity layout
+ * (cap / alive [B][S][n], link_cost [B][S-1][n_dst][n_src]) with K data nodes each: src_cost /
+ * snk_cost [K][B][n], supply [K][B] (int64, <= 2^20).  Runs the rounds from the empty state until
+ * steady_window quiet rounds or max_rounds; every non-FREE slot carries its chain's data node, so
+ * requests, grants, Change and self-pairing stay within one data node (K = 1 is
+ * gwtf_flow_decentralized_rounds from an empty state).  Outputs (device, caller-owned): rounds_run
+ * [B], dec_flow / dec_cost [K][B] (complete SRC_k -> SNK_k chains and their Eq. 2 cost), dangling
+ * [B], round_digests [B][max_rounds] or NULL, up / down / tag [B][S][n][max_cap] or NULL (final
+ * state; data-node slot i of D_k = -2 - (k Mmax + i), Mmax = max supply; tag -1 on FREE slots).
+ * All device pointers on `stream` (a cudaStream_t); reads the supplies back (synchronizes).
+ * INVALID on bad shapes or parameters, UNSUPPORTED when one instance's state exceeds 227 KB. */
+gwtf_status gwtf_mc_rounds(int32_t B, int32_t S, int32_t n, int32_t max_cap, int32_t K, const int32_t* cap,
+                           const uint8_t* alive, const int32_t* link_cost, const int32_t* src_cost,
+                           const int32_t* snk_cost, const int64_t* supply, uint64_t seed, int64_t inst_base, double T0,
+                           double alpha, int32_t objective, int32_t steady_window, int32_t deny_after,
+                           int32_t max_rounds, int32_t* rounds_run, int64_t* dec_flow, int64_t* dec_cost,
+                           int32_t* dangling, uint64_t* round_digests, int32_t* up, int32_t* down, int32_t* tag,
+                           void* stream);
+
 /* Save / restore the handle's mutable state (masks, costs, round state) on the device,
  * e.g. to replay the same churn step several times in a benchmark. */
 gwtf_status gwtf_flow_snapshot(gwtf_flow_t h);

@@ -68,6 +68,15 @@ def lib():
         L.orc_rounds_instance.argtypes = [P] + [P] * 5
         L.orc_llama_victim.restype = ctypes.c_int32
         L.orc_llama_victim.argtypes = [P, ctypes.c_uint64, ctypes.c_uint64]
+        L.orc_mc_rounds_create.restype = P
+        L.orc_mc_rounds_create.argtypes = [IP, ctypes.c_int32, P, P, P, ctypes.c_uint64, ctypes.c_int64,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_int32]
+        L.orc_mc_rounds_destroy.argtypes = [P]
+        L.orc_mc_rounds_run.argtypes = [P, ctypes.c_int32, P, P, P, P, P]
+        L.orc_mc_rounds_export.argtypes = [P] + [P] * 9
+        L.orc_mc_rounds_digest.restype = ctypes.c_uint64
+        L.orc_mc_rounds_digest.argtypes = [P]
         L.orc_pipeline_batch.argtypes = ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [P] * 6
                                          + [ctypes.c_int32, P, P, ctypes.c_int64, P, ctypes.c_uint64, ctypes.c_int64,
                                             ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
@@ -552,4 +561,58 @@ def rng_h(seed: int, inst: int, rnd: int, gid: int, stream: int) -> int:
 
 def pick(x: int, m: int) -> int:
     return int(lib().orc_pick(x & (2**64 - 1), m))
+
+
+class McRounds:
+    """Multi-data-node synchronous rounds (MC-SYNC): K data nodes with
+    their own src / snk costs ([K][n]) and supplies ([K]) on I's relays and links."""
+
+    def __init__(self, I: Instance, srcs, snks, supplies, seed=0, inst_id=0, T0=1.7, alpha=0.95,
+                 objective=OBJ_SUM, W=5, deny_after=3):
+        self.I = I
+        self.K = len(supplies)
+        self.src = np.ascontiguousarray(np.asarray(srcs, np.int32).reshape(self.K, I.n))
+        self.snk = np.ascontiguousarray(np.asarray(snks, np.int32).reshape(self.K, I.n))
+        self.M = np.ascontiguousarray(np.asarray(supplies, np.int64).reshape(self.K))
+        self.Mmax = max(1, int(self.M.max()))
+        c = I.c()
+        self.h = lib().orc_mc_rounds_create(ctypes.byref(c), self.K, _ptr(self.src), _ptr(self.snk), _ptr(self.M),
+                                            seed, inst_id, T0, alpha, objective, W, deny_after)
+        if not self.h:
+            raise ValueError("orc_mc_rounds_create rejected the parameters")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_mc_rounds_destroy(self.h)
+            self.h = None
+
+    def run(self, max_rounds, digests=False):
+        rr = ctypes.c_int32()
+        F = np.zeros(self.K, np.int64)
+        C = np.zeros(self.K, np.int64)
+        dg = ctypes.c_int32()
+        d = np.zeros(max(max_rounds, 1), np.uint64) if digests else None
+        lib().orc_mc_rounds_run(self.h, max_rounds, ctypes.byref(rr), _ptr(F), _ptr(C), ctypes.byref(dg), _ptr(d))
+        out = dict(rounds=rr.value, F_dec=F, cost_dec=C, dangling=dg.value)
+        if digests:
+            out["digests"] = d[: rr.value]
+        return out
+
+    def export(self):
+        I = self.I
+        up = np.zeros((I.S, I.n, I.max_cap), np.int32)
+        dn = np.zeros_like(up)
+        tg = np.zeros_like(up)
+        sd = np.zeros((self.K, self.Mmax), np.int32)
+        su = np.zeros_like(sd)
+        k = np.zeros((I.S, I.n), np.int32)
+        dw = np.zeros_like(k)
+        q = ctypes.c_int32()
+        r = ctypes.c_int64()
+        lib().orc_mc_rounds_export(self.h, _ptr(up), _ptr(dn), _ptr(tg), _ptr(sd), _ptr(su), _ptr(k), _ptr(dw),
+                                   ctypes.byref(q), ctypes.byref(r))
+        return dict(up=up, down=dn, tag=tg, src_down=sd, snk_up=su, kacc=k, deny=dw, quiet=q.value, round=r.value)
+
+    def digest(self) -> int:
+        return int(lib().orc_mc_rounds_digest(self.h))
 

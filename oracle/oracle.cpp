@@ -1091,6 +1091,359 @@ int warm_reroute(const Inst& Iold, const Flow& fold, const Inst& Inew, Flow& out
 }  // namespace
 
 struct orc_rounds { Rounds R; };
+// ---------------------------------------------------------------------------
+// Multi-data-node decentralized rounds, MC-SYNC.
+// "each data node ... must receive its own flow back", :209, settings 5-6 of :501-502.  K data
+// nodes D_0..D_{K-1}, each with its own supply M_k, SRC_k / SNK_k slots and source / sink costs;
+// the relays and links are shared.  Every non-FREE relay slot carries the data node (tag) of its
+// chain: an OUT slot of tag k is "unpaired outflow to data node k", so requests, grants,
+// swaps and self-pairing stay within one tag.  With K = 1 every rule is the single-commodity one.
+// Pointers: relay slot >= 0, NONE, data-node slot -2 - (k * Mmax + i).
+// ---------------------------------------------------------------------------
+struct McRounds {
+  Inst I;
+  int K = 1;
+  int64_t Mmax = 0;
+  std::vector<int64_t> M;                  // [K]
+  std::vector<int32_t> srcK, snkK;         // [K][n]
+  uint64_t seed = 0;
+  int64_t inst = 0;
+  int obj = 0, W = 5, deny_after = 3;
+  Anneal ann;
+  std::vector<int32_t> up, down, tag, src_down, snk_up, kacc, deny;  // src_down / snk_up [K][Mmax]
+  int32_t quiet = 0;
+  int64_t round = 0;
+
+  int Sn() const { return I.S * I.n; }
+  int stage(int gid) const { return gid / I.n; }
+  int capE(int gid) const { return I.capE(gid / I.n, gid % I.n); }
+  bool alive(int gid) const { return I.alive[gid] != 0; }
+  int slot(int gid, int j) const { return gid * I.MC + j; }
+  int st(int p) const { return Rounds::state_of(up[p], down[p]); }
+  static int32_t dptr(int k, int64_t i, int64_t Mm) { return (int32_t)(-2 - (k * Mm + i)); }
+  int dk(int32_t p) const { return (int)((-2 - (int64_t)p) / Mmax); }   // data node of a data-node pointer
+  int64_t di(int32_t p) const { return (-2 - (int64_t)p) % Mmax; }      // its slot index
+
+  void reset_state() {
+    const size_t ns = (size_t)Sn() * I.MC;
+    up.assign(ns, NONE); down.assign(ns, NONE); tag.assign(ns, 0);
+    src_down.assign((size_t)K * Mmax, NONE); snk_up.assign((size_t)K * Mmax, NONE);
+    kacc.assign(Sn(), 0); deny.assign(Sn(), 0);
+    quiet = 0; round = 0;
+  }
+  // d(a, b); node -1-k = data node k (SRC side for a, SNK side for b)
+  int64_t d(int a, int b) const {
+    int32_t c = ABSENT;
+    if (a < 0 && b >= 0 && stage(b) == 0) c = srcK[(size_t)(-1 - a) * I.n + b % I.n];
+    else if (b < 0 && a >= 0 && stage(a) == I.S - 1) c = snkK[(size_t)(-1 - b) * I.n + a % I.n];
+    else if (a >= 0 && b >= 0 && stage(b) == stage(a) + 1) c = I.C(stage(a), b % I.n, a % I.n);
+    return c == ABSENT ? INF : (int64_t)c;
+  }
+  int node_of(int32_t p) const { return p >= 0 ? p / I.MC : -1 - dk(p); }  // relay or data node (-1-k)
+  void set_up_of(int32_t p, int32_t v) { if (p >= 0) up[p] = v; else snk_up[(size_t)dk(p) * Mmax + di(p)] = v; }
+  void set_down_of(int32_t p, int32_t v) { if (p >= 0) down[p] = v; else src_down[(size_t)dk(p) * Mmax + di(p)] = v; }
+  int64_t res_id_up(int32_t p) const { return p >= 0 ? p : (int64_t)Sn() * I.MC + (-2 - (int64_t)p); }
+  int64_t res_id_down(int32_t p) const { return p >= 0 ? p : (int64_t)Sn() * I.MC + (int64_t)K * Mmax + (-2 - (int64_t)p); }
+  uint64_t h(int gid, int stream) const {
+    return mix64(mix64(mix64(mix64(seed) ^ (uint64_t)inst) ^ (uint64_t)round) ^ ((uint64_t)gid * 4 + stream));
+  }
+
+  std::vector<int64_t> costs() const {  // R0, back to front
+    std::vector<int64_t> c((size_t)Sn() * I.MC, INF);
+    for (int s = I.S - 1; s >= 0; --s)
+      for (int i = 0; i < I.n; ++i) {
+        const int v = s * I.n + i;
+        for (int j = 0; j < capE(v); ++j) {
+          const int p = slot(v, j);
+          if (down[p] == NONE) c[p] = INF;
+          else if (down[p] <= -2) c[p] = d(v, -1 - dk(down[p]));
+          else c[p] = Rounds::sadd(d(v, down[p] / I.MC), c[down[p]]);
+        }
+      }
+    return c;
+  }
+  // adv(v, k) = min cost over v's OUT slots of tag k (INF if none)
+  int64_t adv(int v, int k, const std::vector<int64_t>& c) const {
+    int64_t best = INF;
+    if (!alive(v)) return best;
+    for (int j = 0; j < capE(v); ++j) {
+      const int p = slot(v, j);
+      if (st(p) == OUT && tag[p] == k && c[p] < best) best = c[p];
+    }
+    return best;
+  }
+  bool sink_free(int k) const {
+    for (int64_t i = 0; i < M[k]; ++i) if (snk_up[(size_t)k * Mmax + i] == NONE) return true;
+    return false;
+  }
+
+  int64_t one_round() {
+    const int S = I.S, n = I.n, Sn_ = Sn();
+    int64_t changes = 0;
+    {  // R0a: the lowest IN slot whose tag has an OUT slot takes its min-(cost, slot) OUT slot's downstream
+      const std::vector<int64_t> c0 = costs();
+      for (int v = 0; v < Sn_; ++v) {
+        if (!alive(v)) continue;
+        int x = -1, o = -1;
+        for (int j = 0; j < capE(v) && x < 0; ++j) {
+          const int p = slot(v, j);
+          if (st(p) != IN) continue;
+          int ob = -1;
+          for (int jj = 0; jj < capE(v); ++jj) {
+            const int q = slot(v, jj);
+            if (st(q) == OUT && tag[q] == tag[p] && (ob < 0 || c0[q] < c0[ob])) ob = q;
+          }
+          if (ob >= 0) { x = p; o = ob; }
+        }
+        if (x < 0) continue;
+        const int32_t cdn = down[o];
+        down[x] = cdn;
+        set_up_of(cdn, x);
+        down[o] = NONE;
+        ++changes;
+      }
+    }
+    const std::vector<int64_t> c = costs();
+    std::vector<int64_t> ad((size_t)Sn_ * K);
+    for (int v = 0; v < Sn_; ++v) for (int k = 0; k < K; ++k) ad[(size_t)v * K + k] = adv(v, k, c);
+    std::vector<char> sfree(K);
+    for (int k = 0; k < K; ++k) sfree[k] = sink_free(k);
+    // R1: requests (requester slot, target node or -1-k for D_k-sink, commodity)
+    std::vector<int32_t> rslot(Sn_, NONE), target(Sn_, INT32_MIN), rk(Sn_, -1);
+    std::vector<char> requested(Sn_, 0);
+    for (int r = 0; r < Sn_; ++r) {
+      if (!alive(r)) continue;
+      int xin = -1, xfree = -1;
+      bool has_out = false;
+      for (int j = 0; j < capE(r); ++j) {
+        const int p = slot(r, j), t = st(p);
+        if (t == IN && xin < 0) xin = p;
+        if (t == FREE && xfree < 0) xfree = p;
+        if (t == OUT) has_out = true;
+      }
+      int32_t rs = NONE;
+      if (xin >= 0) rs = xin;
+      else if (!has_out && xfree >= 0) rs = xfree;
+      if (rs == NONE) continue;
+      const int s = stage(r);
+      const int klo = xin >= 0 ? tag[xin] : 0, khi = xin >= 0 ? tag[xin] : K - 1;  // (a) own tag, (b) any
+      int best = INT32_MIN, bk = -1;
+      int64_t bestc = INF;
+      if (s == S - 1) {
+        for (int k = klo; k <= khi; ++k)
+          if (sfree[k] && d(r, -1 - k) != INF && d(r, -1 - k) < bestc) { bestc = d(r, -1 - k); best = -1 - k; bk = k; }
+      } else {
+        for (int jj = 0; jj < n; ++jj) {  // lowest j, then lowest k, on ties
+          const int j = (s + 1) * n + jj;
+          if (!alive(j) || d(r, j) == INF) continue;
+          for (int k = klo; k <= khi; ++k) {
+            const int64_t a = ad[(size_t)j * K + k];
+            if (a == INF) continue;
+            if (d(r, j) + a < bestc) { bestc = d(r, j) + a; best = j; bk = k; }
+          }
+        }
+      }
+      if (bk < 0) continue;  // no target: idle
+      rslot[r] = rs; target[r] = best; rk[r] = bk; requested[r] = 1;
+    }
+    // data nodes: D_k requests for its lowest unpaired SRC_k slot (stage-0 advertisers of tag k)
+    std::vector<int64_t> d_slot(K, -1);
+    std::vector<int> d_target(K, -1);
+    for (int k = 0; k < K; ++k) {
+      for (int64_t i = 0; i < M[k]; ++i) if (src_down[(size_t)k * Mmax + i] == NONE) { d_slot[k] = i; break; }
+      if (d_slot[k] < 0) continue;
+      int64_t bestc = INF;
+      for (int j = 0; j < n; ++j) {
+        const int64_t a = ad[(size_t)j * K + k];
+        if (alive(j) && d(-1 - k, j) != INF && a != INF && d(-1 - k, j) + a < bestc) { bestc = d(-1 - k, j) + a; d_target[k] = j; }
+      }
+    }
+    // R2 + R3: targets serve D_0..D_{K-1} then relays in gid order, per-tag OUT slots with cost == adv
+    {
+      std::vector<int> rank((size_t)Sn_ * K, 0);
+      auto eligible = [&](int j, int k, int q) -> int32_t {
+        int cnt = 0;
+        for (int jj = 0; jj < capE(j); ++jj) {
+          const int p = slot(j, jj);
+          if (st(p) == OUT && tag[p] == k && c[p] == ad[(size_t)j * K + k]) { if (cnt == q) return p; ++cnt; }
+        }
+        return NONE;
+      };
+      struct Grant { int req; int k; int32_t rs; int32_t ts; };
+      std::vector<Grant> grants;
+      for (int k = 0; k < K; ++k)
+        if (d_target[k] >= 0) {
+          const int j = d_target[k];
+          const int32_t ts = eligible(j, k, rank[(size_t)j * K + k]++);
+          if (ts != NONE) grants.push_back({-1, k, dptr(k, d_slot[k], Mmax), ts});
+        }
+      std::vector<size_t> snk_rank(K, 0);
+      std::vector<std::vector<int>> snk_free(K);
+      for (int k = 0; k < K; ++k)
+        for (int64_t i = 0; i < M[k]; ++i) if (snk_up[(size_t)k * Mmax + i] == NONE) snk_free[k].push_back((int)i);
+      for (int r = 0; r < Sn_; ++r) {
+        if (!requested[r]) continue;
+        const int k = rk[r];
+        if (target[r] < 0) {
+          if (snk_rank[k] < snk_free[k].size()) grants.push_back({r, k, rslot[r], dptr(k, snk_free[k][snk_rank[k]], Mmax)});
+          ++snk_rank[k];
+        } else {
+          const int j = target[r];
+          const int32_t ts = eligible(j, k, rank[(size_t)j * K + k]++);
+          if (ts != NONE) grants.push_back({r, k, rslot[r], ts});
+        }
+      }
+      for (const Grant& gr : grants) {
+        if (gr.req == -1) src_down[(size_t)dk(gr.rs) * Mmax + di(gr.rs)] = gr.ts;
+        else { down[gr.rs] = gr.ts; tag[gr.rs] = gr.k; deny[gr.req] = 0; }
+        if (gr.ts >= 0) up[gr.ts] = gr.rs;
+        else snk_up[(size_t)dk(gr.ts) * Mmax + di(gr.ts)] = gr.rs;
+        ++changes;
+      }
+    }
+    // R4 proposals by idle relays (post-R3 state); R5 reservations; R6 commits
+    std::vector<Proposal> props;
+    for (int p = 0; p < Sn_; ++p) {
+      if (!alive(p) || requested[p]) continue;
+      const int s = stage(p), i = p % n;
+      int xin = -1, zfree = -1;
+      bool has_out = false;
+      std::vector<int> Pl;
+      for (int j = 0; j < capE(p); ++j) {
+        const int q = slot(p, j), t = st(q);
+        if (t == IN && xin < 0) xin = q;
+        if (t == FREE && zfree < 0) zfree = q;
+        if (t == OUT) has_out = true;
+        if (t == PAIRED) Pl.push_back(q);
+      }
+      if (xin >= 0) {
+        deny[p] += 1;
+        if (deny[p] >= deny_after) {
+          Proposal pr;
+          pr.kind = 3; pr.gid = p; pr.key = (uint64_t)p; pr.x = xin;
+          pr.touched = {xin, res_id_up(up[xin])};
+          props.push_back(pr);
+        }
+        continue;
+      }
+      if (n < 2) continue;
+      uint32_t qi = pick(h(p, 0), (uint32_t)(n - 1));
+      if ((int)qi >= i) qi += 1;
+      const int q = s * n + (int)qi;
+      if (!alive(q)) continue;
+      std::vector<int> Q;
+      for (int j = 0; j < capE(q); ++j) if (st(slot(q, j)) == PAIRED) Q.push_back(slot(q, j));
+      if (Q.empty()) continue;
+      Proposal pr;
+      pr.gid = p;
+      int64_t delta;
+      if (zfree >= 0 && !has_out) {  // Redirect: z takes y's (up, down, tag)
+        const int y = Q[pick(h(p, 2), (uint32_t)Q.size())];
+        const int a = node_of(up[y]), cc = node_of(down[y]), b = q;
+        const int64_t dax = d(a, p), dxc = d(p, cc), dab = d(a, b), dbc = d(b, cc);
+        if (dax == INF || dxc == INF || dab == INF || dbc == INF) continue;
+        delta = (obj == ORC_OBJ_SUM) ? (dax + dxc) - (dab + dbc) : std::max(dax, dxc) - std::max(dab, dbc);
+        pr.kind = 2; pr.y = y; pr.z = zfree;
+        pr.touched = {y, res_id_up(up[y]), res_id_down(down[y]), zfree};
+      } else if (!Pl.empty()) {  // Change: both chains of the same data node
+        const int x = Pl[pick(h(p, 1), (uint32_t)Pl.size())];
+        const int y = Q[pick(h(p, 2), (uint32_t)Q.size())];
+        if (tag[x] != tag[y]) continue;
+        const int j1 = node_of(down[x]), j2 = node_of(down[y]);
+        if (j1 == j2) continue;
+        const int64_t dpj2 = d(p, j2), dqj1 = d(q, j1), dpj1 = d(p, j1), dqj2 = d(q, j2);
+        if (dpj2 == INF || dqj1 == INF || dpj1 == INF || dqj2 == INF) continue;
+        delta = (obj == ORC_OBJ_SUM) ? (dpj2 + dqj1) - (dpj1 + dqj2) : std::max(dpj2, dqj1) - std::max(dpj1, dqj2);
+        pr.kind = 1; pr.x = x; pr.y = y;
+        pr.touched = {x, y, res_id_down(down[x]), res_id_down(down[y])};
+      } else {
+        continue;
+      }
+      if (delta == 0) continue;
+      if (delta > 0 && !((h(p, 3) >> 32) < (uint64_t)ann.get(kacc[p], delta))) continue;
+      pr.key = ((uint64_t)(delta + (1ll << 40)) << 22) | (uint64_t)p;
+      props.push_back(pr);
+    }
+    const int64_t nres = (int64_t)Sn_ * I.MC + 2 * (int64_t)K * Mmax;
+    std::vector<uint64_t> res((size_t)nres, UINT64_MAX);
+    for (const Proposal& pr : props) for (int64_t t : pr.touched) res[t] = std::min(res[t], pr.key);
+    for (const Proposal& pr : props) {
+      bool win = true;
+      for (int64_t t : pr.touched) win = win && res[t] == pr.key;
+      if (!win) continue;
+      if (pr.kind == 1) {
+        const int32_t dx = down[pr.x], dy = down[pr.y];
+        down[pr.x] = dy; down[pr.y] = dx;
+        set_up_of(dy, pr.x); set_up_of(dx, pr.y);
+        kacc[pr.gid] += 1;
+      } else if (pr.kind == 2) {
+        const int32_t a = up[pr.y], cc = down[pr.y];
+        up[pr.z] = a; down[pr.z] = cc; tag[pr.z] = tag[pr.y];
+        set_down_of(a, pr.z); set_up_of(cc, pr.z);
+        up[pr.y] = NONE; down[pr.y] = NONE;
+        kacc[pr.gid] += 1;
+      } else if (pr.kind == 3) {
+        const int32_t a = up[pr.x];
+        up[pr.x] = NONE;
+        set_down_of(a, NONE);
+        deny[pr.gid] = 0;
+      }
+      ++changes;
+    }
+    quiet = changes > 0 ? 0 : quiet + 1;
+    round += 1;
+    return changes;
+  }
+
+  void result(int64_t* F_dec, int64_t* cost_dec, int32_t* dangling) const {
+    for (int k = 0; k < K; ++k) {
+      int64_t F = 0, C = 0;
+      for (int64_t i = 0; i < M[k]; ++i) {
+        int32_t p = src_down[(size_t)k * Mmax + i];
+        if (p == NONE) continue;
+        int64_t cc = d(-1 - k, p / I.MC);
+        int guard = 0;
+        while (p >= 0 && ++guard <= I.S + 1) {
+          const int32_t nx = down[p];
+          if (nx == NONE) { cc = -1; break; }
+          cc = Rounds::sadd(cc, nx <= -2 ? d(p / I.MC, -1 - dk(nx)) : d(p / I.MC, nx / I.MC));
+          p = nx;
+        }
+        if (cc >= 0 && cc != INF && p <= -2 && dk(p) == k) { F += 1; C += cc; }
+      }
+      F_dec[k] = F;
+      cost_dec[k] = C;
+    }
+    int32_t dang = 0;
+    for (size_t p = 0; p < up.size(); ++p) if (st((int)p) == OUT) ++dang;
+    *dangling = dang;
+  }
+
+  // digest: per slot (state, enc(up), enc(down), tag + 1 if not FREE else 0); SRC_k / SNK_k in
+  // (k, i) order; (kacc, deny) per relay; quiet.  enc: relay slot 1 + p, SRC_k i 2^40 + k 2^20 + i,
+  // SNK_k i 2^41 + k 2^20 + i, none 0
+  uint64_t digest() const {
+    uint64_t dg = 0, pos = 0;
+    auto add = [&](uint64_t val) { dg += mix64(mix64(pos) ^ val); ++pos; };
+    auto enc = [&](int32_t p, uint64_t side) -> uint64_t {
+      return p == NONE ? 0 : p >= 0 ? 1 + (uint64_t)p : side + ((uint64_t)dk(p) << 20) + (uint64_t)di(p);
+    };
+    for (size_t p = 0; p < up.size(); ++p) {
+      const int s = st((int)p);
+      add((uint64_t)s); add(enc(up[p], 1ull << 40)); add(enc(down[p], 1ull << 41));
+      add(s == FREE ? 0 : (uint64_t)tag[p] + 1);
+    }
+    for (int k = 0; k < K; ++k)
+      for (int64_t i = 0; i < Mmax; ++i) add(src_down[(size_t)k * Mmax + i] == NONE ? 0 : 1 + (uint64_t)src_down[(size_t)k * Mmax + i]);
+    for (int k = 0; k < K; ++k)
+      for (int64_t i = 0; i < Mmax; ++i) add(snk_up[(size_t)k * Mmax + i] == NONE ? 0 : 1 + (uint64_t)snk_up[(size_t)k * Mmax + i]);
+    for (int g = 0; g < Sn(); ++g) { add((uint64_t)(uint32_t)kacc[g]); add((uint64_t)(uint32_t)deny[g]); }
+    add((uint64_t)(uint32_t)quiet);
+    return dg;
+  }
+};
+struct orc_mc_rounds { McRounds R; };
+
 
 extern "C" {
 
@@ -1396,5 +1749,60 @@ int orc_pipeline_batch(int64_t B, int32_t S, int32_t n, int32_t max_cap, const i
   });
   return err.load() ? -1 : 0;
 }
+
+// ---- multi-data-node rounds (MC-SYNC) ----
+orc_mc_rounds* orc_mc_rounds_create(const orc_instance* I, int32_t K, const int32_t* src_k, const int32_t* snk_k,
+                                    const int64_t* M_k, uint64_t seed, int64_t inst_id, double T0, double alpha,
+                                    int32_t objective, int32_t W, int32_t deny_after) {
+  if (!I || K < 1 || I->S < 1 || I->n < 1 || W < 1 || deny_after < 1) return nullptr;
+  orc_mc_rounds* o = new orc_mc_rounds();
+  McRounds& R = o->R;
+  R.I = Inst(I);
+  R.K = K;
+  R.M.assign(M_k, M_k + K);
+  R.Mmax = 1;
+  for (int k = 0; k < K; ++k) R.Mmax = std::max<int64_t>(R.Mmax, R.M[k]);
+  R.srcK.assign(src_k, src_k + (size_t)K * I->n);
+  R.snkK.assign(snk_k, snk_k + (size_t)K * I->n);
+  R.seed = seed; R.inst = inst_id; R.obj = objective; R.W = W; R.deny_after = deny_after;
+  if (R.ann.init(T0, alpha)) { delete o; return nullptr; }
+  R.reset_state();
+  return o;
+}
+void orc_mc_rounds_destroy(orc_mc_rounds* o) { delete o; }
+int orc_mc_rounds_run(orc_mc_rounds* o, int32_t max_rounds, int32_t* rounds_run, int64_t* F_dec, int64_t* cost_dec,
+                      int32_t* dangling, uint64_t* digests) {
+  McRounds& R = o->R;
+  R.quiet = 0;
+  int32_t r = 0;
+  while (r < max_rounds) {
+    R.one_round();
+    if (digests) digests[r] = R.digest();
+    ++r;
+    if (R.quiet >= R.W) break;
+  }
+  if (rounds_run) *rounds_run = r;
+  std::vector<int64_t> f(R.K), c(R.K);
+  int32_t dg = 0;
+  R.result(f.data(), c.data(), &dg);
+  for (int k = 0; k < R.K; ++k) { if (F_dec) F_dec[k] = f[k]; if (cost_dec) cost_dec[k] = c[k]; }
+  if (dangling) *dangling = dg;
+  return 0;
+}
+int orc_mc_rounds_export(const orc_mc_rounds* o, int32_t* up, int32_t* down, int32_t* tag, int32_t* src_down,
+                         int32_t* snk_up, int32_t* kacc, int32_t* deny, int32_t* quiet, int64_t* round) {
+  const McRounds& R = o->R;
+  if (up) std::copy(R.up.begin(), R.up.end(), up);
+  if (down) std::copy(R.down.begin(), R.down.end(), down);
+  if (tag) for (size_t p = 0; p < R.tag.size(); ++p) tag[p] = R.st((int)p) == FREE ? -1 : R.tag[p];
+  if (src_down) std::copy(R.src_down.begin(), R.src_down.end(), src_down);
+  if (snk_up) std::copy(R.snk_up.begin(), R.snk_up.end(), snk_up);
+  if (kacc) std::copy(R.kacc.begin(), R.kacc.end(), kacc);
+  if (deny) std::copy(R.deny.begin(), R.deny.end(), deny);
+  if (quiet) *quiet = R.quiet;
+  if (round) *round = R.round;
+  return 0;
+}
+uint64_t orc_mc_rounds_digest(const orc_mc_rounds* o) { return o->R.digest(); }
 
 }  // extern "C"

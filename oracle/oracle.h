@@ -110,6 +110,24 @@ int orc_rounds_instance(const orc_rounds* R, int32_t* cap_eff, uint8_t* alive, i
 /* LLaMA "crash during backward" victim rule; returns victim gid or -1. */
 int32_t orc_llama_victim(const orc_rounds* R, uint64_t draw_stage, uint64_t draw_pick);
 
+/* ---- multi-data-node decentralized rounds, MC-SYNC ----
+ * K data nodes with source / sink costs src_k / snk_k [K][n] and supplies M_k [K] on the shared
+ * relays and links of I (I->src / I->snk / I->M are ignored).  Every non-FREE slot carries the
+ * data node of its chain; requests, grants, Change and self-pairing stay within one data node.
+ * Rounds from the empty state; F_dec / cost_dec [K]; digests per round (optional).  Pointers:
+ * relay slot >= 0, -1 none, data-node slot i of D_k = -2 - (k * Mmax + i), Mmax = max_k M_k. */
+typedef struct orc_mc_rounds orc_mc_rounds;
+orc_mc_rounds* orc_mc_rounds_create(const orc_instance* I, int32_t K, const int32_t* src_k, const int32_t* snk_k,
+                                    const int64_t* M_k, uint64_t seed, int64_t inst_id, double T0, double alpha,
+                                    int32_t objective, int32_t W, int32_t deny_after);
+void orc_mc_rounds_destroy(orc_mc_rounds* R);
+int orc_mc_rounds_run(orc_mc_rounds* R, int32_t max_rounds, int32_t* rounds_run, int64_t* F_dec, int64_t* cost_dec,
+                      int32_t* dangling, uint64_t* digests);
+/* up/down/tag [S][n][max_cap] (tag -1 on FREE slots), src_down/snk_up [K][Mmax], kacc/deny [S][n] */
+int orc_mc_rounds_export(const orc_mc_rounds* R, int32_t* up, int32_t* down, int32_t* tag, int32_t* src_down,
+                         int32_t* snk_up, int32_t* kacc, int32_t* deny, int32_t* quiet, int64_t* round);
+uint64_t orc_mc_rounds_digest(const orc_mc_rounds* R);
+
 /* Whole per-instance workload of one bench step, for the cpu_baseline and
  * the full-size parity samples: pre-churn rounds to quiescence, churn, cold SSP on
  * the masked graph, repair rounds.  churn_kind 0 none, 1 random (alive_new +

@@ -677,6 +677,54 @@ gwtf_status gwtf_flow_export_round_state(gwtf_flow_t h, int32_t* up, int32_t* do
   return GWTF_OK;
 }
 
+gwtf_status gwtf_mc_rounds(int32_t B, int32_t S, int32_t n, int32_t max_cap, int32_t K, const int32_t* cap,
+                           const uint8_t* alive, const int32_t* link_cost, const int32_t* src_cost,
+                           const int32_t* snk_cost, const int64_t* supply, uint64_t seed, int64_t inst_base, double T0,
+                           double alpha, int32_t objective, int32_t steady_window, int32_t deny_after,
+                           int32_t max_rounds, int32_t* rounds_run, int64_t* dec_flow, int64_t* dec_cost,
+                           int32_t* dangling, uint64_t* round_digests, int32_t* up, int32_t* down, int32_t* tag,
+                           void* stream) {
+  if (B < 1 || S < 1 || n < 1 || K < 1 || max_cap < 0 || max_cap > 32 || max_rounds < 0 || steady_window < 1 ||
+      deny_after < 1 || (objective != GWTF_OBJ_SUM && objective != GWTF_OBJ_MINIMAX))
+    return fail(GWTF_E_INVALID, "mc_rounds: shape / parameter out of range");
+  if (!cap || !src_cost || !snk_cost || !supply || (S > 1 && !link_cost) || !rounds_run || !dec_flow || !dec_cost ||
+      !dangling)
+    return fail(GWTF_E_INVALID, "mc_rounds: NULL required array");
+  if ((up || down || tag) && !(up && down && tag)) return fail(GWTF_E_INVALID, "mc_rounds: up/down/tag all or none");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int64_t> sup((size_t)K * B);
+  if (cudaMemcpyAsync(sup.data(), supply, sup.size() * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return fail(GWTF_E_CUDA, "mc_rounds: supply readback");
+  int64_t mmax = 1;
+  for (int64_t m : sup) {
+    if (m < 0 || m > (1 << 20)) return fail(GWTF_E_INVALID, "mc_rounds: supply outside [0, 2^20]");
+    mmax = std::max(mmax, m);
+  }
+  const size_t smem = mc_rounds_smem(S, n, max_cap, K, (int)mmax);
+  if (smem > 227 * 1024) return fail(GWTF_E_UNSUPPORTED, "mc_rounds: instance state exceeds shared memory");
+  std::vector<uint32_t> thr;
+  int32_t width = 1, Kt = 0;
+  if (gwtf_status s = anneal_table(T0, alpha, thr, width, Kt); s != GWTF_OK) return s;
+  uint32_t* thr_d = nullptr;
+  if (cudaMallocAsync(&thr_d, thr.size() * 4, st) != cudaSuccess) return fail(GWTF_E_NOMEM, "mc_rounds: thr");
+  cudaMemcpyAsync(thr_d, thr.data(), thr.size() * 4, cudaMemcpyHostToDevice, st);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  McRoundsCall c{};
+  c.B = B; c.S = S; c.n = n; c.MC = max_cap; c.K = K; c.Mmax = (int32_t)mmax;
+  c.cap = cap; c.alive = alive; c.tile = link_cost; c.ld = n; c.src = src_cost; c.snk = snk_cost; c.supply = supply;
+  c.seed = seed; c.inst_base = inst_base; c.objective = objective; c.W = steady_window; c.deny_after = deny_after;
+  c.max_rounds = max_rounds; c.thr = thr_d; c.thr_width = width; c.thr_K = Kt;
+  c.rounds_run = rounds_run; c.F_dec = dec_flow; c.cost_dec = dec_cost; c.dangling = dangling;
+  c.digests = round_digests; c.up_out = up; c.down_out = down; c.tag_out = tag;
+  const cudaError_t e = launch_mc_rounds(c, st, sms);
+  cudaFreeAsync(thr_d, st);
+  if (e != cudaSuccess) return fail(GWTF_E_CUDA, cudaGetErrorString(e));
+  return GWTF_OK;
+}
+
 gwtf_status gwtf_flow_import_round_state(gwtf_flow_t h, const int32_t* up, const int32_t* down,
                                          const int32_t* src_down, const int32_t* snk_up, const int32_t* kacc,
                                          const int32_t* deny, const int32_t* quiet, const int64_t* round) {

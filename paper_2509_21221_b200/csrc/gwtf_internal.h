@@ -116,6 +116,18 @@ cudaError_t launch_addition_build(int32_t S, int32_t n, const int32_t* cap, cons
                                   int32_t* snk_o, int32_t* link_o, cudaStream_t st);
 cudaError_t launch_addition_select(int64_t count, const int64_t* F, const int64_t* cost, int64_t* best, cudaStream_t st);
 cudaError_t launch_greedy(const Problem& P, int32_t* rem, int64_t* F, int64_t* cost, cudaStream_t st);
+// multi-data-node rounds (mc_rounds.cu): one stateless call over a batch
+struct McRoundsCall {
+  int32_t B, S, n, MC, K, Mmax;
+  const int32_t* cap; const uint8_t* alive; const int32_t* tile; int32_t ld;
+  const int32_t* src; const int32_t* snk; const int64_t* supply;
+  uint64_t seed; int64_t inst_base; int32_t objective, W, deny_after, max_rounds;
+  const uint32_t* thr; int32_t thr_width, thr_K;
+  int32_t* rounds_run; int64_t* F_dec; int64_t* cost_dec; int32_t* dangling; uint64_t* digests;
+  int32_t *up_out, *down_out, *tag_out;
+};
+size_t mc_rounds_smem(int S, int n, int MC, int K, int Mmax);
+cudaError_t launch_mc_rounds(const McRoundsCall& c, cudaStream_t st, int num_sms);
 size_t warm_ws_bytes(const Problem& P, int grid);
 int warm_grid(const Problem& P);
 cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* arc, int32_t* snk_f, void* ws,

@@ -58,3 +58,40 @@ def multi_source_ssp_unit(cap, alive, link_cost, src_costs, snk_costs, supplies,
             NF[k] += nf
             active[k] = active[k] & routed & (F[k] < supplies[k])
     return [(F[k], C[k], NF[k]) for k in range(K)]
+
+
+def mc_rounds(cap, alive, link_cost, src_costs, snk_costs, supplies, *, max_cap: int, max_rounds: int, seed=0,
+              inst_base=0, T0=1.7, alpha=0.95, objective=0, steady_window=5, deny_after=3, digests=False,
+              state=False, stream=None):
+    """Multi-data-node decentralized rounds (gwtf_mc_rounds): K data
+    nodes with src_costs / snk_costs (K tensors [B][n] int32) and supplies (K tensors [B] int64) on the
+    shared relays and links; rounds from the empty state.  Returns a dict: rounds [B], F_dec / cost_dec
+    [K][B], dangling [B], digests [B][max_rounds] (if asked), up / down / tag [B][S][n][max_cap] (if
+    state)."""
+    import ctypes
+
+    from ._lib import check, lib
+    B, S, n = cap.shape
+    K = len(supplies)
+    dev = cap.device
+    src = torch.stack(list(src_costs)).to(torch.int32).contiguous()
+    snk = torch.stack(list(snk_costs)).to(torch.int32).contiguous()
+    sup = torch.stack(list(supplies)).to(torch.int64).contiguous()
+    out = dict(rounds=torch.empty(B, dtype=torch.int32, device=dev),
+               F_dec=torch.empty((K, B), dtype=torch.int64, device=dev),
+               cost_dec=torch.empty((K, B), dtype=torch.int64, device=dev),
+               dangling=torch.empty(B, dtype=torch.int32, device=dev))
+    if digests:
+        out["digests"] = torch.zeros((B, max(max_rounds, 1)), dtype=torch.int64, device=dev)
+    if state:
+        for k in ("up", "down", "tag"):
+            out[k] = torch.empty((B, S, n, max_cap), dtype=torch.int32, device=dev)
+    p = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    link = link_cost.contiguous() if S > 1 else None
+    check("gwtf_mc_rounds", lib().gwtf_mc_rounds(
+        B, S, n, max_cap, K, p(cap.contiguous()), p(alive.contiguous() if alive is not None else None), p(link),
+        p(src), p(snk), p(sup), seed, inst_base, T0, alpha, objective, steady_window, deny_after, max_rounds,
+        p(out["rounds"]), p(out["F_dec"]), p(out["cost_dec"]), p(out["dangling"]), p(out.get("digests")),
+        p(out.get("up")), p(out.get("down")), p(out.get("tag")), ctypes.c_void_p(st.cuda_stream)))
+    return out
