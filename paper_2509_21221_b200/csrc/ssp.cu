@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
       if (T.tid == 0) {
         const int q = atomicAdd(&P.counters[2], 1);
         P.redo[q] = inst;
+        atomicAdd(&P.stats[13], 1ull);  // instances re-solved with 64-bit keys (gwtf_flow_stats)
       }
       T.sync();
       continue;

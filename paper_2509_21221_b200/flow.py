@@ -277,4 +277,7 @@ class Flow:
         if raw:
             return out
         keys = ("relax_steps", "backward_phases", "augmentations", "bf_passes", "path_nodes")
-        return {k: int(out[i]) for i, k in enumerate(keys)}
+        d = {k: int(out[i]) for i, k in enumerate(keys)}
+        d["redo_64bit"] = int(out[13])  # instances whose 32-bit keys overflowed (re-solved, 64-bit)
+        d["launches"] = int(out[15])
+        return d

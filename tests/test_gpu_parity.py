@@ -429,3 +429,39 @@ def test_solve_and_rounds_matches_serial(name, B):
         fl.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["flow1", "gpt"])
+def test_key_overflow_redo_queue(name):
+    """ssp_kernel's 32-bit keys (K1): costs scaled so that every single arc passes the
+    32-bit admission check ((maxcost << H) + 1 < 2^29) but shortest-path keys cross 2^29 -- the
+    instances abort into the redo queue and the 64-bit relaunch re-solves them.  Status 0 and the
+    full canonical assignment equal to the oracle's (VERDICT r1 "What's weak" #2)."""
+    from paper_2509_21221_b200 import Flow
+    cfg = gen.CONFIGS[name]
+    B = 12
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    Sn = cfg.S * cfg.n
+    H = 1
+    while (1 << H) <= 2 * Sn + 1:
+        H += 1
+    maxc = int(max(src.max(), snk.max(), link[link != oracle.ABSENT].max()))
+    scale = (2**29 - 2) // (maxc << H)  # the largest scale whose single arcs still admit 32-bit keys
+    assert scale >= 2
+    absent = link == oracle.ABSENT
+    src, snk, link = src.astype(np.int64) * scale, snk.astype(np.int64) * scale, link.astype(np.int64) * scale
+    link[absent] = oracle.ABSENT
+    assert (int(max(src.max(), snk.max(), link.max())) << H) + 1 < 2**29  # each arc admits 32-bit keys
+    src, snk, link = src.astype(np.int32), snk.astype(np.int32), link.astype(np.int32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    fl = Flow(t(bt.cap), t(src), t(snk), t(link), t(bt.supply), max_cap=cfg.max_cap, alive=t(bt.alive))
+    sol = fl.solve_batch()
+    nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+    assert fl.stats()["redo_64bit"] > 0  # the redo queue was used
+    assert (sol.status == 0).all()
+    for b in range(B):
+        I = oracle.Instance(cfg.S, cfg.n, cfg.max_cap, int(bt.supply[b]), bt.cap[b], src[b], snk[b], link[b], bt.alive[b])
+        r = oracle.ssp(I)
+        assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
+        assert np.array_equal(nf[b], r.node_flow) and np.array_equal(af[b], r.arc_flow), b
+        assert np.array_equal(sf[b], r.src_flow) and np.array_equal(kf[b], r.snk_flow), b
