@@ -83,24 +83,37 @@ gwtf_status cuda_fail(gwtf_flow_s* h, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail((h), _e, #expr);  \
   } while (0)
 
-// Device memory of a handle comes from the device's stream-ordered pool (cudaMallocAsync on the
-// handle's stream): creating and destroying handles back to back (the e2e pipeline, node-addition
-// batches, multi-source turns) then reuses pool memory instead of paying cudaMalloc/cudaFree,
-// whose unmap synchronises the device.  The pool keeps up to kPoolKeep bytes across handles.
-constexpr uint64_t kPoolKeep = 8ull << 30;
+// Device memory of a handle comes from the library's own stream-ordered pool (one per device,
+// cudaMallocFromPoolAsync on the handle's stream): creating and destroying handles back to back (the
+// e2e pipeline, node-addition batches, multi-source turns) reuses pool memory instead of paying
+// cudaMalloc / cudaFree, whose unmap synchronises the device.  A private pool leaves the device's
+// default pool (and other libraries' settings) alone; it keeps up to kPoolKeep bytes after a
+// synchronisation, so a large handle's memory (stress: GBs) goes back to the device.
+constexpr uint64_t kPoolKeep = 1ull << 30;
 void* dev_alloc(gwtf_flow_s* h, size_t bytes) {
-  static bool configured[64] = {};
-  if (h->device >= 0 && h->device < 64 && !configured[h->device]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
-      uint64_t keep = kPoolKeep;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  static cudaMemPool_t pools[64] = {};
+  static bool tried[64] = {};
+  cudaMemPool_t pool = nullptr;
+  if (h->device >= 0 && h->device < 64) {
+    if (!tried[h->device]) {
+      tried[h->device] = true;
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = h->device;
+      if (cudaMemPoolCreate(&pools[h->device], &props) == cudaSuccess) {
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(pools[h->device], cudaMemPoolAttrReleaseThreshold, &keep);
+      } else {
+        pools[h->device] = nullptr;
+      }
+      cudaGetLastError();
     }
-    cudaGetLastError();
-    configured[h->device] = true;
+    pool = pools[h->device];
   }
   void* q = nullptr;
-  if (cudaMallocAsync(&q, bytes, h->stream) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  const cudaError_t e = pool ? cudaMallocFromPoolAsync(&q, bytes, pool, h->stream) : cudaMallocAsync(&q, bytes, h->stream);
+  if (e != cudaSuccess) { cudaGetLastError(); return nullptr; }
   return q;
 }
 void dev_free(gwtf_flow_s* h, void* p) {

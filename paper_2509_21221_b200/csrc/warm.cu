@@ -76,6 +76,24 @@ __device__ ArcV arc_of(const WarmCtx& c, int64_t e) {
   return a;
 }
 
+// the id of the idx-th forward arc in layer order: src arcs, then per stage s its node arcs and
+// (s < S-1) its outgoing link arcs, then the snk arcs -- a pass over the arcs in this order (or in
+// reverse) carries a label update through every stage at once
+__device__ __forceinline__ int64_t layered_arc(const WarmCtx& c, int64_t idx) {
+  const int n = c.n;
+  if (idx < n) return idx;
+  idx -= n;
+  const int64_t blk = (int64_t)n + (int64_t)n * n;  // one stage: n node arcs + n^2 link arcs
+  const int64_t full = (int64_t)(c.S - 1) * blk;
+  if (idx < full) {
+    const int64_t s = idx / blk, r = idx - s * blk;
+    return r < n ? n + s * n + r : n + (int64_t)c.S * n + s * n * n + (r - n);
+  }
+  idx -= full;
+  if (idx < n) return n + (int64_t)(c.S - 1) * n + idx;  // node arcs of the last stage
+  return idx - n + n + (int64_t)c.S * n + (int64_t)(c.S - 1) * n * n;  // snk arcs
+}
+
 // labels are lowered by global atomics (performed at L2): read them around the L1
 __device__ __forceinline__ uint64_t ld_lab(const uint64_t* p) { return *(const volatile uint64_t*)p; }
 __device__ __forceinline__ int64_t lab_dist(uint64_t L) { return (int64_t)(L >> kArcBits) - kBias; }
@@ -414,7 +432,11 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
       if (threadIdx.x == 0) changed_sm = 0;
       __syncthreads();
       int ch = 0;
-      for (int64_t r = threadIdx.x; r < 2 * E; r += blockDim.x) {
+      // passes alternate the sweep direction (arc ids run stage by stage): forward and backward
+      // chains of label updates each propagate within one pass
+      for (int64_t rr = threadIdx.x; rr < 2 * E; rr += blockDim.x) {
+        const int64_t q = (passes & 1) ? 2 * E - 1 - rr : rr;  // layered order, alternating direction
+        const int64_t r = 2 * layered_arc(c, q >> 1) + (q & 1);
         const ArcV a = arc_of(c, r >> 1);
         const int64_t xk = *a.x < a.cap ? *a.x : a.cap;  // the kept flow
         int from, to;
@@ -504,7 +526,9 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
         if (threadIdx.x == 0) changed_sm = 0;
         __syncthreads();
         int ch = 0;
-        for (int64_t r = threadIdx.x; r < nr_now; r += blockDim.x) {
+        for (int64_t rr = threadIdx.x; rr < nr_now; rr += blockDim.x) {
+          const int64_t q = (sp & 1) ? nr_now - 1 - rr : rr;  // layered order, alternating direction
+          const int64_t r = q >= 2 * E ? q : 2 * layered_arc(c, q >> 1) + (q & 1);
           int from, to, sign;
           int64_t rcap, rcost;
           int32_t* xp;

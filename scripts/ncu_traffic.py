@@ -25,15 +25,17 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[0]
 ki, kr, kw, kt = (hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum"),
                   hdr.index("gpu__time_duration.sum"))
-unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 units = rows[1]
 acc = {}
 for r in rows[2:]:
-    m = re.search(r"(ssp_cluster_kernel|ssp_kernel|rounds_kernel|churn_state_kernel|edge_update_kernel)", r[ki])
+    m = re.search(r"(ssp_cluster_kernel|ssp_kernel|rounds_cluster_kernel|rounds_kernel|churn_state_kernel|"
+                  r"edge_update_kernel|warm_kernel|mc_rounds_kernel)", r[ki])
     if not m:
         continue
+    name = {"rounds_cluster_kernel": "rounds_kernel"}.get(m.group(1), m.group(1))  # the library's names
     b = float(r[kr].replace(",", "")) * unit[units[kr]] + float(r[kw].replace(",", "")) * unit[units[kw]]
-    a = acc.setdefault(prefix + m.group(1), [0.0, 0, 0.0])
+    a = acc.setdefault(prefix + name, [0.0, 0, 0.0])
     a[0] += b
     a[1] += 1
     a[2] += float(r[kt].replace(",", ""))
