@@ -20,6 +20,7 @@
 //   e in [n+Sn+(S-1)n^2, E)          snk arc     out(S-1,i) -> D      cap M, cost snk[i]
 // Nodes: 0 = s*, 1 = t*, in(s,i) = 2 + 2(s n + i), out(s,i) = in(s,i) + 1.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "gwtf_internal.h"
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) klein_kernel(const Problem P, int32_
   const int N = 2 + 2 * S * n;
   const int64_t E = 2ll * n + (int64_t)S * n + (int64_t)(S - 1) * n * n;
   for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
-    if (status_out[b] != 7) continue;  // solved by warm_kernel
+    if (status_out[b] != 7 && (status_out[b] < 70 || status_out[b] > 79)) continue;  // solved by the repair
     WarmCtx c;
     c.S = S; c.n = n; c.ld = P.ld; c.N = N; c.E = E; c.M = P.supply[b];
     c.tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
@@ -635,6 +636,359 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// The same potential-carrying repair with the instance in shared memory (round 2): labels, preds,
+// potentials, imbalances, node / src / snk flows and the link flows (int16) of one instance per
+// CTA, the link costs read through L1; every Bellman-Ford pass is a layered sweep -- forward arcs
+// stage by stage (s* -> in_0, in -> out, out_s -> in_{s+1} as one row minimum per destination,
+// out_{S-1} -> t*, the bypass), then reverse arcs back to front -- one block barrier per layer, so a
+// pass carries a label across every stage in one direction.  Labels are (distance, pred node):
+// the arc between two adjacent nodes is unique, so the pred node names it.  Same phases P, C, V,
+// A, B as warm_kernel; an instance that does not fit (or whose kept flow has a negative cycle) is
+// left to the next kernel with status 7.
+constexpr int64_t kDInf = INT64_MAX / 4;
+struct WsLayout { size_t dist, pi, pred, imb, g, srcf, snkf, arcf, red, total; };
+__host__ __device__ inline WsLayout ws_layout(int S, int n) {
+  WsLayout L;
+  const size_t N = 2 + 2 * (size_t)S * n, Sn = (size_t)S * n, A = (size_t)(S > 1 ? S - 1 : 0) * n * n;
+  size_t o = 0;
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  L.dist = o; o += al(N * 8);
+  L.pi = o; o += al(N * 8);
+  L.pred = o; o += al(N * 4);
+  L.imb = o; o += al(N * 4);
+  L.g = o; o += al(Sn * 4);
+  L.srcf = o; o += al((size_t)n * 4);
+  L.snkf = o; o += al((size_t)n * 4);
+  L.arcf = o; o += al(A * 2);
+  L.red = o; o += 64;
+  L.total = o;
+  return L;
+}
+
+__global__ void __launch_bounds__(kThreads) warm_smem_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
+                                                             int32_t* arc_all, int32_t* snk_f_all, int64_t* F_out,
+                                                             int64_t* cost_out, int64_t* stats_out, int32_t* status_out) {
+  extern __shared__ __align__(16) uint8_t wsm[];
+  const int S = P.S, n = P.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = kThreads / 32;
+  const int N = 2 + 2 * S * n, Sn = S * n;
+  const WsLayout L = ws_layout(S, n);
+  int64_t* dist = (int64_t*)(wsm + L.dist);
+  int64_t* pi = (int64_t*)(wsm + L.pi);
+  int32_t* pred = (int32_t*)(wsm + L.pred);
+  int32_t* imb = (int32_t*)(wsm + L.imb);
+  int32_t* g = (int32_t*)(wsm + L.g);
+  int32_t* srcf = (int32_t*)(wsm + L.srcf);
+  int32_t* snkf = (int32_t*)(wsm + L.snkf);
+  int16_t* arcf = (int16_t*)(wsm + L.arcf);
+  unsigned long long* red = (unsigned long long*)(wsm + L.red);
+  int* ired = (int*)(red + 4);
+  auto IN = [&](int s, int i) { return 2 + 2 * (s * n + i); };
+  for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
+    const int32_t* tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
+    const int32_t* src = P.src + (size_t)b * n;
+    const int32_t* snk = P.snk + (size_t)b * n;
+    const int32_t* cap = P.cap + (size_t)b * Sn;
+    const uint8_t* alive = P.alive + (size_t)b * Sn;
+    const uint8_t* alive_prev = P.alive_prev + (size_t)b * Sn;
+    int32_t* gG = g_all + (size_t)b * Sn;
+    int32_t* sG = src_f_all + (size_t)b * n;
+    int32_t* kG = snk_f_all + (size_t)b * n;
+    int32_t* aG = arc_all + (size_t)b * (S - 1) * n * n;
+    const int64_t M = P.supply[b];
+    auto capE = [&](int k) -> int32_t { return alive[k] ? cap[k] : 0; };
+    auto C = [&](int s, int u, int v) -> int32_t { return __ldg(&tile[((size_t)s * n + v) * P.ld + u]); };
+    // ---- load, cut (units the churned graph cannot carry), BIG ----
+    if (tid == 0) { red[0] = 0; red[1] = 0; red[2] = 0; ired[0] = 0; ired[2] = 0; ired[3] = 0; }
+    for (int k = tid; k < N; k += kThreads) imb[k] = 0;
+    __syncthreads();
+    long long cut = 0, F0 = 0;
+    int32_t maxc = 0, bigf = 0;
+    for (int k = tid; k < n; k += kThreads) {
+      int32_t x = sG[k];
+      const int32_t c = src[k];
+      if (c != kAbsent && c > maxc) maxc = c;
+      F0 += x;
+      if (c == kAbsent && x > 0) { atomicAdd(&imb[0], x); atomicSub(&imb[IN(0, k)], x); cut += x; x = 0; }
+      srcf[k] = x;
+      int32_t y = kG[k];
+      const int32_t d = snk[k];
+      if (d != kAbsent && d > maxc) maxc = d;
+      if (d == kAbsent && y > 0) { atomicAdd(&imb[IN(S - 1, k) + 1], y); atomicSub(&imb[1], y); cut += y; y = 0; }
+      snkf[k] = y;
+    }
+    for (int k = tid; k < Sn; k += kThreads) {
+      int32_t x = gG[k];
+      const int32_t ce = capE(k);
+      if (x > ce) { atomicAdd(&imb[2 + 2 * k], x - ce); atomicSub(&imb[3 + 2 * k], x - ce); cut += x - ce; x = ce; }
+      g[k] = x;
+    }
+    for (int64_t e = tid; e < (int64_t)(S - 1) * n * n; e += kThreads) {
+      const int s = (int)(e / ((int64_t)n * n)), r = (int)(e - (int64_t)s * n * n), v = r / n, u = r - v * n;
+      int32_t x = aG[e];
+      const int32_t c = C(s, u, v);
+      if (c != kAbsent && c > maxc) maxc = c;
+      if (x > 32767) bigf = 1;
+      if (c == kAbsent && x > 0) { atomicAdd(&imb[IN(s, u) + 1], x); atomicSub(&imb[IN(s + 1, v)], x); cut += x; x = 0; }
+      arcf[e] = (int16_t)x;
+    }
+    atomicAdd(&red[0], (unsigned long long)F0);
+    atomicMax(&red[1], (unsigned long long)maxc);
+    if (bigf) atomicOr(&ired[0], 1);
+    __syncthreads();
+    const int64_t big = (2 * (int64_t)S * n + 2) * (int64_t)red[1] + 1;
+    int64_t byp = M - (int64_t)red[0];
+    if (ired[0] || M > 32767 || big >= (1ll << 40)) {  // int16 link flows / label range: next kernel
+      if (tid == 0) status_out[b] = 70;
+      __syncthreads();
+      continue;
+    }
+    // ---- one layered Bellman-Ford pass ----
+    // mode 0: potentials (real costs, rejoined relays' node arcs and the bypass left out);
+    // mode 1: reduced costs, bypass forward allowed (phase A); mode 2: reduced costs, no bypass (B)
+    auto relax = [&](int to, int64_t cand, int from, int& ch) {
+      if (cand < dist[to]) { dist[to] = cand; pred[to] = from; ch = 1; }
+    };
+    auto w = [&](int mode, int from, int to, int64_t c) -> int64_t { return mode ? c + pi[from] - pi[to] : c; };
+    auto pass = [&](int mode) -> bool {
+      int ch = 0;
+      // forward: s* -> in_0
+      for (int i = tid; i < n; i += kThreads)
+        if (dist[0] < kDInf && src[i] != kAbsent) relax(IN(0, i), dist[0] + w(mode, 0, IN(0, i), src[i]), 0, ch);
+      __syncthreads();
+      for (int s = 0; s < S; ++s) {
+        for (int i = tid; i < n; i += kThreads) {  // in -> out (node arc, residual cap - g)
+          const int k = s * n + i, a = IN(s, i);
+          if (g[k] >= capE(k) || dist[a] >= kDInf) continue;
+          if (mode == 0 && alive[k] && !alive_prev[k]) continue;  // a rejoined relay's arc is new
+          relax(a + 1, dist[a] + w(mode, a, a + 1, 0), a, ch);
+        }
+        __syncthreads();
+        if (s + 1 < S) {  // out_s -> in_{s+1}: one row minimum per destination (warp per row)
+          for (int v = wid; v < n; v += nw) {
+            const int to = IN(s + 1, v);
+            int64_t best = kDInf;
+            int bu = -1;
+            for (int u = lane; u < n; u += 32) {
+              const int fr = IN(s, u) + 1;
+              const int32_t c = C(s, u, v);
+              if (c == kAbsent || dist[fr] >= kDInf) continue;
+              const int64_t cand = dist[fr] + w(mode, fr, to, c);
+              if (cand < best) { best = cand; bu = fr; }
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+              const int64_t ob = __shfl_xor_sync(0xffffffffu, best, off);
+              const int ou = __shfl_xor_sync(0xffffffffu, bu, off);
+              if (ob < best || (ob == best && ou < bu && ou >= 0)) { best = ob; bu = ou; }
+            }
+            if (lane == 0 && bu >= 0) relax(to, best, bu, ch);
+          }
+          __syncthreads();
+        }
+      }
+      if (tid == 0) {  // out_{S-1} -> t*, then the bypass s* -> t*
+        for (int i = 0; i < n; ++i) {
+          const int fr = IN(S - 1, i) + 1;
+          if (snk[i] != kAbsent && dist[fr] < kDInf) relax(1, dist[fr] + w(mode, fr, 1, snk[i]), fr, ch);
+        }
+        if (mode == 1 && byp < M && dist[0] < kDInf) relax(1, dist[0] + w(mode, 0, 1, big), 0, ch);
+      }
+      __syncthreads();
+      // backward: t* -> out_{S-1} (snk flow), then per stage out -> in (node flow) and in_{s} -> out_{s-1}
+      for (int i = tid; i < n; i += kThreads) {
+        const int to = IN(S - 1, i) + 1;
+        if (snkf[i] > 0 && dist[1] < kDInf) relax(to, dist[1] + w(mode, 1, to, -(int64_t)snk[i]), 1, ch);
+      }
+      __syncthreads();
+      for (int s = S - 1; s >= 0; --s) {
+        for (int i = tid; i < n; i += kThreads) {  // out -> in (reverse node arc, residual g)
+          const int k = s * n + i, a = IN(s, i);
+          if (g[k] > 0 && dist[a + 1] < kDInf) relax(a, dist[a + 1] + w(mode, a + 1, a, 0), a + 1, ch);
+        }
+        __syncthreads();
+        if (s > 0) {  // in_s -> out_{s-1}: reverse link arcs carrying flow (warp per source u)
+          for (int u = wid; u < n; u += nw) {
+            const int to = IN(s - 1, u) + 1;
+            int64_t best = kDInf;
+            int bv = -1;
+            for (int v = lane; v < n; v += 32) {
+              const int fr = IN(s, v);
+              if (arcf[((size_t)(s - 1) * n + v) * n + u] <= 0 || dist[fr] >= kDInf) continue;
+              const int64_t cand = dist[fr] + w(mode, fr, to, -(int64_t)C(s - 1, u, v));
+              if (cand < best) { best = cand; bv = fr; }
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+              const int64_t ob = __shfl_xor_sync(0xffffffffu, best, off);
+              const int ov = __shfl_xor_sync(0xffffffffu, bv, off);
+              if (ob < best || (ob == best && ov < bv && ov >= 0)) { best = ob; bv = ov; }
+            }
+            if (lane == 0 && bv >= 0) relax(to, best, bv, ch);
+          }
+          __syncthreads();
+        }
+      }
+      if (tid == 0)  // in_0 -> s* (reverse src arcs)
+        for (int i = 0; i < n; ++i)
+          if (srcf[i] > 0 && dist[IN(0, i)] < kDInf) relax(0, dist[IN(0, i)] + w(mode, IN(0, i), 0, -(int64_t)src[i]), IN(0, i), ch);
+      return __syncthreads_or(ch) != 0;
+    };
+    // ---- P. potentials of the kept (cut) flow from a virtual root ----
+    for (int k = tid; k < N; k += kThreads) { dist[k] = 0; pred[k] = -1; }
+    __syncthreads();
+    int passes = 0;
+    bool conv = true;
+    while (pass(0)) if (++passes > N + 2) { conv = false; break; }
+    if (!conv) {  // a negative cycle on the kept flow (a lowered cost): the Klein fallback, flows untouched
+      if (tid == 0) status_out[b] = 71;
+      __syncthreads();
+      continue;
+    }
+    for (int k = tid; k < N; k += kThreads) pi[k] = dist[k];
+    __syncthreads();
+    // ---- V. saturate rejoined relays' node arcs with a negative reduced cost ----
+    long long sat = 0;
+    for (int k = tid; k < Sn; k += kThreads) {
+      const int a = 2 + 2 * k;
+      if (alive[k] && !alive_prev[k] && g[k] == 0 && capE(k) > 0 && pi[a] - pi[a + 1] < 0) {
+        g[k] = capE(k);
+        imb[a] -= capE(k);
+        imb[a + 1] += capE(k);
+        ++sat;
+      }
+    }
+    __syncthreads();
+    // ---- A / B. successive shortest paths on reduced costs ----
+    long long iters = 0;
+    bool phaseB = false, bad = false;
+    for (;;) {
+      if (tid == 0) ired[1] = 0;
+      __syncthreads();
+      for (int k = tid; k < N; k += kThreads) {
+        const bool srcn = imb[k] > 0;
+        dist[k] = srcn ? 0 : kDInf;
+        pred[k] = -1;
+        if (srcn) ired[1] = 1;
+      }
+      __syncthreads();
+      if (!ired[1]) {
+        if (phaseB || byp == 0) break;
+        phaseB = true;  // B: the bypass's units become s*'s excess and t*'s deficit
+        if (tid == 0) { imb[0] += (int32_t)byp; imb[1] -= (int32_t)byp; }
+        __syncthreads();
+        continue;
+      }
+      int sp = 0;
+      while (pass(phaseB ? 2 : 1)) if (++sp > N + 2) { bad = true; break; }
+      if (bad) { if (tid == 0) ired[3] = 74; break; }
+      if (tid == 0) red[3] = ~0ull;
+      __syncthreads();
+      for (int k = tid; k < N; k += kThreads)
+        if (imb[k] < 0 && dist[k] < kDInf) atomicMin(&red[3], ((unsigned long long)dist[k] << 20) | (unsigned long long)k);
+      __syncthreads();
+      const unsigned long long bestv = red[3];
+      if (bestv == ~0ull) {
+        if (phaseB) {  // t* unreachable: the units left at s* stay on the bypass
+          byp = imb[0];
+          __syncthreads();
+          if (tid == 0) { imb[1] += imb[0]; imb[0] = 0; }
+          __syncthreads();
+          break;
+        }
+        if (tid == 0) ired[3] = 72;
+        bad = true;
+        break;
+      }
+      const int tgt = (int)(bestv & 0xFFFFF);
+      const int64_t dt = dist[tgt];
+      if (tid == 0) {  // trace, bottleneck, augment
+        int64_t bott = -(int64_t)imb[tgt];
+        int x = tgt, guard = 0;
+        auto rescap = [&](int fr, int to) -> int64_t {
+          if (fr == 0 && to == 1) return M - byp;
+          if (fr == 1 && to == 0) return byp;
+          if (fr == 0) return kDInf;                                   // src forward
+          if (to == 0) return srcf[(fr - 2) / 2];                      // src reverse
+          if (to == 1) return kDInf;                                   // snk forward
+          if (fr == 1) return snkf[(to - 3) / 2 - (S - 1) * n];        // snk reverse
+          const int kf = (fr - 2) / 2, kt = (to - 2) / 2;
+          if (kf == kt) return (fr & 1) ? g[kf] : capE(kf) - g[kf];    // node arc reverse / forward
+          if (fr & 1) return kDInf;                                    // link forward
+          const int sv = kf / n, v = kf % n, u = kt % n;               // link reverse: in_{sv,v} -> out_{sv-1,u}
+          return arcf[((size_t)(sv - 1) * n + v) * n + u];
+        };
+        while (pred[x] >= 0 && ++guard <= N + 2) {
+          const int64_t rc = rescap(pred[x], x);
+          bott = rc < bott ? rc : bott;
+          x = pred[x];
+        }
+        const int s0 = x;
+        if (guard > N + 2 || imb[s0] <= 0 || bott <= 0) {
+          ired[2] = 1;
+        } else {
+          bott = imb[s0] < bott ? imb[s0] : bott;
+          for (x = tgt; x != s0; x = pred[x]) {
+            const int fr = pred[x], to = x;
+            const int32_t d = (int32_t)bott;
+            if (fr == 0 && to == 1) byp += bott;
+            else if (fr == 1 && to == 0) byp -= bott;
+            else if (fr == 0) srcf[(to - 2) / 2] += d;
+            else if (to == 0) srcf[(fr - 2) / 2] -= d;
+            else if (to == 1) snkf[(fr - 3) / 2 - (S - 1) * n] += d;
+            else if (fr == 1) snkf[(to - 3) / 2 - (S - 1) * n] -= d;
+            else {
+              const int kf = (fr - 2) / 2, kt = (to - 2) / 2;
+              if (kf == kt) g[kf] += (fr & 1) ? -d : d;
+              else if (fr & 1) { const int su = kf / n; arcf[((size_t)su * n + kt % n) * n + kf % n] += (int16_t)d; }
+              else { const int sv = kf / n; arcf[((size_t)(sv - 1) * n + kf % n) * n + kt % n] -= (int16_t)d; }
+            }
+          }
+          imb[s0] -= (int32_t)bott;
+          imb[tgt] += (int32_t)bott;
+          if (phaseB) byp -= bott;
+          red[2] = (unsigned long long)byp;
+        }
+      }
+      __syncthreads();
+      if (ired[2]) { if (tid == 0) ired[3] = 73; bad = true; break; }
+      byp = (int64_t)red[2];
+      for (int k = tid; k < N; k += kThreads) pi[k] += dist[k] < dt ? dist[k] : dt;
+      ++iters;
+      __syncthreads();
+    }
+    if (bad) {  // never expected: leave the instance to the fallback (its input flows are untouched)
+      if (tid == 0) status_out[b] = ired[3];
+      __syncthreads();
+      continue;
+    }
+    // ---- write back, objective ----
+    if (tid == 0) { red[0] = 0; red[1] = 0; red[2] = 0; }
+    __syncthreads();
+    long long part = 0;
+    for (int k = tid; k < n; k += kThreads) {
+      sG[k] = srcf[k]; kG[k] = snkf[k];
+      part += (long long)srcf[k] * (src[k] == kAbsent ? 0 : src[k]) + (long long)snkf[k] * (snk[k] == kAbsent ? 0 : snk[k]);
+    }
+    for (int k = tid; k < Sn; k += kThreads) gG[k] = g[k];
+    for (int64_t e = tid; e < (int64_t)(S - 1) * n * n; e += kThreads) {
+      const int s = (int)(e / ((int64_t)n * n)), r = (int)(e - (int64_t)s * n * n), v = r / n, u = r - v * n;
+      aG[e] = arcf[e];
+      if (arcf[e]) part += (long long)arcf[e] * C(s, u, v);
+    }
+    atomicAdd(&red[0], (unsigned long long)part);
+    atomicAdd(&red[1], (unsigned long long)cut);
+    atomicAdd(&red[2], (unsigned long long)sat);
+    __syncthreads();
+    if (tid == 0) {
+      F_out[b] = M - byp;
+      cost_out[b] = (int64_t)red[0];
+      if (stats_out) { stats_out[3 * b] = (int64_t)red[1]; stats_out[3 * b + 1] = (int64_t)red[2]; stats_out[3 * b + 2] = iters; }
+      status_out[b] = 0;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 size_t warm_ws_bytes(const Problem& P, int grid) {
@@ -654,8 +1008,22 @@ cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* a
   int64_t* pi = (int64_t*)(labv + (size_t)grid * N);
   int32_t* imb = (int32_t*)(pi + (size_t)grid * N);
   int32_t* stamp = imb + (size_t)grid * N;
-  warm_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, pi, imb, F, cost, stats, status);
-  klein_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, stamp, F, cost, stats, status);
+  // the shared-memory repair when one instance's state fits (<= 100 KB: at least two CTAs per SM),
+  // else the global-memory one; both leave status 7 to the Klein fallback
+  const size_t wsm = ws_layout(P.S, P.n).total;
+  if (wsm <= 100 * 1024 && P.S > 1) {
+    cudaError_t e = cudaFuncSetAttribute(warm_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warm_smem_kernel, kThreads, wsm);
+    if (e != cudaSuccess) return e;
+    const int g2 = (int)std::min<int64_t>(P.B, (int64_t)std::max(per_sm, 1) * 148);
+    warm_smem_kernel<<<g2, kThreads, wsm, st>>>(P, src_f, g, arc, snk_f, F, cost, stats, status);
+  } else {
+    warm_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, pi, imb, F, cost, stats, status);
+  }
+  if (!getenv("GWTF_WARM_NO_FALLBACK"))  // testing: see what the repair alone does (status 70-79)
+    klein_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, stamp, F, cost, stats, status);
   return cudaGetLastError();
 }
 
