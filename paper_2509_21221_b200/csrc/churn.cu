@@ -51,7 +51,12 @@ __global__ void pack_tile8_kernel(const Problem P, int32_t* bad) {
     const int c = (int)(t % P.ld8);
     const int32_t v = c < P.n ? P.tile[row * P.ld + c] : 255;
     if (c < P.n && (v == kAbsent || v >= 255)) fail = 1;
-    P.tile8[t] = (uint8_t)(v == kAbsent || v >= 255 ? 255 : v);
+    const uint8_t b8 = (uint8_t)(v == kAbsent || v >= 255 ? 255 : v);
+    P.tile8[t] = b8;
+    if (c < P.n) {  // source-major copy: row u = column u of the dest-major tile
+      const size_t bs = row / P.n, dst = row % P.n;
+      P.tile8t[(bs * P.n + c) * P.ld8 + dst] = b8;
+    }
   }
   if (fail) atomicOr(bad, 1);
 }
@@ -99,6 +104,7 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
       if (P.tile8) {  // the 8-bit copy: an absent link or a cost >= 255 retires it (bit 8)
         if (c == kAbsent || c >= 255) atomicOr(bad, 8);
         P.tile8[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld8 + w] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
+        P.tile8t[(((size_t)b * (P.S - 1) + s) * P.n + w) * P.ld8 + v] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
       }
       if (P.tile16) {  // the cluster tier's 16-bit copy; a finite cost >= t16code retires it (bit 2)
         if (c != kAbsent && c >= P.t16code) atomicOr(bad, 2);

@@ -24,6 +24,7 @@ struct Problem {
   uint8_t* tile8;              // cluster tier: [B][S-1][n][ld8] 8-bit copy when every arc is present and
                                // every cost < 255 (255 = padding); nullptr otherwise (or once retired)
   int32_t ld8;                 // n rounded up to 16
+  uint8_t* tile8t;             // the same 8-bit costs source-major, [B][S-1][n_src][ld8] (frontier columns)
   int32_t t16code;             // T32 of the cluster tier's 32-bit keys (ssp_cluster.cu), < 2^16
   int32_t* src;                // [B][n]
   int32_t* snk;                // [B][n]

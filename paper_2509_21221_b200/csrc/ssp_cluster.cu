@@ -270,13 +270,24 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               for (int i = tid; i < nU; i += CT) spk[i] = ldk_out(s, (int)spu[i]);
               for (int j = tid; j < nr; j += CT) rowmin[j] = INF;
               __syncthreads();
-              for (int t = tid; t < nr * nU; t += CT) {
-                const int j = t / nU, i = t - j * nU;
-                const uint64_t k = spk[i];
-                if (k == INF) continue;
-                const int32_t w = tile[((size_t)s * n + v0 + j) * ld + spu[i]];
-                if (w == kAbsent) continue;
-                atomicMin((unsigned long long*)&rowmin[j], (unsigned long long)(k + ((uint64_t)(uint32_t)w << kHopBits) + 1ull));
+              if (t8) {  // source-major 8-bit column: consecutive threads read consecutive rows
+                const uint8_t* colb = P.tile8t + ((size_t)inst * (S - 1) + s) * (size_t)n * P.ld8 + v0;
+                for (int t = tid; t < nr * nU; t += CT) {
+                  const int i = t / nr, j = t - i * nr;
+                  const uint64_t k = spk[i];
+                  if (k == INF) continue;
+                  const uint32_t w = colb[(size_t)spu[i] * P.ld8 + j];  // tile8 holds no absent arc
+                  atomicMin((unsigned long long*)&rowmin[j], (unsigned long long)(k + ((uint64_t)w << kHopBits) + 1ull));
+                }
+              } else {
+                for (int t = tid; t < nr * nU; t += CT) {
+                  const int j = t / nU, i = t - j * nU;
+                  const uint64_t k = spk[i];
+                  if (k == INF) continue;
+                  const int32_t w = tile[((size_t)s * n + v0 + j) * ld + spu[i]];
+                  if (w == kAbsent) continue;
+                  atomicMin((unsigned long long*)&rowmin[j], (unsigned long long)(k + ((uint64_t)(uint32_t)w << kHopBits) + 1ull));
+                }
               }
               __syncthreads();
               int chs = 0;
