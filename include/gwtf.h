@@ -201,8 +201,11 @@ gwtf_status gwtf_flow_import_round_state(gwtf_flow_t h, const int32_t* up, const
  * requests, grants, Change and self-pairing stay within one data node (K = 1 is
  * gwtf_flow_decentralized_rounds from an empty state).  Outputs (device, caller-owned): rounds_run
  * [B], dec_flow / dec_cost [K][B] (complete SRC_k -> SNK_k chains and their Eq. 2 cost), dangling
- * [B], round_digests [B][max_rounds] or NULL, up / down / tag [B][S][n][max_cap] or NULL (final
- * state; data-node slot i of D_k = -2 - (k Mmax + i), Mmax = max supply; tag -1 on FREE slots).
+ * [B], round_digests [B][max_rounds] or NULL; the state arrays up / down / tag [B][S][n][max_cap] and
+ * src_down / snk_up [B][K][Mmax] (all or none; data-node slot i of D_k = -2 - (k Mmax + i), Mmax =
+ * max supply; tag -1 on FREE slots) receive the final state, and with resume != 0 they also give the
+ * starting state (a valid tagged pairing, caller-checked; accepted-move and deny counters start at 0)
+ * and round0 the RNG round counter to start from (0 from the empty state).
  * All device pointers on `stream` (a cudaStream_t); reads the supplies back (synchronizes).
  * INVALID on bad shapes or parameters, UNSUPPORTED when one instance's state exceeds 227 KB. */
 gwtf_status gwtf_mc_rounds(int32_t B, int32_t S, int32_t n, int32_t max_cap, int32_t K, const int32_t* cap,
@@ -211,7 +214,7 @@ gwtf_status gwtf_mc_rounds(int32_t B, int32_t S, int32_t n, int32_t max_cap, int
                            double alpha, int32_t objective, int32_t steady_window, int32_t deny_after,
                            int32_t max_rounds, int32_t* rounds_run, int64_t* dec_flow, int64_t* dec_cost,
                            int32_t* dangling, uint64_t* round_digests, int32_t* up, int32_t* down, int32_t* tag,
-                           void* stream);
+                           int32_t* src_down, int32_t* snk_up, int32_t resume, int64_t round0, void* stream);
 
 /* Save / restore the handle's mutable state (masks, costs, round state) on the device,
  * e.g. to replay the same churn step several times in a benchmark. */

@@ -75,6 +75,7 @@ def lib():
         L.orc_mc_rounds_destroy.argtypes = [P]
         L.orc_mc_rounds_run.argtypes = [P, ctypes.c_int32, P, P, P, P, P]
         L.orc_mc_rounds_export.argtypes = [P] + [P] * 9
+        L.orc_mc_rounds_import.argtypes = [P] + [P] * 7 + [ctypes.c_int32, ctypes.c_int64]
         L.orc_mc_rounds_digest.restype = ctypes.c_uint64
         L.orc_mc_rounds_digest.argtypes = [P]
         L.orc_pipeline_batch.argtypes = ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [P] * 6
@@ -612,6 +613,14 @@ class McRounds:
         lib().orc_mc_rounds_export(self.h, _ptr(up), _ptr(dn), _ptr(tg), _ptr(sd), _ptr(su), _ptr(k), _ptr(dw),
                                    ctypes.byref(q), ctypes.byref(r))
         return dict(up=up, down=dn, tag=tg, src_down=sd, snk_up=su, kacc=k, deny=dw, quiet=q.value, round=r.value)
+
+    def import_state(self, st: dict):
+        """Install a state in export()'s layouts (ValueError unless a valid tagged pairing)."""
+        c = lambda k: None if st.get(k) is None else np.ascontiguousarray(np.asarray(st[k], np.int32).reshape(-1))  # noqa: E731
+        arrs = [c("up"), c("down"), c("tag"), c("src_down"), c("snk_up"), c("kacc"), c("deny")]
+        rc = lib().orc_mc_rounds_import(self.h, *[_ptr(a) for a in arrs], int(st.get("quiet", 0)), int(st.get("round", 0)))
+        if rc != 0:
+            raise ValueError("orc_mc_rounds_import: not a valid tagged pairing")
 
     def digest(self) -> int:
         return int(lib().orc_mc_rounds_digest(self.h))

@@ -1805,4 +1805,49 @@ int orc_mc_rounds_export(const orc_mc_rounds* o, int32_t* up, int32_t* down, int
 }
 uint64_t orc_mc_rounds_digest(const orc_mc_rounds* o) { return o->R.digest(); }
 
+// Install an MC round state in the export layouts (tag -1 on FREE slots); kacc / deny / quiet may be
+// NULL (0).  -1 (state unchanged) unless it is a valid pairing whose pointers cross one stage
+// boundary, whose data-node slots are below their supply, and whose every link joins slots of one tag,
+// SRC_k / SNK_k only slots tagged k.
+int orc_mc_rounds_import(orc_mc_rounds* o, const int32_t* up, const int32_t* down, const int32_t* tag,
+                         const int32_t* src_down, const int32_t* snk_up, const int32_t* kacc, const int32_t* deny,
+                         int32_t quiet, int64_t round) {
+  McRounds& R = o->R;
+  const Inst& I = R.I;
+  const int S = I.S, n = I.n, MC = I.MC, K = R.K;
+  const int64_t ns = (int64_t)S * n * MC, Mm = R.Mmax;
+  auto dk = [&](int32_t p) { return (int)((-2 - (int64_t)p) / Mm); };
+  auto di = [&](int32_t p) { return (-2 - (int64_t)p) % Mm; };
+  for (int64_t p = 0; p < ns; ++p) {
+    const int g = (int)(p / MC), j = (int)(p % MC), s = g / n;
+    const bool usable = R.alive(g) && j < R.capE(g);
+    const bool free_ = up[p] == NONE && down[p] == NONE;
+    if (!usable && !free_) return -1;
+    if (!free_ && (tag[p] < 0 || tag[p] >= K)) return -1;
+    if (up[p] >= 0 && (up[p] >= ns || up[p] / MC / n != s - 1 || down[up[p]] != (int32_t)p || tag[up[p]] != tag[p])) return -1;
+    if (up[p] <= -2 && (s != 0 || dk(up[p]) >= K || dk(up[p]) != tag[p] || di(up[p]) >= R.M[dk(up[p])] ||
+                        src_down[(size_t)dk(up[p]) * Mm + di(up[p])] != (int32_t)p)) return -1;
+    if (down[p] >= 0 && (down[p] >= ns || down[p] / MC / n != s + 1 || up[down[p]] != (int32_t)p || tag[down[p]] != tag[p])) return -1;
+    if (down[p] <= -2 && (s != S - 1 || dk(down[p]) >= K || dk(down[p]) != tag[p] || di(down[p]) >= R.M[dk(down[p])] ||
+                          snk_up[(size_t)dk(down[p]) * Mm + di(down[p])] != (int32_t)p)) return -1;
+  }
+  for (int k = 0; k < K; ++k)
+    for (int64_t i = 0; i < Mm; ++i) {
+      const int32_t sd = src_down[(size_t)k * Mm + i], su = snk_up[(size_t)k * Mm + i];
+      if (i >= R.M[k] && (sd != NONE || su != NONE)) return -1;
+      if (sd != NONE && (sd < 0 || sd >= ns || up[sd] != McRounds::dptr(k, i, Mm))) return -1;
+      if (su != NONE && (su < 0 || su >= ns || down[su] != McRounds::dptr(k, i, Mm))) return -1;
+    }
+  R.up.assign(up, up + ns);
+  R.down.assign(down, down + ns);
+  for (int64_t p = 0; p < ns; ++p) R.tag[p] = tag[p] < 0 ? 0 : tag[p];
+  R.src_down.assign(src_down, src_down + (size_t)K * Mm);
+  R.snk_up.assign(snk_up, snk_up + (size_t)K * Mm);
+  if (kacc) R.kacc.assign(kacc, kacc + (size_t)S * n); else R.kacc.assign((size_t)S * n, 0);
+  if (deny) R.deny.assign(deny, deny + (size_t)S * n); else R.deny.assign((size_t)S * n, 0);
+  R.quiet = quiet;
+  R.round = round;
+  return 0;
+}
+
 }  // extern "C"

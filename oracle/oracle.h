@@ -127,6 +127,10 @@ int orc_mc_rounds_run(orc_mc_rounds* R, int32_t max_rounds, int32_t* rounds_run,
 int orc_mc_rounds_export(const orc_mc_rounds* R, int32_t* up, int32_t* down, int32_t* tag, int32_t* src_down,
                          int32_t* snk_up, int32_t* kacc, int32_t* deny, int32_t* quiet, int64_t* round);
 uint64_t orc_mc_rounds_digest(const orc_mc_rounds* R);
+/* Inverse of orc_mc_rounds_export (-1 unless a valid tagged pairing; kacc / deny may be NULL). */
+int orc_mc_rounds_import(orc_mc_rounds* R, const int32_t* up, const int32_t* down, const int32_t* tag,
+                         const int32_t* src_down, const int32_t* snk_up, const int32_t* kacc, const int32_t* deny,
+                         int32_t quiet, int64_t round);
 
 /* Whole per-instance workload of one bench step, for the cpu_baseline and
  * the full-size parity samples: pre-churn rounds to quiescence, churn, cold SSP on

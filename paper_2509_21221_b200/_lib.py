@@ -51,7 +51,7 @@ EXPORTS = {
     "gwtf_flow_export_round_state": ([P, P, P, P, P, P, P, P, P], I32),
     "gwtf_flow_import_round_state": ([P, P, P, P, P, P, P, P, P], I32),
     "gwtf_mc_rounds": ([I32, I32, I32, I32, I32, P, P, P, P, P, P, U64, I64, DBL, DBL, I32, I32, I32, I32,
-                        P, P, P, P, P, P, P, P, P], I32),
+                        P, P, P, P, P, P, P, P, P, P, I32, I64, P], I32),
     "gwtf_flow_snapshot": ([P], I32),
     "gwtf_flow_restore": ([P], I32),
     "gwtf_flow_set_profiling": ([P, I32], I32),

@@ -698,14 +698,16 @@ gwtf_status gwtf_mc_rounds(int32_t B, int32_t S, int32_t n, int32_t max_cap, int
                            double alpha, int32_t objective, int32_t steady_window, int32_t deny_after,
                            int32_t max_rounds, int32_t* rounds_run, int64_t* dec_flow, int64_t* dec_cost,
                            int32_t* dangling, uint64_t* round_digests, int32_t* up, int32_t* down, int32_t* tag,
-                           void* stream) {
+                           int32_t* src_down, int32_t* snk_up, int32_t resume, int64_t round0, void* stream) {
   if (B < 1 || S < 1 || n < 1 || K < 1 || max_cap < 0 || max_cap > 32 || max_rounds < 0 || steady_window < 1 ||
       deny_after < 1 || (objective != GWTF_OBJ_SUM && objective != GWTF_OBJ_MINIMAX))
     return fail(GWTF_E_INVALID, "mc_rounds: shape / parameter out of range");
   if (!cap || !src_cost || !snk_cost || !supply || (S > 1 && !link_cost) || !rounds_run || !dec_flow || !dec_cost ||
       !dangling)
     return fail(GWTF_E_INVALID, "mc_rounds: NULL required array");
-  if ((up || down || tag) && !(up && down && tag)) return fail(GWTF_E_INVALID, "mc_rounds: up/down/tag all or none");
+  if ((up || down || tag || src_down || snk_up) && !(up && down && tag && src_down && snk_up))
+    return fail(GWTF_E_INVALID, "mc_rounds: up/down/tag/src_down/snk_up all or none");
+  if (resume && !up) return fail(GWTF_E_INVALID, "mc_rounds: resume needs the state arrays");
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int64_t> sup((size_t)K * B);
   if (cudaMemcpyAsync(sup.data(), supply, sup.size() * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -734,6 +736,7 @@ gwtf_status gwtf_mc_rounds(int32_t B, int32_t S, int32_t n, int32_t max_cap, int
   c.max_rounds = max_rounds; c.thr = thr_d; c.thr_width = width; c.thr_K = Kt;
   c.rounds_run = rounds_run; c.F_dec = dec_flow; c.cost_dec = dec_cost; c.dangling = dangling;
   c.digests = round_digests; c.up_out = up; c.down_out = down; c.tag_out = tag;
+  c.sd_out = src_down; c.su_out = snk_up; c.resume = resume; c.round0 = round0;
   const cudaError_t e = launch_mc_rounds(c, st, sms);
   cudaFreeAsync(thr_d, st);
   if (e != cudaSuccess) return fail(GWTF_E_CUDA, cudaGetErrorString(e));

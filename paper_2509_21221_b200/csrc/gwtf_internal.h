@@ -125,7 +125,9 @@ struct McRoundsCall {
   uint64_t seed; int64_t inst_base; int32_t objective, W, deny_after, max_rounds;
   const uint32_t* thr; int32_t thr_width, thr_K;
   int32_t* rounds_run; int64_t* F_dec; int64_t* cost_dec; int32_t* dangling; uint64_t* digests;
-  int32_t *up_out, *down_out, *tag_out;
+  int32_t *up_out, *down_out, *tag_out, *sd_out, *su_out;
+  int32_t resume;
+  int64_t round0;
 };
 size_t mc_rounds_smem(int S, int n, int MC, int K, int Mmax);
 cudaError_t launch_mc_rounds(const McRoundsCall& c, cudaStream_t st, int num_sms);

@@ -61,6 +61,9 @@ struct McArgs {
   int32_t* dangling;     // [B]
   uint64_t* digests;     // [B][max_rounds] or null
   int32_t *up_out, *down_out, *tag_out;  // [B][S][n][MC] or null (final state)
+  int32_t *sd_out, *su_out;              // [B][K][Mmax] or null
+  int32_t resume;                        // start from the state in the five arrays above
+  int64_t round0;                        // the RNG round counter at the start
 };
 
 struct McLayout { size_t up, down, tag, sd, su, kacc, deny, capv, scost, adv, rs, rt, rk, prop, ptouch, pkey, res, red, total; };
@@ -135,8 +138,17 @@ __global__ void __launch_bounds__(kT) mc_rounds_kernel(const McArgs A) {
     auto set_down_of = [&](int32_t p, int32_t v) { if (p >= 0) down[p] = v; else sd[dk(p) * Mmax + di(p)] = v; };
     auto res_up = [&](int32_t p) -> int { return p >= 0 ? p : ns + (-2 - p); };
     auto res_dn = [&](int32_t p) -> int { return p >= 0 ? p : ns + K * Mmax + (-2 - p); };
-    for (int p = tid; p < ns; p += kT) { up[p] = kNone; down[p] = kNone; tag[p] = 0; }
-    for (int k = tid; k < K * Mmax; k += kT) { sd[k] = kNone; su[k] = kNone; }
+    if (A.resume) {  // a given state (the export layouts; tag -1 on FREE slots)
+      for (int p = tid; p < ns; p += kT) {
+        up[p] = A.up_out[(size_t)b * ns + p];
+        down[p] = A.down_out[(size_t)b * ns + p];
+        tag[p] = max(A.tag_out[(size_t)b * ns + p], 0);
+      }
+      for (int k = tid; k < K * Mmax; k += kT) { sd[k] = A.sd_out[(size_t)b * K * Mmax + k]; su[k] = A.su_out[(size_t)b * K * Mmax + k]; }
+    } else {
+      for (int p = tid; p < ns; p += kT) { up[p] = kNone; down[p] = kNone; tag[p] = 0; }
+      for (int k = tid; k < K * Mmax; k += kT) { sd[k] = kNone; su[k] = kNone; }
+    }
     for (int v = tid; v < Sn; v += kT) { kacc[v] = 0; deny[v] = 0; capv[v] = alive(v) ? A.cap[(size_t)b * Sn + v] : 0; }
     for (int k = tid; k < ns + 2 * K * Mmax; k += kT) res[k] = RES_NONE;
     __syncthreads();
@@ -153,7 +165,7 @@ __global__ void __launch_bounds__(kT) mc_rounds_kernel(const McArgs A) {
       }
     };
     int quiet = 0, r = 0;
-    uint64_t round = 0;
+    uint64_t round = (uint64_t)A.round0;
     while (r < A.max_rounds) {
       const uint64_t hpre = mix(mix(mix(A.seed) ^ (uint64_t)(A.inst_base + b)) ^ round);
       auto h = [&](int gid, int stream) -> uint64_t { return mix(hpre ^ ((uint64_t)gid * 4 + stream)); };
@@ -481,6 +493,10 @@ __global__ void __launch_bounds__(kT) mc_rounds_kernel(const McArgs A) {
       A.down_out[(size_t)b * ns + p] = down[p];
       A.tag_out[(size_t)b * ns + p] = st(p) == ST_FREE ? -1 : tag[p];
     }
+    if (A.sd_out) for (int k = tid; k < K * Mmax; k += kT) {
+      A.sd_out[(size_t)b * K * Mmax + k] = sd[k];
+      A.su_out[(size_t)b * K * Mmax + k] = su[k];
+    }
     __syncthreads();
     if (tid == 0) { A.rounds_run[b] = r; A.dangling[b] = (int32_t)red[4]; }
     __syncthreads();
@@ -499,6 +515,7 @@ cudaError_t launch_mc_rounds(const McRoundsCall& c, cudaStream_t st, int num_sms
   A.max_rounds = c.max_rounds; A.thr = c.thr; A.thr_width = c.thr_width; A.thr_K = c.thr_K;
   A.rounds_run = c.rounds_run; A.F_dec = c.F_dec; A.cost_dec = c.cost_dec; A.dangling = c.dangling;
   A.digests = c.digests; A.up_out = c.up_out; A.down_out = c.down_out; A.tag_out = c.tag_out;
+  A.sd_out = c.sd_out; A.su_out = c.su_out; A.resume = c.resume; A.round0 = c.round0;
   const size_t smem = mc_layout(c.S, c.n, c.MC, c.K, c.Mmax).total;
   cudaError_t e = cudaFuncSetAttribute(mc_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -62,7 +62,7 @@ def multi_source_ssp_unit(cap, alive, link_cost, src_costs, snk_costs, supplies,
 
 def mc_rounds(cap, alive, link_cost, src_costs, snk_costs, supplies, *, max_cap: int, max_rounds: int, seed=0,
               inst_base=0, T0=1.7, alpha=0.95, objective=0, steady_window=5, deny_after=3, digests=False,
-              state=False, stream=None):
+              state=False, start_state=None, round0=0, stream=None):
     """Multi-data-node decentralized rounds (gwtf_mc_rounds): K data
     nodes with src_costs / snk_costs (K tensors [B][n] int32) and supplies (K tensors [B] int64) on the
     shared relays and links; rounds from the empty state.  Returns a dict: rounds [B], F_dec / cost_dec
@@ -83,9 +83,15 @@ def mc_rounds(cap, alive, link_cost, src_costs, snk_costs, supplies, *, max_cap:
                dangling=torch.empty(B, dtype=torch.int32, device=dev))
     if digests:
         out["digests"] = torch.zeros((B, max(max_rounds, 1)), dtype=torch.int64, device=dev)
-    if state:
+    Mmax = max(1, int(sup.max()))
+    if state or start_state is not None:
         for k in ("up", "down", "tag"):
             out[k] = torch.empty((B, S, n, max_cap), dtype=torch.int32, device=dev)
+        for k in ("src_down", "snk_up"):
+            out[k] = torch.empty((B, K, Mmax), dtype=torch.int32, device=dev)
+        if start_state is not None:  # the starting state (copied in; the arrays receive the final state)
+            for k in ("up", "down", "tag", "src_down", "snk_up"):
+                out[k].copy_(start_state[k].reshape(out[k].shape))
     p = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     link = link_cost.contiguous() if S > 1 else None
@@ -93,5 +99,6 @@ def mc_rounds(cap, alive, link_cost, src_costs, snk_costs, supplies, *, max_cap:
         B, S, n, max_cap, K, p(cap.contiguous()), p(alive.contiguous() if alive is not None else None), p(link),
         p(src), p(snk), p(sup), seed, inst_base, T0, alpha, objective, steady_window, deny_after, max_rounds,
         p(out["rounds"]), p(out["F_dec"]), p(out["cost_dec"]), p(out["dangling"]), p(out.get("digests")),
-        p(out.get("up")), p(out.get("down")), p(out.get("tag")), ctypes.c_void_p(st.cuda_stream)))
+        p(out.get("up")), p(out.get("down")), p(out.get("tag")), p(out.get("src_down")), p(out.get("snk_up")),
+        1 if start_state is not None else 0, int(round0), ctypes.c_void_p(st.cuda_stream)))
     return out

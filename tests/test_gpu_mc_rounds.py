@@ -77,3 +77,21 @@ def test_gpu_mc_single_data_node(name):
         o = oracle.Rounds(I, seed=2, inst_id=b).run(cfg.max_rounds)
         assert (int(out["rounds"][b]), int(out["F_dec"][0, b]), int(out["cost_dec"][0, b])) == (
             o["rounds"], o["F_dec"], o["cost_dec"]), (name, b)
+
+
+def test_gpu_mc_in_slot_trace():
+    """The IN-slot rule on the GPU from the same imported state (tests/test_oracle_mc_rounds.in_slot_case):
+    b0's unpaired inflow of D0 goes to D0's sink; (F, cost) = ([1, 1], [12, 3]) after 8 rounds."""
+    from tests.test_oracle_mc_rounds import in_slot_case
+    I, srcs, snks, M, st0 = in_slot_case()
+    B = 2
+    rep = lambda a: np.broadcast_to(np.asarray(a), (B,) + np.asarray(a).shape).copy()  # noqa: E731
+    start = {k: torch.from_numpy(rep(np.asarray(st0[k], np.int32))).cuda() for k in ("up", "down", "tag", "src_down", "snk_up")}
+    out = _mc(rep(I.cap), rep(I.alive), rep(I.link), [rep(np.asarray(s, np.int32)) for s in srcs],
+              [rep(np.asarray(s, np.int32)) for s in snks], [np.full(B, m, np.int64) for m in M], 1,
+              max_rounds=100, T0=0.0, seed=4, start_state=start, round0=20, state=True)
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert int(out["rounds"][b]) == 8
+        assert out["F_dec"][:, b].tolist() == [1, 1] and out["cost_dec"][:, b].tolist() == [12, 3]
+        assert out["down"][b].reshape(-1).tolist() == [2, 3, -2, -3] and out["tag"][b].reshape(-1).tolist() == [0, 1, 0, 1]

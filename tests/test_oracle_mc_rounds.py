@@ -117,3 +117,37 @@ def test_mc_invariants_flow_settings_5_6(name):
         # and together at most what the shared relays can carry
         assert r["F_dec"].sum() <= oracle.ssp(Instance(I.S, I.n, I.max_cap, sum(Ms), I.cap, srcs[0], snks[0],
                                                         I.link, I.alive)).F
+
+
+def in_slot_case():
+    """S=2, n=2, caps 1, K=2, one microbatch each; every link 1, src_k = [1, 1], snk_0 = [10, 10],
+    snk_1 = [1, 1] (D1's sink is the cheaper one from both last-stage relays).  Start (round 20):
+    SRC_0 -> a0 -> b0, and b0's slot is IN (tag 0: its chain came from D0, its downstream is gone);
+    everything else empty.
+      r20: b0 holds unpaired inflow of D0, so it may only ask D0's sink -- 10, although D1's costs 1
+           (each data node gets its own flow back); b1 (stable) takes the cheaper D1-sink.
+      r21: a1 (stable) pairs with b1's tag-1 outflow (1 + 1 = 2).
+      r22: D1 pairs a1 (1 + 2 = 3).  Change a0 <-> a1 or b0 <-> b1 would mix D0's and D1's chains.
+      r23-r27 quiet: (F, cost) = ([1, 1], [12, 3]) after 8 rounds.
+    (A requester holding an IN slot asking any data node would send D0's chain to D1's sink.)"""
+    from tests.pin_cases import D, NONE as N_, state
+    I = Instance(2, 2, 1, 1, np.ones((2, 2)), np.zeros(2), np.zeros(2), np.ones((1, 2, 2), np.int32))
+    st = state(2, 2, 1, 1, {0: (D(0), 2), 2: (0, N_)}, src_down=[[0], [N_]], snk_up=[[N_], [N_]], rnd=20)
+    st["tag"] = np.array([0, -1, 0, -1], np.int32).reshape(2, 2, 1)
+    return I, [[1, 1], [1, 1]], [[10, 10], [1, 1]], [1, 1], st
+
+
+def test_mc_in_slot_asks_its_own_data_node():
+    I, srcs, snks, M, st0 = in_slot_case()
+    R = oracle.McRounds(I, srcs, snks, M, T0=0.0, seed=4)
+    R.import_state(st0)
+    R.run(1)
+    st = R.export()
+    assert list(st["down"].ravel()) == [2, NONE, -2, -3] and list(st["tag"].ravel()) == [0, -1, 0, 1]
+    r = R.run(100)
+    assert r["rounds"] == 7 and list(r["F_dec"]) == [1, 1] and list(r["cost_dec"]) == [12, 3]
+    assert R.export()["round"] == 28
+    bad = {k: (np.array(v, copy=True) if isinstance(v, np.ndarray) else v) for k, v in st0.items()}
+    bad["tag"].reshape(-1)[2] = 1  # b0's slot tagged 1 under a0's tag-0 slot: not a valid tagged pairing
+    with pytest.raises(ValueError):
+        oracle.McRounds(I, srcs, snks, M, T0=0.0).import_state(bad)
