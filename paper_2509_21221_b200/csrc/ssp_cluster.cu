@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           const bool nostream = P.debug & 64;  // testing: time the compute without the stream
           if (pf_n && pf_s != s) drain();     // the speculation missed
           const int pre = pf_n;                // chunks of this boundary already in flight
-          const int nxt = (s + 2 < S && !nostream && !(P.debug & 512)) ? s + 1 : -1;
+          const int nxt = (s + 2 < S && !nostream && !(P.debug & 512) && ((fresh >> (s + 1)) & 1ull)) ? s + 1 : -1;
           const uint8_t* rows_next = nxt >= 0 ? rows_of(nxt) : nullptr;
           pf_s = nxt;
           pf_n = nxt >= 0 ? min(nbc, nch) : 0;
@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             pko = kout[(s + 1) * R + jr];
             pres = g[(s + 1) * R + jr] < capE[(s + 1) * R + jr];
           }
+          TMARK(13);  // stream issue + row-key prefetch
           const uint32_t lim = T32 > (uint32_t)maxw ? T32 - (uint32_t)maxw : 0u;
           int wide = lim == 0u || (P.debug & 32) || (t8 && T32 < 255u);  // testing (32): force the 64-bit path
           for (int u0 = 0; u0 < ldk; u0 += 4 * CT) {  // gather out_s from L2 (4 loads in flight)

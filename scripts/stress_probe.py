@@ -53,8 +53,8 @@ if a.rounds:
                       "F_dec": rr.dec_flow.tolist(), "cost_dec": rr.dec_cost.tolist()}))
 if os.environ.get("GWTF_DEBUG_FLAGS", "0") != "0" and int(os.environ["GWTF_DEBUG_FLAGS"]) & 16:
     raw = fl.stats(raw=True)
-    names = ["gather", "relax(dense, after 1st chunk)", "relax_vote", "tstar", "trev", "backward", "trace", "lookup",
-             "augment", "other", "frontier relax", "frontier vote", "dense: wait 1st chunk", "-"]
+    names = ["dense: key gather", "relax(dense, after 1st chunk)", "relax_vote", "tstar", "trev", "backward", "trace", "lookup",
+             "augment", "other", "frontier relax", "frontier vote", "dense: wait 1st chunk", "dense: issue + prefetch"]
     cyc = raw[1100:1114].astype(float)
     tot = cyc.sum()
     print("phase cycles (leader thread, all solves, summed over clusters):")
