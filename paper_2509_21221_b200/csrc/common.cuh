@@ -76,13 +76,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// 16-byte asynchronous global -> shared copy (LDGSTS), committed as a group per thread
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 // ---- distributed shared memory (thread-block clusters) ----------------------------------
 // shared::cluster address of `local_ptr`'s counterpart in CTA `rank` of the cluster
 __device__ __forceinline__ uint32_t dsmem_addr(const void* local_ptr, uint32_t rank) {
