@@ -261,6 +261,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
             }
             __syncthreads();
             const int nU = misc->red32;
+            if ((P.debug & 2048) && r == 0 && tid == 0)  // testing: histogram of changed columns
+              atomicAdd(&P.stats[1200 + (nU == 0 ? 0 : 32 - __clz(nU))], 1ull);
             if (nU <= ksp) {
               if (m) {
                 int k = atomicAdd(&misc->ucnt, __popc(m));
