@@ -294,6 +294,7 @@ def warm_reroute(dev, names=("gpt", "llama", "churn"), steps=3, warmup=2):
             upd = None
         fl.snapshot()
         work = [t.clone() for t in base]
+        cold0 = fl.stats()["warm_cold_instances"]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         tw = tc = 0.0
         for it in range(warmup + steps):
@@ -317,8 +318,8 @@ def warm_reroute(dev, names=("gpt", "llama", "churn"), steps=3, warmup=2):
         out[name] = {"workload": workload_name(cfg), "instances": B, "warm_ms": tw / steps, "cold_ms": tc / steps,
                      "warm_instances_per_s": B * steps / (tw / 1e3), "cold_instances_per_s": B * steps / (tc / 1e3),
                      "F_cost_mismatches": int(((F != cold.flow_value) | (C != cold.total_cost)).sum()),
-                     "status_nonzero": int((Q != 0).sum()), "stripped": int(S[:, 0].sum()),
-                     "cycles": int(S[:, 1].sum()), "augmentations": int(S[:, 2].sum()),
+                     "status_nonzero": int((Q != 0).sum()), "units_cut": int(S[:, 0].sum()),
+                     "cold_subset_instances": (fl.stats()["warm_cold_instances"] - cold0) // (warmup + steps),
                      "cold_augmentations": int(cold.augmentations.sum())}
         fl.close()
     return out

@@ -35,6 +35,7 @@ extern "C" {
 #define GWTF_ABI_VERSION 1
 #define GWTF_ABSENT INT32_MAX
 #define GWTF_HOST_PTRS (1u << 0) /* array arguments of every call on this handle are host pointers */
+#define GWTF_WARM_REPAIR_ALL (1u << 1) /* gwtf_flow_warm_reroute repairs every instance (no triage) */
 #define GWTF_FORCE_GLOBAL_TIER (1u << 30) /* testing: run the exact solve through the global-memory tier */
 #define GWTF_FORCE_CLUSTER_TIER (1u << 29) /* testing: run the exact solve through the cluster tier */
 
@@ -75,7 +76,7 @@ typedef struct {
   int32_t deny_after;          /* idle rounds holding unpaired inflow before DENY (default 3) */
   int32_t device;              /* CUDA device ordinal */
   void* stream;                /* cudaStream_t (NULL = legacy default stream) */
-  uint32_t flags;              /* GWTF_HOST_PTRS | GWTF_FORCE_GLOBAL_TIER | GWTF_FORCE_CLUSTER_TIER */
+  uint32_t flags;              /* GWTF_HOST_PTRS | GWTF_WARM_REPAIR_ALL | GWTF_FORCE_GLOBAL_TIER | GWTF_FORCE_CLUSTER_TIER */
 } gwtf_problem_desc;
 
 /* Eq. 1 evaluated on the device in integer half-units:
@@ -238,19 +239,26 @@ gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_
 
 /* Warm-start rerouting after churn ("reroute" after a failure,
  * PAPER.md:274-288 crash handling), on the handle's current (churned) graph,
- * starting from a pre-churn assignment instead of zero flow:
- *   1. strip every unit the graph can no longer carry (crashed relay, relay over capacity,
- *      link / src / snk now GWTF_ABSENT), one unit path at a time;
- *   2. cancel negative residual cycles (Bellman-Ford, predecessor walk, bottleneck push);
- *   3. resume successive shortest paths until F = M or no augmenting path is left.
+ * starting from a pre-churn assignment instead of zero flow.  Per instance:
+ *   0. triage: when 4 x (units the churned graph can no longer carry) > the assignment's flow,
+ *      re-routing would cost about as many searches as a cold solve, and instances with fewer
+ *      than 4,096 links are cheaper to solve cold than to repair: those are solved cold (the
+ *      create flag GWTF_WARM_REPAIR_ALL skips the triage);
+ *   1. otherwise the potential-carrying repair: potentials of the kept flow (Bellman-Ford), cut
+ *      the units over capacity (crashed relay, relay over capacity, link / src / snk now
+ *      GWTF_ABSENT), saturate the rejoined relays' shortcuts, route the excesses to the
+ *      deficits, then resume successive shortest paths until F = M or no augmenting path is left;
+ *   2. an instance whose repair stops (lowered costs, ranges) is solved cold as well.
+ * The cold solves run the exact-solve kernels on that subset only.
  * node_flow [B][S][n], src_flow [B][n], snk_flow [B][n], arc_flow_dense [B][S-1][n_dst][n_src]
  * (the gwtf_flow_get_assignment layouts, taken before gwtf_flow_apply_churn) are read and
  * OVERWRITTEN in place with the repaired optimum.  Outputs [B]: max-flow value, min cost (equal
  * to a cold gwtf_flow_solve_batch's: the optimum's (F, cost) is unique; the assignment may
- * differ), stats [B][3] = {units stripped, cycles cancelled, augmentations} (may be NULL),
- * inst_status (0 ok, 1 distance bound 2^38 exceeded, 2/3 no convergence, 4 the given
- * assignment is not conserved, 5 internal: a non-negative predecessor cycle; may be NULL).  Does not touch the handle's own solver or round
- * state.  INVALID on NULL required arrays; UNSUPPORTED when 2(2n + Sn + (S-1)n^2) >= 2^24. */
+ * differ), stats [B][3] = {units cut, arcs saturated, repair iterations} for repaired instances
+ * and {units cut, 0, augmentations} for cold-solved ones (may be NULL), inst_status (0 ok, else
+ * the exact solve's status codes; may be NULL: then any nonzero status fails the call with
+ * GWTF_E_STATE).  Does not touch the handle's own solver or round state.  INVALID on NULL
+ * required arrays; UNSUPPORTED when 2(2n + Sn + (S-1)n^2) >= 2^24. */
 gwtf_status gwtf_flow_warm_reroute(gwtf_flow_t h, int32_t* node_flow, int32_t* src_flow, int32_t* snk_flow,
                                    int32_t* arc_flow_dense, int64_t* flow_value, int64_t* total_cost,
                                    int64_t* stats, int32_t* inst_status);
@@ -258,7 +266,8 @@ gwtf_status gwtf_flow_warm_reroute(gwtf_flow_t h, int32_t* node_flow, int32_t* s
 /* Work counters of the exact solve accumulated since create (host int64 out[cap], cap <= 2048):
  * [0] dense boundary relaxations, [1] backward (reverse-arc) phases, [2] augmentations,
  * [3] Bellman-Ford passes, [4] traced path nodes (cluster tier), [11] frontier relaxations (cluster
- * tier), [15] kernels launched by this handle (host count).  Synchronizes the stream. */
+ * tier), [12] instances gwtf_flow_warm_reroute solved cold, [13] instances re-solved with 64-bit
+ * keys, [15] kernels launched by this handle (host count).  Synchronizes the stream. */
 gwtf_status gwtf_flow_stats(gwtf_flow_t h, int64_t* out, int32_t cap);
 
 /* Synchronizes the stream, frees everything.  NULL is a no-op. */

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libgwtf.so")
 
 GWTF_ABI_VERSION = 1
 GWTF_HOST_PTRS = 1 << 0
+GWTF_WARM_REPAIR_ALL = 1 << 1  # warm_reroute repairs every instance (no triage)
 GWTF_FORCE_GLOBAL_TIER = 1 << 30  # testing: exact solve through the global-memory tier
 GWTF_FORCE_CLUSTER_TIER = 1 << 29  # testing: exact solve through the cluster tier
 OBJ_SUM, OBJ_MINIMAX = 0, 1

@@ -897,8 +897,29 @@ gwtf_status gwtf_flow_warm_reroute(gwtf_flow_t h, int32_t* node_flow, int32_t* s
   if (!ws) return fail(GWTF_E_NOMEM, "warm_reroute workspace");
   Timer t;
   prof_begin(h, "warm_kernel", &t);
-  CK(h, launch_warm(P, dev[0], dev[1], dev[2], dev[3], ws, F, C, St, Qd, h->stream));
-  h->kernel_launches += 2;
+  CK(h, launch_warm(P, dev[0], dev[1], dev[2], dev[3], ws, F, C, St, Qd, (h->flags & GWTF_WARM_REPAIR_ALL) != 0, h->stream));
+  h->kernel_launches += (P.debug & 4096) ? 3 : 2;
+  // the instances the repair leaves (triage: too much of the flow to re-route; or a stopped
+  // repair): the exact solve of that subset, written straight into the caller's arrays (the
+  // handle's own solver state stays untouched)
+  int32_t* sel = (int32_t*)scratch(h, 28, (B + 1) * 4);
+  const size_t nbl = (size_t)std::max(P.S - 1, 1) * P.Lcap;
+  Problem P2 = P;
+  P2.arcs = (uint32_t*)scratch(h, 29, B * nbl * 4);
+  P2.arc_cnt = (int32_t*)scratch(h, 30, B * std::max(P.S - 1, 1) * 4);
+  P2.arcw = P.arcw ? (int32_t*)scratch(h, 31, B * nbl * 4) : nullptr;
+  int32_t* aug = (int32_t*)scratch(h, 32, B * 4);
+  if (!sel || !P2.arcs || !P2.arc_cnt || (P.arcw && !P2.arcw) || !aug) return fail(GWTF_E_NOMEM, "warm_reroute cold subset");
+  P2.sel = sel;
+  P2.sel_count = sel + B;
+  P2.src_f = dev[0];
+  P2.g = dev[1];
+  P2.snk_f = dev[3];
+  CK(h, launch_warm_collect((int32_t)B, Qd, sel, sel + B, P.stats + 12, h->stream));
+  const int tier = (h->flags & GWTF_FORCE_GLOBAL_TIER) ? 1 : (h->flags & GWTF_FORCE_CLUSTER_TIER) ? 2 : 0;
+  CK(h, launch_ssp(P2, SspOut{F, C, aug, Qd}, h->stream, h->num_sms, tier));
+  CK(h, launch_warm_dense(P2, sel, sel + B, dev[2], aug, St, h->stream));
+  h->kernel_launches += 1 + ssp_launch_count(P, tier) + (P.S > 1 ? 2 : 1);
   prof_end(h, &t);
   if (!inst_status) {  // no status array from the caller: a failed instance fails the call
     std::vector<int32_t> q(B);

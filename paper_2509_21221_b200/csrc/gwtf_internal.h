@@ -71,6 +71,9 @@ struct Problem {
   uint8_t* ws_cluster;
   int32_t ws_cluster_slots;
   int32_t debug;               // GWTF_DEBUG_FLAGS (testing)
+  // exact solve of a subset: the queue hands out sel[0 .. *sel_count) instead of 0 .. B (nullptr: all)
+  const int32_t* sel;
+  const int32_t* sel_count;
   // global workspace for teams whose instance does not fit in shared memory
   uint8_t* ws;
   size_t ws_per_team;
@@ -133,8 +136,12 @@ size_t mc_rounds_smem(int S, int n, int MC, int K, int Mmax);
 cudaError_t launch_mc_rounds(const McRoundsCall& c, cudaStream_t st, int num_sms);
 size_t warm_ws_bytes(const Problem& P, int grid);
 int warm_grid(const Problem& P);
+cudaError_t launch_warm_collect(int32_t B, int32_t* status, int32_t* sel, int32_t* sel_count, unsigned long long* ctr,
+                                cudaStream_t st);
+cudaError_t launch_warm_dense(const Problem& P2, const int32_t* sel, const int32_t* sel_count, int32_t* dense,
+                              const int32_t* aug, int64_t* stats, cudaStream_t st);
 cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* arc, int32_t* snk_f, void* ws,
-                        int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, cudaStream_t st);
+                        int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, bool repair_all, cudaStream_t st);
 cudaError_t launch_scan_costs(const int32_t* v, int64_t count, int32_t* out_max, int32_t* out_min,
                               cudaStream_t st);
 

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
         q = q < P.counters[2] ? P.redo[q] : P.B;
       } else {
         q = atomicAdd(&P.counters[0], 1);
+        if (P.sel) q = q < *P.sel_count ? P.sel[q] : P.B;
       }
       *inst_p = q;
     }

@@ -181,7 +181,11 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   __syncthreads();
 
   for (;;) {
-    if (r == 0 && tid == 0) misc->inst = atomicAdd(&P.counters[4], 1);
+    if (r == 0 && tid == 0) {
+      int q = atomicAdd(&P.counters[4], 1);
+      if (P.sel) q = q < *P.sel_count ? P.sel[q] : P.B;  // subset solve
+      misc->inst = q;
+    }
     cl.sync();
     const int inst = M0->inst;
     cl.sync();  // every CTA has read the leader's value before any CTA exits or it is rewritten

@@ -30,6 +30,7 @@ namespace gwtf {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int32_t kDeferred = 80;  // status: the instance is re-solved cold (triage or failed repair)
 constexpr int kStripList = 256;  // over-capacity arcs listed per instance (more: thread 0 rescans all)
 constexpr int kArcBits = 24;
 constexpr uint64_t kNoPred = (1ull << kArcBits) - 1;
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
   const int64_t E = 2ll * n + (int64_t)S * n + (int64_t)(S - 1) * n * n;
   const int64_t NR = 2 * E + 2;  // residual arcs incl. the bypass pair
   for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
+    if (status_out[b] == kDeferred) continue;  // triage: left to the cold solve
     WarmCtx c;
     c.S = S; c.n = n; c.ld = P.ld; c.N = N; c.E = E; c.M = P.supply[b];
     c.tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
@@ -686,6 +688,7 @@ __global__ void __launch_bounds__(kThreads) warm_smem_kernel(const Problem P, in
   int* ired = (int*)(red + 4);
   auto IN = [&](int s, int i) { return 2 + 2 * (s * n + i); };
   for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
+    if (status_out[b] == kDeferred) continue;  // triage: left to the cold solve
     const int32_t* tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
     const int32_t* src = P.src + (size_t)b * n;
     const int32_t* snk = P.snk + (size_t)b * n;
@@ -1000,10 +1003,100 @@ int warm_grid(const Problem& P) { return (int)std::min<int64_t>(P.B, 148 * 8); }
 
 // status must be a device array of B entries: the repair kernel runs every instance, the fallback
 // kernel the ones it marked 7
+// Triage (before the repair): the units the churned graph can no longer carry (flow above an
+// arc's new capacity: crashed relays, dropped links) against the assignment's flow F0.  A repair
+// has to re-route at least those units with one layered search each, while a cold solve of these
+// small instances costs about F0 searches of the (faster) exact-solve kernels; an instance with
+// kWarmCutShare x cut > F0 is left to the cold solve (status kDeferred, stats {cut, 0, 0}), and so
+// is every instance with fewer than kWarmMinLinks links: there the whole cold batch costs a few
+// microseconds per instance, less than one repaired instance's chain of layered passes (gpt shape:
+// 1,280 links, 16,384 instances cold in 4.4 ms, 730 repaired ones in ~10 ms).
+constexpr int kWarmCutShare = 4;
+constexpr int64_t kWarmMinLinks = 4096;
+__global__ void __launch_bounds__(kThreads) warm_triage_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
+                                                                int32_t* arc_all, int32_t* snk_f_all,
+                                                                int64_t* stats_out, int32_t* status_out, bool repair_all) {
+  __shared__ unsigned long long red[2];
+  const int S = P.S, n = P.n;
+  const int64_t E = 2ll * n + (int64_t)S * n + (int64_t)(S - 1) * n * n;
+  for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
+    WarmCtx c;
+    c.S = S; c.n = n; c.ld = P.ld; c.N = 2 + 2 * S * n; c.E = E; c.M = P.supply[b];
+    c.tile = P.tile + (size_t)b * (S - 1) * n * P.ld;
+    c.src = P.src + (size_t)b * n;
+    c.snk = P.snk + (size_t)b * n;
+    c.cap = P.cap + (size_t)b * S * n;
+    c.alive = P.alive + (size_t)b * S * n;
+    c.alive_prev = P.alive_prev + (size_t)b * S * n;
+    c.src_f = src_f_all + (size_t)b * n;
+    c.g = g_all + (size_t)b * S * n;
+    c.arc = arc_all + (size_t)b * (S - 1) * n * n;
+    c.snk_f = snk_f_all + (size_t)b * n;
+    if (threadIdx.x == 0) { red[0] = 0; red[1] = 0; }
+    __syncthreads();
+    unsigned long long cut = 0, f0 = 0;
+    for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+      const ArcV a = arc_of(c, e);
+      if (*a.x > a.cap) cut += (unsigned long long)(*a.x - a.cap);
+      if (e < n) f0 += (unsigned long long)*a.x;
+    }
+    atomicAdd(&red[0], cut);
+    atomicAdd(&red[1], f0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const bool defer = !repair_all && ((int64_t)(S - 1) * n * n < kWarmMinLinks ||
+                                         (unsigned long long)kWarmCutShare * red[0] > red[1]);
+      status_out[b] = defer ? kDeferred : 0;
+      // {cut, 0, 0}: a repair overwrites it, a cold solve sets [2] to its augmentations
+      if (stats_out) { stats_out[3 * b] = (int64_t)red[0]; stats_out[3 * b + 1] = 0; stats_out[3 * b + 2] = 0; }
+    }
+    __syncthreads();
+  }
+}
+
+// instances left to the cold solve: deferred by the triage, or whose repair stopped (7, 70-79)
+__global__ void warm_collect_kernel(int32_t B, int32_t* status, int32_t* sel, int32_t* sel_count,
+                                    unsigned long long* ctr) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    const int32_t q = status[b];
+    if (q == 7 || q >= 70) {
+      status[b] = kDeferred;
+      sel[atomicAdd(sel_count, 1)] = b;
+      atomicAdd(ctr, 1ull);  // gwtf_flow_stats [12]
+    }
+  }
+}
+
+// the cold-solved instances' link flows into the dense [B][S-1][n][n] layout (zero, then scatter
+// the positive-arc lists), and their augmentation counts into stats[3b + 2]
+__global__ void warm_dense_zero_kernel(const Problem P2, const int32_t* sel, const int32_t* sel_count, int32_t* dense) {
+  const int64_t slab = (int64_t)(P2.S - 1) * P2.n * P2.n, cnt = *sel_count;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cnt * slab; t += (int64_t)gridDim.x * blockDim.x)
+    dense[(int64_t)sel[t / slab] * slab + t % slab] = 0;
+}
+__global__ void warm_dense_scatter_kernel(const Problem P2, const int32_t* sel, const int32_t* sel_count, int32_t* dense,
+                                          const int32_t* aug, int64_t* stats_out) {
+  const int64_t nb = P2.S - 1, per = nb * P2.Lcap, cnt = *sel_count;
+  if (stats_out)
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cnt; t += (int64_t)gridDim.x * blockDim.x)
+      stats_out[3 * (int64_t)sel[t] + 2] = aug[sel[t]];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cnt * per; t += (int64_t)gridDim.x * blockDim.x) {
+    const int b = sel[t / per];
+    const int64_t r = t % per, sb = r / P2.Lcap, e = r % P2.Lcap;
+    const int64_t bs = (int64_t)b * nb + sb;
+    if (e >= P2.arc_cnt[bs]) continue;
+    const uint32_t ent = P2.arcs[bs * P2.Lcap + e];
+    const int u = (int)(ent >> 20), v = (int)((ent >> 8) & 0xFFFu);
+    dense[((int64_t)bs * P2.n + v) * P2.n + u] = (int32_t)(ent & 0xFFu);
+  }
+}
+
 cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* arc, int32_t* snk_f, void* ws,
-                        int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, cudaStream_t st) {
+                        int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, bool repair_all, cudaStream_t st) {
   const int grid = warm_grid(P);
   const size_t N = 2 + 2 * (size_t)P.S * P.n;
+  warm_triage_kernel<<<(int)std::min<int64_t>(P.B, 148 * 8), kThreads, 0, st>>>(P, src_f, g, arc, snk_f, stats, status,
+                                                                                     repair_all);
   uint64_t* labv = (uint64_t*)ws;
   int64_t* pi = (int64_t*)(labv + (size_t)grid * N);
   int32_t* imb = (int32_t*)(pi + (size_t)grid * N);
@@ -1022,8 +1115,23 @@ cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* a
   } else {
     warm_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, pi, imb, F, cost, stats, status);
   }
-  if (!getenv("GWTF_WARM_NO_FALLBACK"))  // testing: see what the repair alone does (status 70-79)
+  if (P.debug & 4096)  // testing (dev builds): the Klein cycle-cancelling fallback instead of the cold solve
     klein_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, stamp, F, cost, stats, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_warm_collect(int32_t B, int32_t* status, int32_t* sel, int32_t* sel_count, unsigned long long* ctr,
+                                cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(sel_count, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return e;
+  warm_collect_kernel<<<(int)std::min<int64_t>((B + 255) / 256, 148 * 4), 256, 0, st>>>(B, status, sel, sel_count, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_warm_dense(const Problem& P2, const int32_t* sel, const int32_t* sel_count, int32_t* dense,
+                              const int32_t* aug, int64_t* stats, cudaStream_t st) {
+  if (P2.S > 1) warm_dense_zero_kernel<<<148 * 8, 256, 0, st>>>(P2, sel, sel_count, dense);
+  warm_dense_scatter_kernel<<<148 * 8, 256, 0, st>>>(P2, sel, sel_count, dense, aug, stats);
   return cudaGetLastError();
 }
 

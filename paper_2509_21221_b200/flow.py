@@ -76,7 +76,7 @@ class Flow:
 
     def __init__(self, cap, src_cost, snk_cost, link_cost, supply, *, max_cap, alive=None, seed=0, inst_base=0,
                  T0=1.7, alpha=0.95, objective=_lib.OBJ_SUM, steady_window=5, deny_after=3, stream=None,
-                 host=False, force_global_tier=False, force_cluster_tier=False):
+                 host=False, force_global_tier=False, force_cluster_tier=False, warm_repair_all=False):
         B, S, n = cap.shape
         self.B, self.S, self.n, self.max_cap = B, S, n, max_cap
         self.host = host
@@ -107,7 +107,8 @@ class Flow:
         d.device = self.device.index if self.device.index is not None else torch.cuda.current_device()
         d.stream = self.stream.cuda_stream
         d.flags = ((_lib.GWTF_HOST_PTRS if host else 0) | (_lib.GWTF_FORCE_GLOBAL_TIER if force_global_tier else 0)
-                   | (_lib.GWTF_FORCE_CLUSTER_TIER if force_cluster_tier else 0))
+                   | (_lib.GWTF_FORCE_CLUSTER_TIER if force_cluster_tier else 0)
+                   | (_lib.GWTF_WARM_REPAIR_ALL if warm_repair_all else 0))
         h = ctypes.c_void_p()
         check("gwtf_flow_create", lib().gwtf_flow_create(ctypes.byref(d), ctypes.byref(h)))
         self.h = h
@@ -278,6 +279,7 @@ class Flow:
             return out
         keys = ("relax_steps", "backward_phases", "augmentations", "bf_passes", "path_nodes")
         d = {k: int(out[i]) for i, k in enumerate(keys)}
+        d["warm_cold_instances"] = int(out[12])  # instances warm_reroute left to the cold solve
         d["redo_64bit"] = int(out[13])  # instances whose 32-bit keys overflowed (re-solved, 64-bit)
         d["launches"] = int(out[15])
         return d

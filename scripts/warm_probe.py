@@ -45,6 +45,6 @@ for r in range(reps + 1):
         tc.append(e[1].elapsed_time(e[2]))
 out = {"config": name, "B": B, "warm_ms": sorted(tw)[len(tw) // 2], "cold_ms": sorted(tc)[len(tc) // 2],
        "F_mismatch": int((F != cold.flow_value).sum()), "cost_mismatch": int((C != cold.total_cost).sum()),
-       "status_nonzero": int((Q != 0).sum()), "stripped": int(S[:, 0].sum()), "cycles": int(S[:, 1].sum()),
-       "augment": int(S[:, 2].sum()), "cold_augment": int(cold.augmentations.sum())}
+       "status_nonzero": int((Q != 0).sum()), "units_cut": int(S[:, 0].sum()),
+       "cold_subset_per_call": fl.stats()["warm_cold_instances"] // (reps + 1), "cold_augment": int(cold.augmentations.sum())}
 print(json.dumps(out))

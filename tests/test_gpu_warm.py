@@ -45,14 +45,17 @@ def _host_instance(cfg, bt, src, snk, link, b, alive=None, upd=None):
                     bt.alive[b] if alive is None else alive[b])
 
 
+@pytest.mark.parametrize("repair_all", [True, False], ids=["repair", "triage"])
 @pytest.mark.parametrize("name,B,samples", [("tiny", 256, 32), ("gpt", 128, 16), ("flow3", 32, 8), ("llama", 8, 4),
                                             ("churn", 4, 2)])
-def test_warm_reroute_parity(name, B, samples):
+def test_warm_reroute_parity(name, B, samples, repair_all):
+    """repair: every instance through the repair kernels (GWTF_WARM_REPAIR_ALL); triage: the default,
+    small or heavily damaged instances re-solved cold on the subset."""
     from paper_2509_21221_b200 import Flow
     cfg = gen.CONFIGS[name]
     hbt, hsrc, hsnk, hlink = harness.host_inputs(cfg, 0, B)
     dbt, src, snk, link = harness.device_inputs(cfg, 0, B)
-    fl = Flow(dbt.cap, src, snk, link, dbt.supply, max_cap=cfg.max_cap, alive=dbt.alive)
+    fl = Flow(dbt.cap, src, snk, link, dbt.supply, max_cap=cfg.max_cap, alive=dbt.alive, warm_repair_all=repair_all)
     fl.solve_batch()
     nf, sf, kf, af = fl.get_assignment()
     base = [oracle.SSPResult(0, 0, 0, nf[b].cpu().numpy(), sf[b].cpu().numpy(), kf[b].cpu().numpy(),
@@ -65,7 +68,10 @@ def test_warm_reroute_parity(name, B, samples):
     assert int(Q.abs().sum()) == 0
     assert torch.equal(F, cold.flow_value) and torch.equal(C, cold.total_cost)
     st = St.cpu().numpy()
-    assert st[:, 0].sum() > 0  # the churn really stripped carried flow
+    assert st[:, 0].sum() > 0  # the churn really cut carried flow
+    ncold = fl.stats()["warm_cold_instances"]
+    if not repair_all and (cfg.S - 1) * cfg.n * cfg.n < 4096:
+        assert ncold == B  # below the triage's size bound every instance is solved cold
     for b in range(min(B, samples)):
         I0 = _host_instance(cfg, hbt, hsrc, hsnk, hlink, b)
         I1 = _host_instance(cfg, hbt, hsrc, hsnk, hlink, b, alive, upd)
@@ -81,7 +87,7 @@ def test_warm_reroute_no_churn_identity():
     from paper_2509_21221_b200 import Flow
     cfg = gen.CONFIGS["gpt"]
     dbt, src, snk, link = harness.device_inputs(cfg, 0, 64)
-    fl = Flow(dbt.cap, src, snk, link, dbt.supply, max_cap=cfg.max_cap, alive=dbt.alive)
+    fl = Flow(dbt.cap, src, snk, link, dbt.supply, max_cap=cfg.max_cap, alive=dbt.alive, warm_repair_all=True)
     sol = fl.solve_batch()
     nf, sf, kf, af = fl.get_assignment()
     nf0, af0 = nf.clone(), af.clone()
