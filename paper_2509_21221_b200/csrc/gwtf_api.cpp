@@ -465,8 +465,9 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     if (maxc < 255 && !getenv("GWTF_NO_TILE8")) {  // and the 8-bit copy when every arc is present
       P.ld8 = (int32_t)((n + 15) / 16 * 16);
       if ((s = alloc(h, &P.tile8, B * nb * n * P.ld8, true)) != GWTF_OK) return bail(s);
-      if ((s = alloc(h, &P.tile8t, B * nb * n * P.ld8, true)) != GWTF_OK) return bail(s);
-      CK(h, cudaMemsetAsync(P.tile8t, 255, B * nb * n * P.ld8, h->stream));  // padding columns
+      // + 16 bytes: the frontier step's 32-bit loads may run up to 3 bytes past the last column
+      if ((s = alloc(h, &P.tile8t, B * nb * n * P.ld8 + 16, true)) != GWTF_OK) return bail(s);
+      CK(h, cudaMemsetAsync(P.tile8t, 255, B * nb * n * P.ld8 + 16, h->stream));  // padding columns
       int32_t bad8 = 0;
       CK(h, cudaMemsetAsync(h->bad_flag, 0, 4, h->stream));
       CK(h, launch_pack_tile8(P, h->bad_flag, h->stream));

@@ -13,7 +13,8 @@
 //     VIMNMX per weight, not the quarter-rate DPX VIADDMNMX), while the out_s key vector is
 //     gathered from the owner CTAs through DSMEM;
 //   * after a boundary's first relaxation since the reset, later ones relax only the columns
-//     whose out-key changed (owner dirty bits) when there are at most KSP of them (frontier);
+//     whose out-key changed (owner dirty bits) when there are at most KSP (8-bit columns: KSP8)
+//     of them (frontier);
 //   * one cluster barrier per boundary step; phase votes and the t* minimum are reduced from
 //     per-CTA slots read by every CTA (no remote atomics, no resets);
 //   * the leader CTA traces the canonical path; the whole cluster locates the path's arcs in the
@@ -38,12 +39,16 @@ constexpr int CT = 512;      // threads per CTA
 constexpr int NW = CT / 32;  // warps per CTA: warp w relaxes rows w, w + NW, ... of a boundary
 constexpr int NBMAX = 64;    // chunk slots of the TMA ring (one chunk of NW rows per bulk copy)
 constexpr int KSP = 32;       // frontier relaxation when at most this many out-keys changed
+constexpr int KSP8 = 256;     // ... with the source-major 8-bit columns (warp per column, rows over the lanes)
 constexpr int KQ = 4;        // register-resident key chunks per lane (16-bit rows up to 1,024 weights)
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr uint64_t INF = ~0ull;
 constexpr uint64_t kBig = 1ull << 62;  // INF inside the branch-free relaxation
 
 __host__ __device__ inline size_t al16c(size_t x) { return (x + 15) & ~size_t(15); }
+// destination rows per CTA: ceil(n / C) rounded up to a multiple of 4, so that a CTA's slice of a
+// source-major 8-bit column starts 4-byte aligned (one 32-bit load covers 4 rows)
+__host__ __device__ inline int cl_rows(int n, int C) { return (((n + C - 1) / C) + 3) & ~3; }
 
 struct Misc {  // per-CTA control block; the leader's copy is authoritative
   int64_t F, cost;
@@ -60,7 +65,7 @@ struct ClLayout {
 };
 __host__ __device__ inline ClLayout cl_layout(const Problem& P, int C) {
   ClLayout L;
-  const size_t R = (P.n + C - 1) / C, SR = (size_t)P.S * R;
+  const size_t R = (size_t)cl_rows(P.n, C), SR = (size_t)P.S * R;
   size_t o = 0;
   L.misc = o; o += al16c(sizeof(Misc));
   L.mbar = o; o += al16c(NBMAX * 8 + NBMAX * 4);  // full barriers + consumed-row counters
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const int r = (int)cl.block_rank(), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cid = blockIdx.x / C;
   const int S = P.S, n = P.n, ld = P.ld, Lt = 2 * S + 1, Lcap = P.Lcap;
-  const int R = (n + C - 1) / C, v0 = r * R, nr = max(0, min(R, n - v0));
+  const int R = cl_rows(n, C), v0 = r * R, nr = max(0, min(R, n - v0));
   const ClLayout L = cl_layout(P, C);
   Misc* misc = (Misc*)(sm + L.misc);
   uint64_t* mbar = (uint64_t*)(sm + L.mbar);
@@ -110,11 +115,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const int DW = (R + 31) / 32;
   uint32_t* dmask = (uint32_t*)(sm + L.dmask);
   const bool track = true;
-  int ksp = KSP;  // frontier threshold (testing override GWTF_DEBUG_FLAGS bits 16..23; 8192: dense only)
-  if (P.debug & 8192) ksp = 0;
-  else if ((P.debug >> 16) & 0xFF) ksp = min(KSP, (P.debug >> 16) & 0xFF);
   uint32_t* spu = aq;                       // frontier step: changed columns (reuses aq)
-  uint64_t* spk = (uint64_t*)(aq + KSP);    // ... and their out-keys
+  uint64_t* spk = (uint64_t*)(aq + KSP8);   // ... and their out-keys
   uint64_t* rowmin = kbuf;                  // ... per-row minima (reuses the gather buffer)
   uint8_t* ring = sm + L.ring;
   const int nbc = L.nbc;
@@ -123,6 +125,10 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   const bool t8 = P.tile8 != nullptr;  // 8-bit rows (every arc present, costs < 255): a quarter of int32
   const bool t16 = !t8 && P.tile16 != nullptr;
   const int ldk = t8 ? P.ld8 : t16 ? P.ld16 : ld;  // weights per streamed row
+  // frontier threshold (testing override GWTF_DEBUG_FLAGS bits 16..23; 8192: dense only)
+  int ksp = t8 ? KSP8 : KSP;
+  if (P.debug & 8192) ksp = 0;
+  else if ((P.debug >> 16) & 0xFF) ksp = min(ksp, (P.debug >> 16) & 0xFF);
   const uint32_t rowbytes = t8 ? (uint32_t)P.ld8 : t16 ? (uint32_t)P.ld16 * 2 : (uint32_t)ld * 4;
   Misc* M0 = cl.map_shared_rank(misc, 0);
   // per-cluster global scratch: path (t* -> s*) and found (gwtf_api.cpp sizes it)
@@ -276,14 +282,36 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
               for (int i = tid; i < nU; i += CT) spk[i] = ldk_out(s, (int)spu[i]);
               for (int j = tid; j < nr; j += CT) rowmin[j] = INF;
               __syncthreads();
-              if (t8) {  // source-major 8-bit column: consecutive threads read consecutive rows
+              if (t8) {
+                // source-major 8-bit columns: warp w takes columns w, w + NW, ... (eight in flight),
+                // lane l the CTA's rows 4l .. 4l+3 of each (one aligned 32-bit load); per-lane row
+                // minima in registers, one shared-memory atomicMin per (warp, row)
                 const uint8_t* colb = P.tile8t + ((size_t)inst * (S - 1) + s) * (size_t)n * P.ld8 + v0;
-                for (int t = tid; t < nr * nU; t += CT) {
-                  const int i = t / nr, j = t - i * nr;
-                  const uint64_t k = spk[i];
-                  if (k == INF) continue;
-                  const uint32_t w = colb[(size_t)spu[i] * P.ld8 + j];  // tile8 holds no absent arc
-                  atomicMin((unsigned long long*)&rowmin[j], (unsigned long long)(k + ((uint64_t)w << kHopBits) + 1ull));
+                for (int jb = 0; jb < nr; jb += 128) {
+                  uint64_t rm[4] = {INF, INF, INF, INF};
+                  const bool on = jb + 4 * lane < nr;
+                  for (int i0 = warp; i0 < nU; i0 += 8 * NW) {
+                    uint32_t wv[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                      const int i = i0 + c * NW;
+                      wv[c] = (i < nU && on) ? *(const uint32_t*)(colb + (size_t)spu[i] * P.ld8 + jb + 4 * lane) : 0u;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                      const int i = i0 + c * NW;
+                      const uint64_t kk = i < nU ? spk[i] : INF;
+                      if (kk == INF) continue;
+#pragma unroll
+                      for (int k = 0; k < 4; ++k)  // tile8 holds no absent arc
+                        rm[k] = umin64(rm[k], kk + ((uint64_t)((wv[c] >> (8 * k)) & 0xFFu) << kHopBits) + 1ull);
+                    }
+                  }
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    const int j = jb + 4 * lane + k;
+                    if (j < nr && rm[k] != INF) atomicMin((unsigned long long*)&rowmin[j], (unsigned long long)rm[k]);
+                  }
                 }
               } else {
                 for (int t = tid; t < nr * nU; t += CT) {
@@ -1078,7 +1106,7 @@ int ssp_cluster_size(const Problem& P) {
               cl_layout(P, C).total, cl_layout(P, C).nbc, cudaGetErrorString(e), ncl);
     if (e != cudaSuccess || ncl < 1) { cudaGetLastError(); continue; }
     const long long waves = (P.B + ncl - 1) / ncl;
-    const long long cost = waves * ((P.n + C - 1) / C + 16);
+    const long long cost = waves * (cl_rows(P.n, C) + 16);
     if (best == 0 || cost < best_cost) { best_cost = cost; best = C; }
   }
   if (const char* f = getenv("GWTF_CLUSTER_SIZE")) best = atoi(f);  // testing override
