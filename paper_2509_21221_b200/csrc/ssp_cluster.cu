@@ -393,6 +393,8 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           TMARK(13);  // stream issue + row-key prefetch
           const uint32_t lim = T32 > (uint32_t)maxw ? T32 - (uint32_t)maxw : 0u;
           int wide = lim == 0u || (P.debug & 32) || (t8 && T32 < 255u);  // testing (32): force the 64-bit path
+          const bool kreg8 = t8 && ldk == 16 * 32 * 2;  // 8-bit rows of 1,024 weights
+          const bool perm8 = kreg8 && !nostream;          // the register-key layout below
           for (int u0 = 0; u0 < ldk; u0 += 4 * CT) {  // gather out_s from L2 (4 loads in flight)
             uint64_t kk[4];
 #pragma unroll
@@ -411,14 +413,16 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 if (c >= lim || hops + 1 >= (1ull << H32)) wide = 1;
                 k32 = ((uint32_t)c << H32) + (uint32_t)hops + 1u;
               }
-              kb32[u] = k32;
+              // 8-bit rows of 1,024 weights: lane l's register keys (columns 16 (l + 32q) + 4t + e) are
+              // stored at uint4 (4q + t) * 32 + l, so that the warps' 16-byte loads below are
+              // conflict-free (the natural layout puts a lane's pieces 64 B apart: 4-way conflicts)
+              kb32[perm8 ? (((((u >> 9) << 2) + ((u >> 2) & 3)) << 5) + ((u >> 4) & 31)) * 4 + (u & 3) : u] = k32;
             }
           }
           wide = __syncthreads_or(wide) && !nostream;
           // 16-bit rows of up to 1,024 weights: every lane keeps the 32-bit keys of its own
           // columns (chunks c = lane + 32q, 8 weights each) in registers for the whole step
           const bool kreg = t16 && ldk <= 8 * 32 * KQ;
-          const bool kreg8 = t8 && ldk == 16 * 32 * 2;  // 8-bit rows of 1,024 weights
           uint4 kr[2 * KQ];
           if (kreg && !wide) {
             const uint4* kv4 = (const uint4*)kb32;
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
 #pragma unroll
             for (int q = 0; q < 2; ++q)
 #pragma unroll
-              for (int t = 0; t < 4; ++t) kr[4 * q + t] = kv4[4 * (lane + 32 * q) + t];
+              for (int t = 0; t < 4; ++t) kr[4 * q + t] = kv4[(4 * q + t) * 32 + lane];
           }
           TMARK(0);
           int ch = 0;
@@ -715,11 +719,17 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
           }
           if (s == 0) { cl.sync(); break; }
           const uint32_t* al = arcs + (size_t)(s - 1) * Lcap;
+          // the thread's first list entry is fetched together with the list length (one L2 round
+          // trip instead of two; entries past the length are never used)
+          const int e0 = r * CT + tid;
+          uint32_t ent0 = 0u;
+          int32_t w0 = 0;
+          if (e0 < Lcap) { ent0 = __ldcg(&al[e0]); w0 = __ldcg(&arcw[(size_t)(s - 1) * Lcap + e0]); }
           const int c = __ldcg(&cnt[s - 1]);
           int ch = 0;
-          for (int e = r * CT + tid; e < c; e += C * CT) {
-            const uint32_t ent = __ldcg(&al[e]);
-            const int32_t w = __ldcg(&arcw[(size_t)(s - 1) * Lcap + e]);
+          for (int e = e0; e < c; e += C * CT) {
+            const uint32_t ent = e == e0 ? ent0 : __ldcg(&al[e]);
+            const int32_t w = e == e0 ? w0 : __ldcg(&arcw[(size_t)(s - 1) * Lcap + e]);
             const int u = (int)(ent >> 20), v = (int)((ent >> 8) & 0xFFFu);
             uint64_t ki = ldk_in(s, v);
             const uint64_t kov = ldk_out(s, v);
