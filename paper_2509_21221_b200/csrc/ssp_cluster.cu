@@ -278,10 +278,12 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                 int k = atomicAdd(&misc->ucnt, __popc(m));
                 for (; m; m &= m - 1) spu[k++] = (tid / DW) * R + (tid % DW) * 32 + (__ffs(m) - 1);
               }
-              __syncthreads();
-              for (int i = tid; i < nU; i += CT) spk[i] = ldk_out(s, (int)spu[i]);
               for (int j = tid; j < nr; j += CT) rowmin[j] = INF;
               __syncthreads();
+              if (!t8) {  // the int32 path reads the keys from shared memory
+                for (int i = tid; i < nU; i += CT) spk[i] = ldk_out(s, (int)spu[i]);
+                __syncthreads();
+              }
               if (t8) {
                 // source-major 8-bit columns: warp w takes columns w, w + NW, ... (eight in flight),
                 // lane l the CTA's rows 4l .. 4l+3 of each (one aligned 32-bit load); per-lane row
@@ -291,16 +293,20 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
                   uint64_t rm[4] = {INF, INF, INF, INF};
                   const bool on = jb + 4 * lane < nr;
                   for (int i0 = warp; i0 < nU; i0 += 8 * NW) {
+                    // the columns' bytes (HBM) and their out-keys (the owners, one broadcast DSMEM
+                    // load per warp) in flight together
                     uint32_t wv[8];
+                    uint64_t kv[8];
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                       const int i = i0 + c * NW;
-                      wv[c] = (i < nU && on) ? *(const uint32_t*)(colb + (size_t)spu[i] * P.ld8 + jb + 4 * lane) : 0u;
+                      const int u = i < nU ? (int)spu[i] : 0;
+                      wv[c] = (i < nU && on) ? *(const uint32_t*)(colb + (size_t)u * P.ld8 + jb + 4 * lane) : 0u;
+                      kv[c] = i < nU ? ldk_out(s, u) : INF;
                     }
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                      const int i = i0 + c * NW;
-                      const uint64_t kk = i < nU ? spk[i] : INF;
+                      const uint64_t kk = kv[c];
                       if (kk == INF) continue;
 #pragma unroll
                       for (int k = 0; k < 4; ++k)  // tile8 holds no absent arc
