@@ -87,9 +87,11 @@ gwtf_status cuda_fail(gwtf_flow_s* h, cudaError_t e, const char* where) {
 // cudaMallocFromPoolAsync on the handle's stream): creating and destroying handles back to back (the
 // e2e pipeline, node-addition batches, multi-source turns) reuses pool memory instead of paying
 // cudaMalloc / cudaFree, whose unmap synchronises the device.  A private pool leaves the device's
-// default pool (and other libraries' settings) alone; it keeps up to kPoolKeep bytes after a
-// synchronisation, so a large handle's memory (stress: GBs) goes back to the device.
-constexpr uint64_t kPoolKeep = 1ull << 30;
+// default pool (and other libraries' settings) alone.  It keeps up to kPoolKeep bytes after a
+// synchronisation (GWTF_POOL_KEEP_MB overrides): 8 GB, 4% of a B200's HBM, holds one stress handle
+// (4.6 GB of tiles, copies and state), so re-creating it maps no new memory (measured: a create +
+// destroy pair cost 0.1-0.7 s more with a 1 GB threshold); anything above goes back to the device.
+constexpr uint64_t kPoolKeep = 8ull << 30;
 void* dev_alloc(gwtf_flow_s* h, size_t bytes) {
   static cudaMemPool_t pools[64] = {};
   static bool tried[64] = {};
@@ -103,6 +105,7 @@ void* dev_alloc(gwtf_flow_s* h, size_t bytes) {
       props.location.id = h->device;
       if (cudaMemPoolCreate(&pools[h->device], &props) == cudaSuccess) {
         uint64_t keep = kPoolKeep;
+        if (const char* f = getenv("GWTF_POOL_KEEP_MB")) keep = (uint64_t)strtoull(f, nullptr, 10) << 20;
         cudaMemPoolSetAttribute(pools[h->device], cudaMemPoolAttrReleaseThreshold, &keep);
       } else {
         pools[h->device] = nullptr;
