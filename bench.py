@@ -727,6 +727,10 @@ def main():
     if ssp_name and dom != ssp_name:
         line["min_plus_roofline"] = ssp_roof(ssp_name)
 
+    # the timed handle is done: its device memory goes back before the end-to-end pipeline creates its own
+    fl.close()
+    del su, fl, sol, rr, flush
+    torch.cuda.empty_cache()
     if not (args.quick or args.no_e2e):  # every rank, whole-job value from the slowest rank
         if world > 1:
             dist.barrier()
