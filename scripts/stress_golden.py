@@ -5,7 +5,8 @@ Calls only gen/ (inputs) and oracle/ (values); the GPU test tests/test_gpu_parit
 test_stress_full_golden compares the CUDA path against this file.  Runtime: ~1-2 h per
 instance on one core (Dijkstra over 66 M arcs per augmentation), hence a stored file.
 
-  python scripts/stress_golden.py [--inst 0 1 ...]
+  python scripts/stress_golden.py [--inst 0 1 ...] [--out PATH]
+  python scripts/stress_golden.py --merge PART.json ...   (parts written by parallel --out runs)
 """
 import argparse
 import hashlib
@@ -23,9 +24,20 @@ import oracle  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--inst", type=int, nargs="+", default=[0])
+ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "stress_ssp.json"))
+ap.add_argument("--merge", nargs="+", default=None, help="merge part files into the golden file and exit")
 a = ap.parse_args()
 cfg = gen.CONFIGS["stress"]
-out_path = os.path.join(ROOT, "tests", "golden", "stress_ssp.json")
+out_path = a.out
+if a.merge:
+    gold = os.path.join(ROOT, "tests", "golden", "stress_ssp.json")
+    res = json.load(open(gold))
+    for part in a.merge:
+        res["instances"].update(json.load(open(part))["instances"])
+    res["instances"] = dict(sorted(res["instances"].items(), key=lambda kv: int(kv[0])))
+    with open(gold, "w") as f:
+        json.dump(res, f, indent=1)
+    sys.exit(0)
 res = json.load(open(out_path)) if os.path.exists(out_path) else {
     "source": "scripts/stress_golden.py (oracle.ssp on gen.CONFIGS['stress'])", "instances": {}}
 for i in a.inst:
