@@ -112,3 +112,28 @@ def test_warm_reroute_host_pointer_mode():
     F, C, St, Q = fl.warm_reroute(nf, sf, kf, af)
     cold = fl.solve_batch()
     assert torch.equal(F, cold.flow_value) and torch.equal(C, cold.total_cost) and int(Q.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("repair_all", [False, True])
+def test_warm_reroute_cluster_tier(repair_all):
+    """The cold subset through the cluster tier (its positive-arc lists and weights redirected to
+    scratch, node / src / snk flows straight into the caller's arrays): stress distributions at 8 x 256."""
+    from paper_2509_21221_b200 import Flow
+    cfg = gen.CONFIGS["stress_s"]
+    B = 3
+    hbt, hsrc, hsnk, hlink = harness.host_inputs(cfg, 0, B)
+    dbt, src, snk, link = harness.device_inputs(cfg, 0, B)
+    fl = Flow(dbt.cap, src, snk, link, dbt.supply, max_cap=cfg.max_cap, alive=dbt.alive, force_cluster_tier=True,
+              warm_repair_all=repair_all)
+    fl.solve_batch()
+    nf, sf, kf, af = fl.get_assignment()
+    alive, upd = _churn(cfg, hbt, seed=11, kill_p=0.05)
+    fl.apply_churn(torch.from_numpy(alive).cuda(), torch.from_numpy(upd).cuda() if len(upd) else None)
+    F, C, St, Q = fl.warm_reroute(nf, sf, kf, af)
+    cold = fl.solve_batch()
+    torch.cuda.synchronize()
+    assert int(Q.abs().sum()) == 0
+    assert torch.equal(F, cold.flow_value) and torch.equal(C, cold.total_cost)
+    I1 = _host_instance(cfg, hbt, hsrc, hsnk, hlink, 0, alive, upd)
+    assert oracle.certify(I1, int(F[0]), int(C[0]), nf[0].cpu().numpy(), sf[0].cpu().numpy(), kf[0].cpu().numpy(),
+                          af[0].cpu().numpy()) == 0
