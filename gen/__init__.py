@@ -115,6 +115,10 @@ CONFIGS = {
     # carry >= 17 hop bits (its shift-and-mask weight path), with a small supply for the oracle
     "stress_h": Config("stress_h", 6, S=64, n=512, M=16, max_cap=20, cap=(1, 20), B=2, cost=(1, 100),
                        max_rounds=120 + 2 * 16),
+    # stress distributions at 3 x 1,024: the cluster tier's 1,024-column 8-bit fast path (register keys)
+    # with a supply small enough for the oracle in seconds
+    "stress_w": Config("stress_w", 8, S=3, n=1024, M=1500, max_cap=20, cap=(1, 20), B=2, cost=(1, 100),
+                       max_rounds=120 + 2 * 1500),
     # node-addition setting 1 (PAPER.md:446-471 and its Table, "Node addition (top)"): 97 nodes = 1 data
     # holder + 8 stages x 12 clients, capacities U{1..20}, interlayer costs U{1..100}; S candidates join
     "addition": Config("addition", 7, S=8, n=12, M=64, max_cap=20, cap=(1, 20), B=1, cost=(1, 100),

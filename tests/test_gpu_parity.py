@@ -311,6 +311,24 @@ def test_cluster_tier_parity_forced(name, B, C, monkeypatch):
     assert (sol.status == 0).all()
 
 
+def test_cluster_tier_full_width():
+    """3 x 1,024 stress distributions: the cluster tier's 1,024-column 8-bit fast path (register keys in
+    the permuted conflict-free layout, sparse 8-bit frontier steps of up to 256 columns), full assignment."""
+    cfg = gen.CONFIGS["stress_w"]
+    B = 2
+    fl, *_ = _gpu_flow(cfg, 0, B)
+    sol = fl.solve_batch()
+    nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    for b in range(B):
+        r = _oracle_ssp(cfg, bt, src, snk, link, b)
+        assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
+        assert np.array_equal(af[b], r.arc_flow) and np.array_equal(nf[b], r.node_flow), b
+        assert np.array_equal(sf[b], r.src_flow) and np.array_equal(kf[b], r.snk_flow), b
+    assert (sol.status == 0).all()
+    assert fl.stats()["path_nodes"] > 0  # the cluster tier ran (it alone counts traced path nodes)
+
+
 def test_cluster_tier_stress_hops():
     """64 x 512 stress distributions: >= 17 hop bits in the 32-bit keys, register-resident keys."""
     cfg = gen.CONFIGS["stress_h"]
