@@ -241,9 +241,10 @@ gwtf_status gwtf_flow_greedy_baseline(gwtf_flow_t h, int64_t* flow_value, int64_
  * PAPER.md:274-288 crash handling), on the handle's current (churned) graph,
  * starting from a pre-churn assignment instead of zero flow.  Per instance:
  *   0. triage: when 4 x (units the churned graph can no longer carry) > the assignment's flow,
- *      re-routing would cost about as many searches as a cold solve, and instances with fewer
- *      than 4,096 links are cheaper to solve cold than to repair: those are solved cold (the
- *      create flag GWTF_WARM_REPAIR_ALL skips the triage);
+ *      re-routing would cost about as many searches as a cold solve; instances with fewer than
+ *      4,096 links are cheaper to solve cold than to repair, and instances whose repair state
+ *      exceeds 100 KB of shared memory (the cluster-tier shapes) are better served by the cold
+ *      cluster tier: those are solved cold (the create flag GWTF_WARM_REPAIR_ALL skips the triage);
  *   1. otherwise the potential-carrying repair: potentials of the kept flow (Bellman-Ford), cut
  *      the units over capacity (crashed relay, relay over capacity, link / src / snk now
  *      GWTF_ABSENT), saturate the rejoined relays' shortcuts, route the excesses to the

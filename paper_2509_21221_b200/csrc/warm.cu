@@ -1015,7 +1015,8 @@ constexpr int kWarmCutShare = 4;
 constexpr int64_t kWarmMinLinks = 4096;
 __global__ void __launch_bounds__(kThreads) warm_triage_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
                                                                 int32_t* arc_all, int32_t* snk_f_all,
-                                                                int64_t* stats_out, int32_t* status_out, bool repair_all) {
+                                                                int64_t* stats_out, int32_t* status_out, bool repair_all,
+                                                                bool smem_repair) {
   __shared__ unsigned long long red[2];
   const int S = P.S, n = P.n;
   const int64_t E = 2ll * n + (int64_t)S * n + (int64_t)(S - 1) * n * n;
@@ -1044,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads) warm_triage_kernel(const Problem P, 
     atomicAdd(&red[1], f0);
     __syncthreads();
     if (threadIdx.x == 0) {
-      const bool defer = !repair_all && ((int64_t)(S - 1) * n * n < kWarmMinLinks ||
+      const bool defer = !repair_all && (!smem_repair || (int64_t)(S - 1) * n * n < kWarmMinLinks ||
                                          (unsigned long long)kWarmCutShare * red[0] > red[1]);
       status_out[b] = defer ? kDeferred : 0;
       // {cut, 0, 0}: a repair overwrites it, a cold solve sets [2] to its augmentations
@@ -1095,16 +1096,18 @@ cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* a
                         int64_t* F, int64_t* cost, int64_t* stats, int32_t* status, bool repair_all, cudaStream_t st) {
   const int grid = warm_grid(P);
   const size_t N = 2 + 2 * (size_t)P.S * P.n;
+  // the repair runs in shared memory when one instance's state fits (<= 100 KB: at least two CTAs per
+  // SM); larger instances (the cluster-tier shapes) are solved cold unless every repair is asked for --
+  // one 256-thread CTA per instance over global memory cannot keep up with the cluster tier
+  const size_t wsm = ws_layout(P.S, P.n).total;
+  const bool smem_repair = wsm <= 100 * 1024 && P.S > 1;
   warm_triage_kernel<<<(int)std::min<int64_t>(P.B, 148 * 8), kThreads, 0, st>>>(P, src_f, g, arc, snk_f, stats, status,
-                                                                                     repair_all);
+                                                                                     repair_all, smem_repair);
   uint64_t* labv = (uint64_t*)ws;
   int64_t* pi = (int64_t*)(labv + (size_t)grid * N);
   int32_t* imb = (int32_t*)(pi + (size_t)grid * N);
   int32_t* stamp = imb + (size_t)grid * N;
-  // the shared-memory repair when one instance's state fits (<= 100 KB: at least two CTAs per SM),
-  // else the global-memory one; both leave status 7 to the Klein fallback
-  const size_t wsm = ws_layout(P.S, P.n).total;
-  if (wsm <= 100 * 1024 && P.S > 1) {
+  if (smem_repair) {
     cudaError_t e = cudaFuncSetAttribute(warm_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
