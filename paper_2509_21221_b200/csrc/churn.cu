@@ -40,6 +40,27 @@ __global__ void pack_tile16_kernel(const Problem P) {
   }
 }
 
+// 16-bit copy of the padded tiles for the shared-memory tier (half the shared memory per instance:
+// more instances resident per SM); valid only when every arc within n is present with a cost <
+// 65535 (bit 0 of bad otherwise); padding columns 0 (their keys are INF)
+__global__ void pack_tile16s_kernel(const Problem P, int32_t* bad) {
+  const size_t per = (size_t)(P.S - 1) * P.n * P.ld;
+  const size_t total = (size_t)P.B * per;
+  int fail = 0;
+  for (size_t t = gtid(); t < total; t += gstride()) {
+    const size_t b = t / per, r = t - b * per;
+    const int c = (int)(r % P.ld);
+    const int32_t v = P.tile[t];
+    uint16_t o = 0;
+    if (c < P.n) {
+      if (v == kAbsent || v >= 65535) fail = 1;
+      else o = (uint16_t)v;
+    }
+    P.tile16s[b * (size_t)P.tile16s_stride + r] = o;
+  }
+  if (fail) atomicOr(bad, 1);
+}
+
 // 8-bit copy of the padded tiles (the cluster tier streams a quarter of the int32 bytes): valid
 // only when every arc within n is present with a cost < 255 (bit 0 of bad otherwise); padding = 255
 __global__ void pack_tile8_kernel(const Problem P, int32_t* bad) {
@@ -105,6 +126,10 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
         if (c == kAbsent || c >= 255) atomicOr(bad, 8);
         P.tile8[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld8 + w] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
         P.tile8t[(((size_t)b * (P.S - 1) + s) * P.n + w) * P.ld8 + v] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
+      }
+      if (P.tile16s) {  // the shared-memory tier's 16-bit copy: an absent link or a cost >= 65535 retires it (bit 16)
+        if (c == kAbsent || c >= 65535) atomicOr(bad, 16);
+        else P.tile16s[(size_t)b * P.tile16s_stride + ((size_t)s * P.n + v) * P.ld + w] = (uint16_t)c;
       }
       if (P.tile16) {  // the cluster tier's 16-bit copy; a finite cost >= t16code retires it (bit 2)
         if (c != kAbsent && c >= P.t16code) atomicOr(bad, 2);
@@ -266,6 +291,12 @@ __global__ void eq1_kernel(int32_t B, int32_t S, int32_t n, int32_t L, const int
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st) {
   const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld;
   if (total) pad_tiles_kernel<<<grid_for(total), 256, 0, st>>>(P, link);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_tile16s(const Problem& P, int32_t* bad, cudaStream_t st) {
+  const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld;
+  if (total && P.tile16s) pack_tile16s_kernel<<<grid_for(total), 256, 0, st>>>(P, bad);
   return cudaGetLastError();
 }
 

@@ -99,13 +99,14 @@ struct SspLayout {
   size_t misc, tile, kin, kout, g, capE, src, snk, srcf, snkf, arcs, cnt, path, total;
 };
 // misc block: 0 mbarrier | 8 F | 16 cost | 24 tnew | 32 A | 36 status | 40 inst
-__host__ __device__ inline SspLayout ssp_layout(const Problem& P, bool with_tile, int key_bytes) {
+// tile_bytes: 4 (int32 tiles) or 2 (the 16-bit copy, Problem::tile16s)
+__host__ __device__ inline SspLayout ssp_layout(const Problem& P, bool with_tile, int key_bytes, int tile_bytes = 4) {
   SspLayout L;
   size_t o = 0;
   const size_t Sn = (size_t)P.S * P.n, Sld = (size_t)P.S * P.ld;
   const size_t nb = (size_t)(P.S > 1 ? P.S - 1 : 0);
   L.misc = o; o += 64;
-  L.tile = o; if (with_tile) o += al16(nb * P.n * P.ld * 4);
+  L.tile = o; if (with_tile) o += al16(nb * P.n * P.ld * tile_bytes);
   L.kin = o; o += al16((Sld + 4) * key_bytes);
   L.kout = o; o += al16((Sld + 4) * key_bytes);
   L.g = o; o += al16(Sn * 4);
@@ -124,7 +125,9 @@ __host__ __device__ inline SspLayout ssp_layout(const Problem& P, bool with_tile
 // node ids of the trace: layer << 16 | position
 __device__ __forceinline__ int nid(int layer, int pos) { return (layer << 16) | pos; }
 
-template <int TPI, bool kSmem, bool k32, bool kRedo>
+// k16: the instance's tiles are staged from the 16-bit copy (Problem::tile16s: every arc present,
+// costs < 65535) and widened on use -- half the shared memory, so more instances per SM
+template <int TPI, bool kSmem, bool k32, bool kRedo, bool k16>
 __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TPI : 6) ssp_kernel(const Problem P, const SspOut o, const size_t ws_bytes) {
   using K = typename KT<k32>::K;
   constexpr K INF = KT<k32>::INF;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
   uint8_t* base;
   if constexpr (kSmem) base = smem + (size_t)T.id * ws_bytes;
   else base = P.ws + (size_t)(blockIdx.x * teams_per_cta + T.id) * ws_bytes;
-  const SspLayout L = ssp_layout(P, kSmem, sizeof(K));
+  const SspLayout L = ssp_layout(P, kSmem, sizeof(K), k16 ? 2 : 4);
   uint64_t* mbar = (uint64_t*)(base + L.misc);
   int64_t* F_p = (int64_t*)(base + L.misc + 8);
   int64_t* cost_p = (int64_t*)(base + L.misc + 16);
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
   const int lane = threadIdx.x & 31;
   const int Lt = 2 * S + 1;  // layer of t*
   const size_t tile_elems = (size_t)(S - 1) * n * ld;
-  const uint32_t tile_bytes = (uint32_t)(tile_elems * 4);
+  const uint32_t tile_bytes = k16 ? (uint32_t)(P.tile16s_stride * 2) : (uint32_t)(tile_elems * 4);
   uint32_t phase = 0;
   unsigned long long n_relax = 0, n_back = 0, n_pass = 0;
 
@@ -195,16 +198,26 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
     // ---- stage the instance: tiles by TMA bulk copy, the rest by plain loads ----
     const int32_t* gtile = P.tile + (size_t)inst * tile_elems;
     const int32_t* tile = gtile;
+    const uint16_t* tile16 = (const uint16_t*)(base + L.tile);  // k16: the staged 16-bit copy
     if constexpr (kSmem) {
       tile = (const int32_t*)(base + L.tile);
+      const uint8_t* gsrc = k16 ? (const uint8_t*)(P.tile16s + (size_t)inst * P.tile16s_stride) : (const uint8_t*)gtile;
       if (T.tid == 0 && tile_bytes) {
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(mbar, tile_bytes);
         for (uint32_t off = 0; off < tile_bytes; off += 32768u)
-          bulk_g2s((uint8_t*)(base + L.tile) + off, (const uint8_t*)gtile + off,
-                   tile_bytes - off < 32768u ? tile_bytes - off : 32768u, mbar);
+          bulk_g2s((uint8_t*)(base + L.tile) + off, gsrc + off, tile_bytes - off < 32768u ? tile_bytes - off : 32768u, mbar);
       }
     }
+    // weight of tile entry idx in the key arithmetic's form (pre-shifted for 32-bit keys)
+    auto wgt = [&](size_t idx) -> int32_t {
+      if constexpr (k16) {
+        const uint32_t c = tile16[idx];
+        return k32 ? (int32_t)((c << H) + 1u) : (int32_t)c;
+      } else {
+        return tile[idx];
+      }
+    };
     const int64_t M = P.supply[inst];
     for (int k = T.tid; k < Sn; k += TPI) {
       g[k] = 0;
@@ -221,7 +234,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
     if (kSmem && tile_bytes) {
       mbar_wait(mbar, phase);
       phase ^= 1u;
-      if constexpr (k32) {  // pre-shift the weights in place: (C << H) + 1, absent -> INF
+      if constexpr (k32 && !k16) {  // pre-shift the weights in place: (C << H) + 1, absent -> INF
         T.sync();
         int32_t* tw = (int32_t*)(base + L.tile);
         for (size_t k = T.tid; k < tile_elems; k += TPI) tw[k] = KT<true>::prep(tw[k], H);
@@ -262,15 +275,29 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
             const int v = vb + gi;
             K acc = INF;
             if (v < n) {
-              const int4* row = (const int4*)(Ts + (size_t)v * ld);
-              for (int c = li; c < chunks; c += G) {
-                const int4 w = row[c];
-                K kk[4];
-                load_keys4<k32>(ko + 4 * c, kk);
-                acc = KT<k32>::relax(acc, kk[0], w.x, one);
-                acc = KT<k32>::relax(acc, kk[1], w.y, one);
-                acc = KT<k32>::relax(acc, kk[2], w.z, one);
-                acc = KT<k32>::relax(acc, kk[3], w.w, one);
+              if constexpr (k16) {  // 4 weights per 8-byte load, widened (no absent arc in this copy)
+                const uint2* row = (const uint2*)(tile16 + ((size_t)s * n + v) * ld);
+                for (int c = li; c < chunks; c += G) {
+                  const uint2 w = row[c];
+                  K kk[4];
+                  load_keys4<k32>(ko + 4 * c, kk);
+                  const uint32_t c0 = w.x & 0xFFFFu, c1 = w.x >> 16, c2 = w.y & 0xFFFFu, c3 = w.y >> 16;
+                  acc = KT<k32>::relax(acc, kk[0], k32 ? (int32_t)((c0 << H) + 1u) : (int32_t)c0, one);
+                  acc = KT<k32>::relax(acc, kk[1], k32 ? (int32_t)((c1 << H) + 1u) : (int32_t)c1, one);
+                  acc = KT<k32>::relax(acc, kk[2], k32 ? (int32_t)((c2 << H) + 1u) : (int32_t)c2, one);
+                  acc = KT<k32>::relax(acc, kk[3], k32 ? (int32_t)((c3 << H) + 1u) : (int32_t)c3, one);
+                }
+              } else {
+                const int4* row = (const int4*)(Ts + (size_t)v * ld);
+                for (int c = li; c < chunks; c += G) {
+                  const int4 w = row[c];
+                  K kk[4];
+                  load_keys4<k32>(ko + 4 * c, kk);
+                  acc = KT<k32>::relax(acc, kk[0], w.x, one);
+                  acc = KT<k32>::relax(acc, kk[1], w.y, one);
+                  acc = KT<k32>::relax(acc, kk[2], w.z, one);
+                  acc = KT<k32>::relax(acc, kk[3], w.w, one);
+                }
               }
             }
             for (int off = G >> 1; off > 0; off >>= 1) acc = shfl_min<K>(acc, off, G);
@@ -349,7 +376,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
             const K kov = kout[idx];
             if (g[s * n + v] > 0 && kov != INF && kov + 1 < ki) ki = kov + 1;
             if (ki == INF) continue;
-            const K cand = KT<k32>::rev(ki, tile[((size_t)(s - 1) * n + v) * ld + u]);
+            const K cand = KT<k32>::rev(ki, wgt(((size_t)(s - 1) * n + v) * ld + u));
             K old;
             if constexpr (k32) old = atomicMin((unsigned int*)&kout[(s - 1) * ld + u], (unsigned int)cand);
             else old = atomicMin((unsigned long long*)&kout[(s - 1) * ld + u], (unsigned long long)cand);
@@ -409,13 +436,14 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
             if (s == 0) {
               if (!KT<k32>::absent(src[i]) && KT<k32>::src_key(src[i]) == kx) pred = 0;
             } else {
-              const int32_t* row = tile + ((size_t)(s - 1) * n + i) * ld;
+              const size_t row = ((size_t)(s - 1) * n + i) * ld;
               for (int b = 0; b < n && pred < 0; b += 32) {
                 const int u = b + lane;
                 bool ok = false;
-                if (u < n && !KT<k32>::absent(row[u])) {
+                const int32_t w = u < n ? wgt(row + u) : 0;
+                if (u < n && !KT<k32>::absent(w)) {
                   const K k = kout[(s - 1) * ld + u];
-                  ok = k != INF && KT<k32>::plus(k, row[u]) == kx;
+                  ok = k != INF && KT<k32>::plus(k, w) == kx;
                 }
                 const uint32_t m = __ballot_sync(0xffffffffu, ok);
                 if (m) pred = nid(2 * s, b + __ffs(m) - 1);
@@ -439,7 +467,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
                 if ((int)(ent >> 20) != i) continue;
                 const int v = (int)((ent >> 8) & 0xFFFu);
                 const K k = kin[(s + 1) * ld + v];
-                if (k != INF && KT<k32>::rev_tight(k, tile[((size_t)s * n + v) * ld + i], kx)) best = min(best, (uint32_t)v);
+                if (k != INF && KT<k32>::rev_tight(k, wgt(((size_t)s * n + v) * ld + i), kx)) best = min(best, (uint32_t)v);
               }
               best = __reduce_min_sync(0xffffffffu, best);
               if (best != 0xFFFFFFFFu) pred = nid(2 * s + 3, (int)best);
@@ -577,10 +605,10 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
   }
 }
 
-template <int TPI, bool kSmem, bool k32, bool kRedo>
+template <int TPI, bool kSmem, bool k32, bool kRedo, bool k16 = false>
 cudaError_t launch_one(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms) {
-  const size_t ws = ssp_layout(P, kSmem, k32 ? 4 : 8).total;
-  auto k = ssp_kernel<TPI, kSmem, k32, kRedo>;
+  const size_t ws = ssp_layout(P, kSmem, k32 ? 4 : 8, k16 ? 2 : 4).total;
+  auto k = ssp_kernel<TPI, kSmem, k32, kRedo, k16>;
   if (kSmem) {
     const size_t limit = 227 * 1024;
     int teams = TPI >= 128 ? 1 : 128 / TPI;
@@ -610,6 +638,12 @@ cudaError_t launch_one(const Problem& P, const SspOut& o, cudaStream_t st, int n
 template <int TPI>
 cudaError_t launch_tpi(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, bool smem_tier) {
   if (!smem_tier) return launch_one<256, false, false, false>(P, o, st, num_sms);
+  if (P.tile16s) {  // the 16-bit shared-memory tiles
+    if (P.hbits == 0) return launch_one<TPI, true, false, false, true>(P, o, st, num_sms);
+    cudaError_t e = launch_one<TPI, true, true, false, true>(P, o, st, num_sms);
+    if (e != cudaSuccess) return e;
+    return launch_one<TPI, true, false, true, true>(P, o, st, num_sms);
+  }
   if (P.hbits == 0) return launch_one<TPI, true, false, false>(P, o, st, num_sms);
   cudaError_t e = launch_one<TPI, true, true, false>(P, o, st, num_sms);
   if (e != cudaSuccess) return e;
@@ -644,7 +678,8 @@ cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int n
   // that fit in an SM's shared memory would leave it with fewer than 512 threads (large tiles:
   // churn 8 x 64 runs one 130 KB team per SM, llama 16 x 32 three 70 KB teams)
   int tpi = P.n <= 32 ? 32 : P.n <= 64 ? 64 : P.n <= 128 ? 128 : 256;
-  const long long teams_per_sm = std::max<long long>(1, (long long)(227 * 1024) / (long long)ssp_layout(P, true, 4).total);
+  const long long teams_per_sm =
+      std::max<long long>(1, (long long)(227 * 1024) / (long long)ssp_layout(P, true, 4, P.tile16s ? 2 : 4).total);
   while (tpi < 512 && teams_per_sm * tpi < 512) tpi *= 2;
   if (const char* f = getenv("GWTF_SSP_TPI")) tpi = atoi(f);  // testing override
   if (tpi <= 32) return launch_tpi<32>(P, o, st, num_sms, true);
