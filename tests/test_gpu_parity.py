@@ -483,3 +483,33 @@ def test_key_overflow_redo_queue(name):
         assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
         assert np.array_equal(nf[b], r.node_flow) and np.array_equal(af[b], r.arc_flow), b
         assert np.array_equal(sf[b], r.src_flow) and np.array_equal(kf[b], r.snk_flow), b
+
+
+@pytest.mark.parametrize("drop", [False, True], ids=["recost", "recost+drop"])
+def test_smem_tile16_edge_updates(drop):
+    """The shared-memory tier's 16-bit tile copy under edge updates: re-costed links are written into
+    the copy (it stays in use), a dropped link or a cost >= 65535 retires it (int32 tiles); either way
+    the solve equals the oracle's on the updated graph, full assignment."""
+    cfg = gen.CONFIGS["llama"]
+    B = 6
+    fl, *_ = _gpu_flow(cfg, 0, B)
+    bt, src, snk, link = harness.host_inputs(cfg, 0, B)
+    rng = np.random.default_rng(5)
+    upd = {}  # one update per arc (the updates of one call apply in parallel)
+    for b in range(B):
+        for _ in range(40):
+            s, v, u = int(rng.integers(0, cfg.S - 1)), int(rng.integers(0, cfg.n)), int(rng.integers(0, cfg.n))
+            upd[(b, s, v, u)] = int(rng.integers(1, 20000))
+    if drop:
+        upd[(1, 3, 5, 7)] = gen.ABSENT
+        upd[(4, 0, 0, 0)] = 70000
+    upd = np.array([(*k, c) for k, c in upd.items()], np.int32)
+    fl.apply_churn(None, torch.from_numpy(upd).cuda())
+    for b, s, v, u, c in upd:
+        link[b, s, v, u] = c
+    sol = fl.solve_batch()
+    nf, sf, kf, af = [x.cpu().numpy() for x in fl.get_assignment()]
+    for b in range(B):
+        r = _oracle_ssp(cfg, bt, src, snk, link, b)
+        assert (int(sol.flow_value[b]), int(sol.total_cost[b]), int(sol.augmentations[b])) == (r.F, r.cost, r.A), b
+        assert np.array_equal(af[b], r.arc_flow) and np.array_equal(nf[b], r.node_flow), b
