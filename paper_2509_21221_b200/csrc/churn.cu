@@ -41,8 +41,8 @@ __global__ void pack_tile16_kernel(const Problem P) {
 }
 
 // 16-bit copy of the padded tiles for the shared-memory tier (half the shared memory per instance:
-// more instances resident per SM); valid only when every arc within n is present with a cost <
-// 65535 (bit 0 of bad otherwise); padding columns 0 (their keys are INF)
+// more instances resident per SM): absent links 0xFFFF, padding columns 0 (their keys are INF); valid
+// only when every finite cost is < 65535 (bit 0 of bad otherwise)
 __global__ void pack_tile16s_kernel(const Problem P, int32_t* bad) {
   const size_t per = (size_t)(P.S - 1) * P.n * P.ld;
   const size_t total = (size_t)P.B * per;
@@ -53,7 +53,8 @@ __global__ void pack_tile16s_kernel(const Problem P, int32_t* bad) {
     const int32_t v = P.tile[t];
     uint16_t o = 0;
     if (c < P.n) {
-      if (v == kAbsent || v >= 65535) fail = 1;
+      if (v == kAbsent) o = 0xFFFFu;
+      else if (v >= 65535) fail = 1;
       else o = (uint16_t)v;
     }
     P.tile16s[b * (size_t)P.tile16s_stride + r] = o;
@@ -127,9 +128,9 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
         P.tile8[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld8 + w] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
         P.tile8t[(((size_t)b * (P.S - 1) + s) * P.n + w) * P.ld8 + v] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
       }
-      if (P.tile16s) {  // the shared-memory tier's 16-bit copy: an absent link or a cost >= 65535 retires it (bit 16)
-        if (c == kAbsent || c >= 65535) atomicOr(bad, 16);
-        else P.tile16s[(size_t)b * P.tile16s_stride + ((size_t)s * P.n + v) * P.ld + w] = (uint16_t)c;
+      if (P.tile16s) {  // the shared-memory tier's 16-bit copy (absent: 0xFFFF); a cost >= 65535 retires it (bit 16)
+        if (c != kAbsent && c >= 65535) atomicOr(bad, 16);
+        else P.tile16s[(size_t)b * P.tile16s_stride + ((size_t)s * P.n + v) * P.ld + w] = c == kAbsent ? (uint16_t)0xFFFFu : (uint16_t)c;
       }
       if (P.tile16) {  // the cluster tier's 16-bit copy; a finite cost >= t16code retires it (bit 2)
         if (c != kAbsent && c >= P.t16code) atomicOr(bad, 2);

@@ -479,8 +479,8 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
       if (bad8) P.tile8 = nullptr;  // an absent link: stream the 16-bit copy
     }
   }
-  // the shared-memory tier's 16-bit tile copy (half the shared memory per instance) when every arc
-  // is present with a cost < 65535
+  // the shared-memory tier's 16-bit tile copy (half the shared memory per instance) when every
+  // finite cost is < 65535
   if (nb && maxc < 65535 && ssp_smem_bytes(P) <= 227 * 1024 && !getenv("GWTF_NO_TILE16S")) {
     P.tile16s_stride = (int64_t)(((size_t)nb * n * P.ld * 2 + 15) / 16 * 16 / 2);
     if ((s = alloc(h, &P.tile16s, B * (size_t)P.tile16s_stride, true)) != GWTF_OK) return bail(s);
@@ -489,7 +489,7 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     CK(h, launch_pack_tile16s(P, h->bad_flag, h->stream));
     CK(h, cudaMemcpyAsync(&bad16, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
-    if (bad16) P.tile16s = nullptr;  // an absent link or a large cost: the int32 tiles
+    if (bad16) P.tile16s = nullptr;  // a cost >= 65535: the int32 tiles
   }
   {  // counters[6]: bound on the largest finite arc weight (raised by apply_churn's edge updates)
     const int32_t mw = (int32_t)maxc;
@@ -633,7 +633,7 @@ gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const
     CK(h, cudaMemcpyAsync(&bad, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     if (bad & 2) h->P.tile16 = nullptr;  // a cost no longer fits 16 bits: stream the int32 tiles
-    if (bad & 16) h->P.tile16s = nullptr;  // an absent link or a cost >= 65535: int32 tiles in shared memory
+    if (bad & 16) h->P.tile16s = nullptr;  // a cost >= 65535: int32 tiles in shared memory
     if (bad & (2 | 8)) h->P.tile8 = nullptr;  // an absent link or a cost >= 255: no 8-bit stream
     if (bad & 1) return fail(GWTF_E_INVALID, "edge update out of range (valid updates were applied)");
     if (bad & 4) return fail(GWTF_E_OVERFLOW, "edge update cost breaks the key bounds (rejected; valid updates were applied)");

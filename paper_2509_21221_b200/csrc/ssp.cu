@@ -125,8 +125,8 @@ __host__ __device__ inline SspLayout ssp_layout(const Problem& P, bool with_tile
 // node ids of the trace: layer << 16 | position
 __device__ __forceinline__ int nid(int layer, int pos) { return (layer << 16) | pos; }
 
-// k16: the instance's tiles are staged from the 16-bit copy (Problem::tile16s: every arc present,
-// costs < 65535) and widened on use -- half the shared memory, so more instances per SM
+// k16: the instance's tiles are staged from the 16-bit copy (Problem::tile16s: costs < 65535, absent
+// 0xFFFF) and widened on use -- half the shared memory, so more instances per SM
 template <int TPI, bool kSmem, bool k32, bool kRedo, bool k16>
 __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TPI : 6) ssp_kernel(const Problem P, const SspOut o, const size_t ws_bytes) {
   using K = typename KT<k32>::K;
@@ -209,14 +209,15 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
           bulk_g2s((uint8_t*)(base + L.tile) + off, gsrc + off, tile_bytes - off < 32768u ? tile_bytes - off : 32768u, mbar);
       }
     }
-    // weight of tile entry idx in the key arithmetic's form (pre-shifted for 32-bit keys)
+    // weight of a 16-bit tile entry in the key arithmetic's form: pre-shifted (C << H) + 1 for
+    // 32-bit keys, the raw cost for 64-bit keys, absent (0xFFFF) -> the absent code of each
+    auto w16 = [&](uint32_t c) -> int32_t {
+      if constexpr (k32) return c == 0xFFFFu ? (int32_t)kInf32 : (int32_t)((c << H) + 1u);
+      else return c == 0xFFFFu ? kAbsent : (int32_t)c;
+    };
     auto wgt = [&](size_t idx) -> int32_t {
-      if constexpr (k16) {
-        const uint32_t c = tile16[idx];
-        return k32 ? (int32_t)((c << H) + 1u) : (int32_t)c;
-      } else {
-        return tile[idx];
-      }
+      if constexpr (k16) return w16(tile16[idx]);
+      else return tile[idx];
     };
     const int64_t M = P.supply[inst];
     for (int k = T.tid; k < Sn; k += TPI) {
@@ -275,17 +276,16 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
             const int v = vb + gi;
             K acc = INF;
             if (v < n) {
-              if constexpr (k16) {  // 4 weights per 8-byte load, widened (no absent arc in this copy)
+              if constexpr (k16) {  // 4 weights per 8-byte load, widened
                 const uint2* row = (const uint2*)(tile16 + ((size_t)s * n + v) * ld);
                 for (int c = li; c < chunks; c += G) {
                   const uint2 w = row[c];
                   K kk[4];
                   load_keys4<k32>(ko + 4 * c, kk);
-                  const uint32_t c0 = w.x & 0xFFFFu, c1 = w.x >> 16, c2 = w.y & 0xFFFFu, c3 = w.y >> 16;
-                  acc = KT<k32>::relax(acc, kk[0], k32 ? (int32_t)((c0 << H) + 1u) : (int32_t)c0, one);
-                  acc = KT<k32>::relax(acc, kk[1], k32 ? (int32_t)((c1 << H) + 1u) : (int32_t)c1, one);
-                  acc = KT<k32>::relax(acc, kk[2], k32 ? (int32_t)((c2 << H) + 1u) : (int32_t)c2, one);
-                  acc = KT<k32>::relax(acc, kk[3], k32 ? (int32_t)((c3 << H) + 1u) : (int32_t)c3, one);
+                  acc = KT<k32>::relax(acc, kk[0], w16(w.x & 0xFFFFu), one);
+                  acc = KT<k32>::relax(acc, kk[1], w16(w.x >> 16), one);
+                  acc = KT<k32>::relax(acc, kk[2], w16(w.y & 0xFFFFu), one);
+                  acc = KT<k32>::relax(acc, kk[3], w16(w.y >> 16), one);
                 }
               } else {
                 const int4* row = (const int4*)(Ts + (size_t)v * ld);

@@ -488,7 +488,7 @@ def test_key_overflow_redo_queue(name):
 @pytest.mark.parametrize("drop", [False, True], ids=["recost", "recost+drop"])
 def test_smem_tile16_edge_updates(drop):
     """The shared-memory tier's 16-bit tile copy under edge updates: re-costed links are written into
-    the copy (it stays in use), a dropped link or a cost >= 65535 retires it (int32 tiles); either way
+    the copy (it stays in use, a dropped link as 0xFFFF), a cost >= 65535 retires it (int32 tiles); either way
     the solve equals the oracle's on the updated graph, full assignment."""
     cfg = gen.CONFIGS["llama"]
     B = 6
