@@ -650,8 +650,9 @@ __global__ void __launch_bounds__(kThreads) warm_kernel(const Problem P, int32_t
 // A, B as warm_kernel; an instance that does not fit (or whose kept flow has a negative cycle) is
 // left to the next kernel with status 7.
 constexpr int64_t kDInf = INT64_MAX / 4;
-struct WsLayout { size_t dist, pi, pred, imb, g, srcf, snkf, arcf, red, total; };
-__host__ __device__ inline WsLayout ws_layout(int S, int n) {
+struct WsLayout { size_t dist, pi, pred, imb, g, srcf, snkf, arcf, red, t16, total; };
+// t16_bytes: the instance's 16-bit tile copy staged in shared memory (0: link costs read from L2)
+__host__ __device__ inline WsLayout ws_layout(int S, int n, size_t t16_bytes = 0) {
   WsLayout L;
   const size_t N = 2 + 2 * (size_t)S * n, Sn = (size_t)S * n, A = (size_t)(S > 1 ? S - 1 : 0) * n * n;
   size_t o = 0;
@@ -665,17 +666,22 @@ __host__ __device__ inline WsLayout ws_layout(int S, int n) {
   L.snkf = o; o += al((size_t)n * 4);
   L.arcf = o; o += al(A * 2);
   L.red = o; o += 64;
+  L.t16 = o; o += al(t16_bytes);
   L.total = o;
   return L;
 }
 
-__global__ void __launch_bounds__(kThreads) warm_smem_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
+__global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
                                                              int32_t* arc_all, int32_t* snk_f_all, int64_t* F_out,
-                                                             int64_t* cost_out, int64_t* stats_out, int32_t* status_out) {
+                                                             int64_t* cost_out, int64_t* stats_out, int32_t* status_out,
+                                                             size_t t16_bytes) {
   extern __shared__ __align__(16) uint8_t wsm[];
   const int S = P.S, n = P.n, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = kThreads / 32;
   const int N = 2 + 2 * S * n, Sn = S * n;
-  const WsLayout L = ws_layout(S, n);
+  // the 16-bit tiles in shared memory when the launch reserved room for them
+  const bool t16 = P.tile16s != nullptr && t16_bytes > 0;
+  const WsLayout L = ws_layout(S, n, t16 ? t16_bytes : 0);
+  const uint16_t* tile16 = (const uint16_t*)(wsm + L.t16);
   int64_t* dist = (int64_t*)(wsm + L.dist);
   int64_t* pi = (int64_t*)(wsm + L.pi);
   int32_t* pred = (int32_t*)(wsm + L.pred);
@@ -701,10 +707,21 @@ __global__ void __launch_bounds__(kThreads) warm_smem_kernel(const Problem P, in
     int32_t* aG = arc_all + (size_t)b * (S - 1) * n * n;
     const int64_t M = P.supply[b];
     auto capE = [&](int k) -> int32_t { return alive[k] ? cap[k] : 0; };
-    auto C = [&](int s, int u, int v) -> int32_t { return __ldg(&tile[((size_t)s * n + v) * P.ld + u]); };
+    auto C = [&](int s, int u, int v) -> int32_t {
+      if (t16) {
+        const uint32_t c = tile16[((size_t)s * n + v) * P.ld + u];
+        return c == 0xFFFFu ? kAbsent : (int32_t)c;
+      }
+      return __ldg(&tile[((size_t)s * n + v) * P.ld + u]);
+    };
     // ---- load, cut (units the churned graph cannot carry), BIG ----
     if (tid == 0) { red[0] = 0; red[1] = 0; red[2] = 0; ired[0] = 0; ired[2] = 0; ired[3] = 0; }
     for (int k = tid; k < N; k += kThreads) imb[k] = 0;
+    if (t16) {  // the instance's 16-bit link costs into shared memory (every pass reads them)
+      const uint4* s4 = (const uint4*)(P.tile16s + (size_t)b * P.tile16s_stride);
+      uint4* d4 = (uint4*)(wsm + L.t16);
+      for (size_t k = tid; k < t16_bytes / 16; k += kThreads) d4[k] = s4[k];
+    }
     __syncthreads();
     long long cut = 0, F0 = 0;
     int32_t maxc = 0, bigf = 0;
@@ -1108,13 +1125,17 @@ cudaError_t launch_warm(const Problem& P, int32_t* src_f, int32_t* g, int32_t* a
   int32_t* imb = (int32_t*)(pi + (size_t)grid * N);
   int32_t* stamp = imb + (size_t)grid * N;
   if (smem_repair) {
+    // the 16-bit link costs join the workspace when two CTAs per SM still fit (113 KB each)
+    const size_t t16b = P.tile16s ? (size_t)P.tile16s_stride * 2 : 0;
+    const size_t t16_bytes = (t16b && ws_layout(P.S, P.n, t16b).total <= 113 * 1024) ? t16b : 0;
+    const size_t wsm = ws_layout(P.S, P.n, t16_bytes).total;
     cudaError_t e = cudaFuncSetAttribute(warm_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warm_smem_kernel, kThreads, wsm);
     if (e != cudaSuccess) return e;
     const int g2 = (int)std::min<int64_t>(P.B, (int64_t)std::max(per_sm, 1) * 148);
-    warm_smem_kernel<<<g2, kThreads, wsm, st>>>(P, src_f, g, arc, snk_f, F, cost, stats, status);
+    warm_smem_kernel<<<g2, kThreads, wsm, st>>>(P, src_f, g, arc, snk_f, F, cost, stats, status, t16_bytes);
   } else {
     warm_kernel<<<grid, kThreads, 0, st>>>(P, src_f, g, arc, snk_f, labv, pi, imb, F, cost, stats, status);
   }
