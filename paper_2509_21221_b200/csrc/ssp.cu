@@ -675,12 +675,15 @@ cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int n
     return launch_tpi<256>(P, o, st, num_sms, false);
   }
   // team size: about one thread per destination row to start with, then doubled while the teams
-  // that fit in an SM's shared memory would leave it with fewer than 512 threads (large tiles:
-  // churn 8 x 64 runs one 130 KB team per SM, llama 16 x 32 three 70 KB teams)
+  // that fit in an SM's shared memory would leave it with fewer than 512 threads
   int tpi = P.n <= 32 ? 32 : P.n <= 64 ? 64 : P.n <= 128 ? 128 : 256;
   const long long teams_per_sm =
       std::max<long long>(1, (long long)(227 * 1024) / (long long)ssp_layout(P, true, 4, P.tile16s ? 2 : 4).total);
   while (tpi < 512 && teams_per_sm * tpi < 512) tpi *= 2;
+  // multi-warp teams (named barriers) keep doubling up to 1,024 threads per SM: measured with the
+  // 16-bit tiles, llama 64.4 -> 56.5 ms at 256 threads per team, churn 704 -> 574 ms at 512; a
+  // single-warp team (gpt: 22 per SM) stays one warp (64 threads measured 2x slower)
+  while (tpi >= 64 && tpi < 512 && teams_per_sm * tpi < 1024) tpi *= 2;
   if (const char* f = getenv("GWTF_SSP_TPI")) tpi = atoi(f);  // testing override
   if (tpi <= 32) return launch_tpi<32>(P, o, st, num_sms, true);
   if (tpi <= 64) return launch_tpi<64>(P, o, st, num_sms, true);
