@@ -671,6 +671,17 @@ __host__ __device__ inline WsLayout ws_layout(int S, int n, size_t t16_bytes = 0
   return L;
 }
 
+// a row minimum's candidate and source packed into one key: (cand + 2^44) << 19 | source.  The
+// shared-memory repair's labels stay within |d| < 2^44 (path costs < 2^42 by the create bounds, plus two
+// potentials) and its node ids below 2^19 (the workspace fits 100 KB), so the packed minimum is the lowest
+// candidate and, among equal ones, the lowest source
+constexpr uint64_t kPackMask = (1ull << 19) - 1;
+__device__ __forceinline__ uint64_t umin64w(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t pack_cand(int64_t cand, int src) {
+  return ((uint64_t)(cand + (1ll << 44)) << 19) | (uint64_t)src;
+}
+__device__ __forceinline__ int64_t unpack_cand(uint64_t k) { return (int64_t)(k >> 19) - (1ll << 44); }
+
 __global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P, int32_t* src_f_all, int32_t* g_all,
                                                              int32_t* arc_all, int32_t* snk_f_all, int64_t* F_out,
                                                              int64_t* cost_out, int64_t* stats_out, int32_t* status_out,
@@ -692,6 +703,8 @@ __global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P,
   int16_t* arcf = (int16_t*)(wsm + L.arcf);
   unsigned long long* red = (unsigned long long*)(wsm + L.red);
   int* ired = (int*)(red + 4);
+  __shared__ unsigned long long dm[4];
+  __shared__ unsigned int dfl[2];
   auto IN = [&](int s, int i) { return 2 + 2 * (s * n + i); };
   for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
     if (status_out[b] == kDeferred) continue;  // triage: left to the cold solve
@@ -767,17 +780,39 @@ __global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P,
     // ---- one layered Bellman-Ford pass ----
     // mode 0: potentials (real costs, rejoined relays' node arcs and the bypass left out);
     // mode 1: reduced costs, bypass forward allowed (phase A); mode 2: reduced costs, no bypass (B)
-    auto relax = [&](int to, int64_t cand, int from, int& ch) {
-      if (cand < dist[to]) { dist[to] = cand; pred[to] = from; ch = 1; }
+    // layers whose labels changed (bit s of dm[0] / dm[1]: in_s / out_s; dfl bit 0 / 1: s* / t*) in
+    // this pass ([0], [1], dfl[0]) and the previous one ([2], [3], dfl[1]): a relaxation whose source
+    // layer changed in neither since it last ran cannot lower anything and is skipped (S <= 64)
+    auto mark = [&](int to) {
+      if (to < 2) atomicOr(&dfl[0], 1u << to);
+      else atomicOr(&dm[to & 1], 1ull << (((to - 2) >> 1) / n));
     };
+    auto relax = [&](int to, int64_t cand, int from, int& ch) {
+      if (cand < dist[to]) { dist[to] = cand; pred[to] = from; ch = 1; mark(to); }
+    };
+    const bool track = S <= 64;
+    auto din = [&](int s) { return !track || (((dm[0] | dm[2]) >> s) & 1ull); };
+    auto dout = [&](int s) { return !track || (((dm[1] | dm[3]) >> s) & 1ull); };
+    auto dnode = [&](int x) { return !track || ((dfl[0] | dfl[1]) >> x) & 1u; };  // 0: s*, 1: t*
     auto w = [&](int mode, int from, int to, int64_t c) -> int64_t { return mode ? c + pi[from] - pi[to] : c; };
-    auto pass = [&](int mode) -> bool {
+    auto pass = [&](int mode, bool first) -> bool {
       int ch = 0;
+      if (tid == 0) {  // this pass's change sets start empty; the previous pass's become "prev"
+        dm[2] = first ? ~0ull : dm[0];
+        dm[3] = first ? ~0ull : dm[1];
+        dfl[1] = first ? 3u : dfl[0];
+        dm[0] = 0;
+        dm[1] = 0;
+        dfl[0] = 0;
+      }
+      __syncthreads();
       // forward: s* -> in_0
-      for (int i = tid; i < n; i += kThreads)
-        if (dist[0] < kDInf && src[i] != kAbsent) relax(IN(0, i), dist[0] + w(mode, 0, IN(0, i), src[i]), 0, ch);
+      if (dnode(0))
+        for (int i = tid; i < n; i += kThreads)
+          if (dist[0] < kDInf && src[i] != kAbsent) relax(IN(0, i), dist[0] + w(mode, 0, IN(0, i), src[i]), 0, ch);
       __syncthreads();
       for (int s = 0; s < S; ++s) {
+        if (din(s))
         for (int i = tid; i < n; i += kThreads) {  // in -> out (node arc, residual cap - g)
           const int k = s * n + i, a = IN(s, i);
           if (g[k] >= capE(k) || dist[a] >= kDInf) continue;
@@ -785,70 +820,61 @@ __global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P,
           relax(a + 1, dist[a] + w(mode, a, a + 1, 0), a, ch);
         }
         __syncthreads();
-        if (s + 1 < S) {  // out_s -> in_{s+1}: one row minimum per destination (warp per row)
+        if (s + 1 < S && dout(s)) {  // out_s -> in_{s+1}: one row minimum per destination (warp per row)
           for (int v = wid; v < n; v += nw) {
             const int to = IN(s + 1, v);
-            int64_t best = kDInf;
-            int bu = -1;
+            uint64_t bk = ~0ull;  // packed (candidate, source): the lowest candidate, then the lowest source
             for (int u = lane; u < n; u += 32) {
               const int fr = IN(s, u) + 1;
               const int32_t c = C(s, u, v);
               if (c == kAbsent || dist[fr] >= kDInf) continue;
-              const int64_t cand = dist[fr] + w(mode, fr, to, c);
-              if (cand < best) { best = cand; bu = fr; }
+              bk = umin64w(bk, pack_cand(dist[fr] + w(mode, fr, to, c), fr));
             }
-            for (int off = 16; off > 0; off >>= 1) {
-              const int64_t ob = __shfl_xor_sync(0xffffffffu, best, off);
-              const int ou = __shfl_xor_sync(0xffffffffu, bu, off);
-              if (ob < best || (ob == best && ou < bu && ou >= 0)) { best = ob; bu = ou; }
-            }
-            if (lane == 0 && bu >= 0) relax(to, best, bu, ch);
+            for (int off = 16; off > 0; off >>= 1) bk = umin64w(bk, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)bk, off));
+            if (lane == 0 && bk != ~0ull) relax(to, unpack_cand(bk), (int)(bk & kPackMask), ch);
           }
           __syncthreads();
         }
       }
       if (tid == 0) {  // out_{S-1} -> t*, then the bypass s* -> t*
+        if (dout(S - 1))
         for (int i = 0; i < n; ++i) {
           const int fr = IN(S - 1, i) + 1;
           if (snk[i] != kAbsent && dist[fr] < kDInf) relax(1, dist[fr] + w(mode, fr, 1, snk[i]), fr, ch);
         }
-        if (mode == 1 && byp < M && dist[0] < kDInf) relax(1, dist[0] + w(mode, 0, 1, big), 0, ch);
+        if (mode == 1 && byp < M && dist[0] < kDInf && dnode(0)) relax(1, dist[0] + w(mode, 0, 1, big), 0, ch);
       }
       __syncthreads();
       // backward: t* -> out_{S-1} (snk flow), then per stage out -> in (node flow) and in_{s} -> out_{s-1}
+      if (dnode(1))
       for (int i = tid; i < n; i += kThreads) {
         const int to = IN(S - 1, i) + 1;
         if (snkf[i] > 0 && dist[1] < kDInf) relax(to, dist[1] + w(mode, 1, to, -(int64_t)snk[i]), 1, ch);
       }
       __syncthreads();
       for (int s = S - 1; s >= 0; --s) {
+        if (dout(s))
         for (int i = tid; i < n; i += kThreads) {  // out -> in (reverse node arc, residual g)
           const int k = s * n + i, a = IN(s, i);
           if (g[k] > 0 && dist[a + 1] < kDInf) relax(a, dist[a + 1] + w(mode, a + 1, a, 0), a + 1, ch);
         }
         __syncthreads();
-        if (s > 0) {  // in_s -> out_{s-1}: reverse link arcs carrying flow (warp per source u)
+        if (s > 0 && din(s)) {  // in_s -> out_{s-1}: reverse link arcs carrying flow (warp per source u)
           for (int u = wid; u < n; u += nw) {
             const int to = IN(s - 1, u) + 1;
-            int64_t best = kDInf;
-            int bv = -1;
+            uint64_t bk = ~0ull;
             for (int v = lane; v < n; v += 32) {
               const int fr = IN(s, v);
               if (arcf[((size_t)(s - 1) * n + v) * n + u] <= 0 || dist[fr] >= kDInf) continue;
-              const int64_t cand = dist[fr] + w(mode, fr, to, -(int64_t)C(s - 1, u, v));
-              if (cand < best) { best = cand; bv = fr; }
+              bk = umin64w(bk, pack_cand(dist[fr] + w(mode, fr, to, -(int64_t)C(s - 1, u, v)), fr));
             }
-            for (int off = 16; off > 0; off >>= 1) {
-              const int64_t ob = __shfl_xor_sync(0xffffffffu, best, off);
-              const int ov = __shfl_xor_sync(0xffffffffu, bv, off);
-              if (ob < best || (ob == best && ov < bv && ov >= 0)) { best = ob; bv = ov; }
-            }
-            if (lane == 0 && bv >= 0) relax(to, best, bv, ch);
+            for (int off = 16; off > 0; off >>= 1) bk = umin64w(bk, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)bk, off));
+            if (lane == 0 && bk != ~0ull) relax(to, unpack_cand(bk), (int)(bk & kPackMask), ch);
           }
           __syncthreads();
         }
       }
-      if (tid == 0)  // in_0 -> s* (reverse src arcs)
+      if (tid == 0 && din(0))  // in_0 -> s* (reverse src arcs)
         for (int i = 0; i < n; ++i)
           if (srcf[i] > 0 && dist[IN(0, i)] < kDInf) relax(0, dist[IN(0, i)] + w(mode, IN(0, i), 0, -(int64_t)src[i]), IN(0, i), ch);
       return __syncthreads_or(ch) != 0;
@@ -858,7 +884,10 @@ __global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P,
     __syncthreads();
     int passes = 0;
     bool conv = true;
-    while (pass(0)) if (++passes > N + 2) { conv = false; break; }
+    for (bool first = true; pass(0, first); first = false) if (++passes > N + 2) { conv = false; break; }
+#ifdef GWTF_DEV_FLAGS
+    if ((P.debug & 16) && tid == 0) { atomicAdd(&P.stats[1300], (unsigned long long)passes + 1); atomicAdd(&P.stats[1303], 1ull); }
+#endif
     if (!conv) {  // a negative cycle on the kept flow (a lowered cost): the Klein fallback, flows untouched
       if (tid == 0) status_out[b] = 71;
       __syncthreads();
@@ -899,7 +928,10 @@ __global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P,
         continue;
       }
       int sp = 0;
-      while (pass(phaseB ? 2 : 1)) if (++sp > N + 2) { bad = true; break; }
+      for (bool first = true; pass(phaseB ? 2 : 1, first); first = false) if (++sp > N + 2) { bad = true; break; }
+#ifdef GWTF_DEV_FLAGS
+      if ((P.debug & 16) && tid == 0) { atomicAdd(&P.stats[1301], (unsigned long long)sp + 1); atomicAdd(&P.stats[1302], 1ull); }
+#endif
       if (bad) { if (tid == 0) ired[3] = 74; break; }
       if (tid == 0) red[3] = ~0ull;
       __syncthreads();
