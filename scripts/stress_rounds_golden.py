@@ -3,7 +3,8 @@ M = 4,096, cold start, max_rounds = 120 + 2M): rounds run, F_dec, cost_dec, dang
 state digest, every 256th per-round digest and the SHA-256 of the whole digest sequence, written
 to tests/golden/stress_rounds.json.  Calls only gen/ and oracle/ (seed 17).
 
-  python scripts/stress_rounds_golden.py [--inst 0 ...]
+  python scripts/stress_rounds_golden.py [--inst 0 ...] [--out PATH]
+  python scripts/stress_rounds_golden.py --merge PART.json ...   (parts written by parallel --out runs)
 """
 import argparse
 import hashlib
@@ -21,9 +22,20 @@ import oracle  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--inst", type=int, nargs="+", default=[0])
+ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "stress_rounds.json"))
+ap.add_argument("--merge", nargs="+", default=None, help="merge part files into the golden file and exit")
 a = ap.parse_args()
 cfg = gen.CONFIGS["stress"]
-out_path = os.path.join(ROOT, "tests", "golden", "stress_rounds.json")
+out_path = a.out
+if a.merge:
+    gold = os.path.join(ROOT, "tests", "golden", "stress_rounds.json")
+    res = json.load(open(gold))
+    for part in a.merge:
+        res["instances"].update(json.load(open(part))["instances"])
+    res["instances"] = dict(sorted(res["instances"].items(), key=lambda kv: int(kv[0])))
+    with open(gold, "w") as f:
+        json.dump(res, f, indent=1)
+    sys.exit(0)
 res = json.load(open(out_path)) if os.path.exists(out_path) else {
     "source": "scripts/stress_rounds_golden.py (oracle.Rounds on gen.CONFIGS['stress'], seed 17)", "seed": 17,
     "max_rounds": cfg.max_rounds, "instances": {}}
