@@ -783,14 +783,15 @@ __global__ void __launch_bounds__(kThreads, 2) warm_smem_kernel(const Problem P,
     // layers whose labels changed (bit s of dm[0] / dm[1]: in_s / out_s; dfl bit 0 / 1: s* / t*) in
     // this pass ([0], [1], dfl[0]) and the previous one ([2], [3], dfl[1]): a relaxation whose source
     // layer changed in neither since it last ran cannot lower anything and is skipped (S <= 64)
+    const bool track = S <= 64;
     auto mark = [&](int to) {
+      if (!track) return;
       if (to < 2) atomicOr(&dfl[0], 1u << to);
       else atomicOr(&dm[to & 1], 1ull << (((to - 2) >> 1) / n));
     };
     auto relax = [&](int to, int64_t cand, int from, int& ch) {
       if (cand < dist[to]) { dist[to] = cand; pred[to] = from; ch = 1; mark(to); }
     };
-    const bool track = S <= 64;
     auto din = [&](int s) { return !track || (((dm[0] | dm[2]) >> s) & 1ull); };
     auto dout = [&](int s) { return !track || (((dm[1] | dm[3]) >> s) & 1ull); };
     auto dnode = [&](int x) { return !track || ((dfl[0] | dfl[1]) >> x) & 1u; };  // 0: s*, 1: t*
