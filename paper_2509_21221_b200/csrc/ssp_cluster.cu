@@ -55,6 +55,7 @@ struct Misc {  // per-CTA control block; the leader's copy is authoritative
   uint64_t tpart[2], red64;
   int32_t inst, A, status, pathlen;
   uint32_t votes[2];  // alternating slots: a CTA is at most one phase ahead of the slowest
+  uint32_t vin[2][16];  // vote stamps pushed by every CTA of the cluster (parity, source CTA)
   int32_t red32, pred, nrem, ucnt;
   uint32_t p2;  // 1 << H32, read back through a volatile load (see the relaxation)
 };
@@ -221,11 +222,15 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
     auto vote = [&](int ch) -> bool {
       // a thread that changed something stamps its CTA's slot with the vote id (idempotent); the
       // cluster barrier orders every stamp before the reads, so no CTA-level reduction is needed
+      // a warp that changed something pushes the stamp into its CTA's slot in every CTA (lane q to
+      // CTA q; idempotent) before the barrier, whose skew hides the remote stores; after it every
+      // CTA reads its own slots only
       ++vote_id;
-      if (ch) misc->votes[vote_id & 1] = vote_id;  // own slot, double-buffered
+      const int p = vote_id & 1;
+      if (__any_sync(0xffffffffu, ch) && lane < C) *cl.map_shared_rank(&misc->vin[p][r], lane) = vote_id;
       cl.sync();
       bool res = false;
-      for (int q = 0; q < C; ++q) res |= cl.map_shared_rank(misc, q)->votes[vote_id & 1] == vote_id;
+      for (int q = 0; q < C; ++q) res |= *(volatile uint32_t*)&misc->vin[p][q] == vote_id;
       return res;
     };
 
