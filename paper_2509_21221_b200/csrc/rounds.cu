@@ -94,6 +94,7 @@ struct Inst {
   const int32_t *tile, *src, *snk;
   const uint8_t* alive;
   uint64_t hpre;  // mix(mix(mix(seed) ^ inst) ^ round), uniform over the round
+  uint64_t hinst;  // mix(mix(seed) ^ inst), fixed per instance
 
   __device__ int st(int p) const { return (up[p] != kNone ? 2 : 0) | (down[p] != kNone ? 1 : 0); }
   __device__ int relay(int32_t p) const { return dmc.div(p); }           // slot index -> gid
@@ -111,7 +112,7 @@ struct Inst {
   __device__ void set_up_of(int32_t p, int32_t v) { if (p >= 0) up[p] = v; else snk_up[-2 - p] = v; }
   __device__ void set_down_of(int32_t p, int32_t v) { if (p >= 0) down[p] = v; else src_down[-2 - p] = v; }
   __device__ void set_round(uint64_t round) {
-    hpre = mix(mix(mix(P->seed) ^ (uint64_t)(P->inst_base + inst)) ^ round);
+    hpre = mix(hinst ^ round);
   }
   __device__ uint64_t h(int gid, int stream) const { return mix(hpre ^ ((uint64_t)gid * 4 + stream)); }
 
@@ -400,6 +401,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
     if (b >= P.B) break;
     Inst I;
     I.P = &P; I.S = S; I.n = n; I.ld = P.ld; I.MC = MC; I.Sn = Sn; I.inst = b;
+    I.hinst = mix(mix(P.seed) ^ (uint64_t)(P.inst_base + b));
     I.dn.init((uint32_t)n);
     I.dmc.init((uint32_t)(MC > 0 ? MC : 1));
     I.M = (int)P.supply[b];
