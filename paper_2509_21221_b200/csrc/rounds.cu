@@ -98,7 +98,8 @@ struct Inst {
 
   __device__ int st(int p) const { return (up[p] != kNone ? 2 : 0) | (down[p] != kNone ? 1 : 0); }
   __device__ int relay(int32_t p) const { return dmc.div(p); }           // slot index -> gid
-  __device__ int64_t c_link(int s, int u, int v) const { return cst(tile[((size_t)s * n + v) * ld + u]); }
+  // one instance's tile has (S-1) n ld < 2^31 entries (create: S <= 64, n <= 4096): 32-bit indices
+  __device__ int64_t c_link(int s, int u, int v) const { return cst(tile[(uint32_t)((s * n + v) * ld + u)]); }
   // d(a, b) between nodes; -1 = data node D.  Missing / absent = INF.
   __device__ int64_t d(int a, int b) const {
     if (a < 0) return (b >= 0 && b < n) ? cst(src[b]) : INF;
