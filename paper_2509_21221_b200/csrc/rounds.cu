@@ -701,7 +701,7 @@ __device__ __forceinline__ void rounds_body(const Problem& P, const RoundsOut& o
                 int64_t avv[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
-                  if (jv[t] >= 0) { cv[t] = col[(size_t)jv[t] * I.ld]; avv[t] = av[jv[t]]; }
+                  if (jv[t] >= 0) { cv[t] = col[(uint32_t)(jv[t] * I.ld)]; avv[t] = av[jv[t]]; }
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
                   if (jv[t] >= 0 && cv[t] != kAbsent && cv[t] + avv[t] < bc) { bc = cv[t] + avv[t]; tgw = (s0 + 1) * n + jv[t]; }
