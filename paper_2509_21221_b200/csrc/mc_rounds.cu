@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(kT) mc_rounds_kernel(const McArgs A) {
     };
     int quiet = 0, r = 0;
     uint64_t round = (uint64_t)A.round0;
+    const uint64_t hinst = mix(mix(A.seed) ^ (uint64_t)(A.inst_base + b));  // fixed per instance
     while (r < A.max_rounds) {
-      const uint64_t hpre = mix(mix(mix(A.seed) ^ (uint64_t)(A.inst_base + b)) ^ round);
+      const uint64_t hpre = mix(hinst ^ round);
       auto h = [&](int gid, int stream) -> uint64_t { return mix(hpre ^ ((uint64_t)gid * 4 + stream)); };
       if (tid == 0) red[0] = 0;
       // ---- R0a self-pairing on round-start costs ----
