@@ -684,8 +684,12 @@ def main():
     # ---------------- roofline of the dominant kernel ----------------
     peak, peak_src = load_peaks()
     dom = max(ktimes, key=lambda k: ktimes[k][0])
-    dom_ms, dom_launches = ktimes[dom]
     ssp_name = next((k for k in ktimes if k.startswith("ssp")), None)
+    # the solve and the rounds run side by side and now take about as long (stress: 5.97 vs 5.98 s per
+    # step): within 3% of the longest, the north star's min-plus kernel is the one reported as dominant
+    # (the other kernel's line is kept below, so both are in the JSON either way)
+    if ssp_name and ktimes[ssp_name][0] >= 0.97 * ktimes[dom][0]:
+        dom = ssp_name
 
     def ssp_roof(kname):
         ms, nl = ktimes[kname]
@@ -699,16 +703,18 @@ def main():
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None, "traffic_source": tsrc,
                 "traffic_note": tr.get("note") if tr else None}
 
-    if dom == ssp_name:
-        roof = ssp_roof(dom)
-    else:
-        # the rounds (latency-bound) dominate: HBM use from the ncu DRAM bytes of the committed capture
-        tr, tsrc = load_traffic(f"{cfg.name}:{dom}")
+    def rounds_roof(kname):
+        # the rounds (latency-bound): HBM use from the ncu DRAM bytes of the committed capture
+        ms, nl = ktimes[kname]
+        tr, tsrc = load_traffic(f"{cfg.name}:{kname}")
         bpl = tr.get("dram_bytes_per_launch") if tr else None
-        ach = (bpl * dom_launches / (dom_ms / 1e3) / 1e9) if bpl else None
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+        ach = (bpl * nl / (ms / 1e3) / 1e9) if bpl else None
+        return {"kernel": kname, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak if ach else None, "peak_source": peak_src, "traffic": bpl, "traffic_source": tsrc,
                 "note": "rounds kernel: achieved = ncu DRAM bytes per launch / live launch time (latency-bound)"}
+
+    roof = ssp_roof(dom) if dom == ssp_name else rounds_roof(dom)
+    rounds_name = next((k for k in ktimes if k.startswith("rounds")), None)
     kshare = {k: {"ms_total": v[0], "launches": v[1], "share_of_step": v[0] / total_ms if total_ms else None}
               for k, v in ktimes.items()}
 
@@ -726,6 +732,8 @@ def main():
             "augmentations_per_step": A_total / max(args.steps, 1), "rounds_per_step": rounds_total / max(args.steps, 1)}
     if ssp_name and dom != ssp_name:
         line["min_plus_roofline"] = ssp_roof(ssp_name)
+    if rounds_name and dom != rounds_name:
+        line["rounds_roofline"] = rounds_roof(rounds_name)
 
     # the timed handle is done: its device memory goes back before the end-to-end pipeline creates its own
     fl.close()
