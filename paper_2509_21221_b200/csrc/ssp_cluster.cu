@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
   auto rsrcf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(srcf, q) + (v - q * R); };
   auto rsnkf = [&](int v) -> int32_t* { const int q = own(v); return cl.map_shared_rank(snkf, q) + (v - q * R); };
 
+  if (tid < 32) misc->vin[tid >> 4][tid & 15] = 0u;  // vote ids start at 1 and never repeat in a launch
   if (tid == 0) {
     misc->p2 = 1u << H32;
     for (int b = 0; b < nbc; ++b) { mbar_init(&mbar[b], 1); ecnt[b] = 0; }
@@ -215,7 +216,6 @@ __global__ void __launch_bounds__(CT, 1) ssp_cluster_kernel(const Problem P, con
       if (tid == 0) { misc->F = 0; misc->cost = 0; misc->A = 0; misc->status = 0; misc->votes[0] = 0; misc->votes[1] = 0; }
       for (int k = tid; k < S - 1; k += CT) __stcg(&cnt[k], 0);
     }
-    vote_id = 0;
     cl.sync();
 
     // vote: did any CTA of the cluster change something in this phase?  (cluster barrier)
