@@ -62,6 +62,27 @@ __global__ void pack_tile16s_kernel(const Problem P, int32_t* bad) {
   if (fail) atomicOr(bad, 1);
 }
 
+// the shared-memory tier's 8-bit copy (a quarter of the shared memory of the int32 tiles): absent
+// links 0xFF, padding 0; valid only when every finite cost is < 255 (bit 0 of bad otherwise)
+__global__ void pack_tile8s_kernel(const Problem P, int32_t* bad) {
+  const size_t per = (size_t)(P.S - 1) * P.n * P.ld;
+  const size_t total = (size_t)P.B * per;
+  int fail = 0;
+  for (size_t t = gtid(); t < total; t += gstride()) {
+    const size_t b = t / per, r = t - b * per;
+    const int c = (int)(r % P.ld);
+    const int32_t v = P.tile[t];
+    uint8_t o = 0;
+    if (c < P.n) {
+      if (v == kAbsent) o = 0xFFu;
+      else if (v >= 255) fail = 1;
+      else o = (uint8_t)v;
+    }
+    P.tile8s[b * (size_t)P.tile8s_stride + r] = o;
+  }
+  if (fail) atomicOr(bad, 1);
+}
+
 // 8-bit copy of the padded tiles (the cluster tier streams a quarter of the int32 bytes): valid
 // only when every arc within n is present with a cost < 255 (bit 0 of bad otherwise); padding = 255
 __global__ void pack_tile8_kernel(const Problem P, int32_t* bad) {
@@ -127,6 +148,10 @@ __global__ void edge_update_kernel(const Problem P, const int32_t* __restrict__ 
         if (c == kAbsent || c >= 255) atomicOr(bad, 8);
         P.tile8[(((size_t)b * (P.S - 1) + s) * P.n + v) * P.ld8 + w] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
         P.tile8t[(((size_t)b * (P.S - 1) + s) * P.n + w) * P.ld8 + v] = (uint8_t)(c == kAbsent || c >= 255 ? 255 : c);
+      }
+      if (P.tile8s) {  // the shared-memory tier's 8-bit copy (absent: 0xFF); a cost >= 255 retires it (bit 32)
+        if (c != kAbsent && c >= 255) atomicOr(bad, 32);
+        else P.tile8s[(size_t)b * P.tile8s_stride + ((size_t)s * P.n + v) * P.ld + w] = c == kAbsent ? (uint8_t)0xFFu : (uint8_t)c;
       }
       if (P.tile16s) {  // the shared-memory tier's 16-bit copy (absent: 0xFFFF); a cost >= 65535 retires it (bit 16)
         if (c != kAbsent && c >= 65535) atomicOr(bad, 16);
@@ -292,6 +317,12 @@ __global__ void eq1_kernel(int32_t B, int32_t S, int32_t n, int32_t L, const int
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st) {
   const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld;
   if (total) pad_tiles_kernel<<<grid_for(total), 256, 0, st>>>(P, link);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_tile8s(const Problem& P, int32_t* bad, cudaStream_t st) {
+  const size_t total = (size_t)P.B * (P.S - 1) * P.n * P.ld;
+  if (total && P.tile8s) pack_tile8s_kernel<<<grid_for(total), 256, 0, st>>>(P, bad);
   return cudaGetLastError();
 }
 

@@ -491,6 +491,17 @@ gwtf_status gwtf_flow_create(const gwtf_problem_desc* d, gwtf_flow_t* out) {
     CK(h, cudaStreamSynchronize(h->stream));
     if (bad16) P.tile16s = nullptr;  // a cost >= 65535: the int32 tiles
   }
+  // and the 8-bit copy (a quarter of the shared memory) when every finite cost is < 255
+  if (P.tile16s && maxc < 255 && !getenv("GWTF_NO_TILE8S")) {
+    P.tile8s_stride = (int64_t)(((size_t)nb * n * P.ld + 15) / 16 * 16);
+    if ((s = alloc(h, &P.tile8s, B * (size_t)P.tile8s_stride, true)) != GWTF_OK) return bail(s);
+    int32_t bad8s = 0;
+    CK(h, cudaMemsetAsync(h->bad_flag, 0, 4, h->stream));
+    CK(h, launch_pack_tile8s(P, h->bad_flag, h->stream));
+    CK(h, cudaMemcpyAsync(&bad8s, h->bad_flag, 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (bad8s) P.tile8s = nullptr;
+  }
   {  // counters[6]: bound on the largest finite arc weight (raised by apply_churn's edge updates)
     const int32_t mw = (int32_t)maxc;
     CK(h, cudaMemcpyAsync(P.counters + 6, &mw, 4, cudaMemcpyHostToDevice, h->stream));
@@ -634,6 +645,7 @@ gwtf_status gwtf_flow_apply_churn(gwtf_flow_t h, const uint8_t* alive_new, const
     CK(h, cudaStreamSynchronize(h->stream));
     if (bad & 2) h->P.tile16 = nullptr;  // a cost no longer fits 16 bits: stream the int32 tiles
     if (bad & 16) h->P.tile16s = nullptr;  // a cost >= 65535: int32 tiles in shared memory
+    if (bad & (16 | 32)) h->P.tile8s = nullptr;  // a cost >= 255: no 8-bit tiles in shared memory
     if (bad & (2 | 8)) h->P.tile8 = nullptr;  // an absent link or a cost >= 255: no 8-bit stream
     if (bad & 1) return fail(GWTF_E_INVALID, "edge update out of range (valid updates were applied)");
     if (bad & 4) return fail(GWTF_E_OVERFLOW, "edge update cost breaks the key bounds (rejected; valid updates were applied)");

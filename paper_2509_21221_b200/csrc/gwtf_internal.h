@@ -29,6 +29,9 @@ struct Problem {
   uint16_t* tile16s;           // shared-memory tier: [B][stride] 16-bit copy of the padded tiles (padding 0) when
                                // every arc is present with a cost < 65535; nullptr otherwise (or once retired)
   int64_t tile16s_stride;      // elements per instance (bytes a multiple of 16: one TMA bulk copy)
+  uint8_t* tile8s;             // shared-memory tier: [B][stride] 8-bit copy (absent 0xFF, padding 0) when every
+                               // finite cost is < 255; nullptr otherwise (or once retired)
+  int64_t tile8s_stride;       // bytes per instance (a multiple of 16)
   int32_t* src;                // [B][n]
   int32_t* snk;                // [B][n]
   int32_t* cap;                // [B][S][n]
@@ -112,6 +115,7 @@ cudaError_t launch_churn(const Problem& P, const uint8_t* alive_new, const int32
 cudaError_t launch_pad_tiles(const Problem& P, const int32_t* link, cudaStream_t st);
 cudaError_t launch_pack_tile16(const Problem& P, cudaStream_t st);
 cudaError_t launch_pack_tile16s(const Problem& P, int32_t* bad, cudaStream_t st);
+cudaError_t launch_pack_tile8s(const Problem& P, int32_t* bad, cudaStream_t st);
 cudaError_t launch_pack_tile8(const Problem& P, int32_t* bad, cudaStream_t st);
 cudaError_t launch_dense_arcs(const Problem& P, int32_t* dense, cudaStream_t st);
 cudaError_t launch_residual_caps(const Problem& P, int32_t* out, cudaStream_t st);

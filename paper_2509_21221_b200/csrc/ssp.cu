@@ -125,9 +125,10 @@ __host__ __device__ inline SspLayout ssp_layout(const Problem& P, bool with_tile
 // node ids of the trace: layer << 16 | position
 __device__ __forceinline__ int nid(int layer, int pos) { return (layer << 16) | pos; }
 
-// k16: the instance's tiles are staged from the 16-bit copy (Problem::tile16s: costs < 65535, absent
-// 0xFFFF) and widened on use -- half the shared memory, so more instances per SM
-template <int TPI, bool kSmem, bool k32, bool kRedo, bool k16>
+// kTB = 2 / 1: the instance's tiles are staged from the 16-bit / 8-bit copy (Problem::tile16s: costs
+// < 65535, absent 0xFFFF; Problem::tile8s: costs < 255, absent 0xFF) and widened on use -- a half / a
+// quarter of the shared memory, so more instances per SM; kTB = 4: the int32 tiles
+template <int TPI, bool kSmem, bool k32, bool kRedo, int kTB>
 __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TPI : 6) ssp_kernel(const Problem P, const SspOut o, const size_t ws_bytes) {
   using K = typename KT<k32>::K;
   constexpr K INF = KT<k32>::INF;
@@ -141,7 +142,8 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
   uint8_t* base;
   if constexpr (kSmem) base = smem + (size_t)T.id * ws_bytes;
   else base = P.ws + (size_t)(blockIdx.x * teams_per_cta + T.id) * ws_bytes;
-  const SspLayout L = ssp_layout(P, kSmem, sizeof(K), k16 ? 2 : 4);
+  constexpr bool k16 = kTB == 2, k8 = kTB == 1;
+  const SspLayout L = ssp_layout(P, kSmem, sizeof(K), kTB);
   uint64_t* mbar = (uint64_t*)(base + L.misc);
   int64_t* F_p = (int64_t*)(base + L.misc + 8);
   int64_t* cost_p = (int64_t*)(base + L.misc + 16);
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
   const int lane = threadIdx.x & 31;
   const int Lt = 2 * S + 1;  // layer of t*
   const size_t tile_elems = (size_t)(S - 1) * n * ld;
-  const uint32_t tile_bytes = k16 ? (uint32_t)(P.tile16s_stride * 2) : (uint32_t)(tile_elems * 4);
+  const uint32_t tile_bytes = k16 ? (uint32_t)(P.tile16s_stride * 2) : k8 ? (uint32_t)P.tile8s_stride : (uint32_t)(tile_elems * 4);
   uint32_t phase = 0;
   unsigned long long n_relax = 0, n_back = 0, n_pass = 0;
 
@@ -199,9 +201,11 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
     const int32_t* gtile = P.tile + (size_t)inst * tile_elems;
     const int32_t* tile = gtile;
     const uint16_t* tile16 = (const uint16_t*)(base + L.tile);  // k16: the staged 16-bit copy
+    const uint8_t* tile8 = (const uint8_t*)(base + L.tile);     // k8: the staged 8-bit copy
     if constexpr (kSmem) {
       tile = (const int32_t*)(base + L.tile);
-      const uint8_t* gsrc = k16 ? (const uint8_t*)(P.tile16s + (size_t)inst * P.tile16s_stride) : (const uint8_t*)gtile;
+      const uint8_t* gsrc = k16 ? (const uint8_t*)(P.tile16s + (size_t)inst * P.tile16s_stride)
+                          : k8 ? P.tile8s + (size_t)inst * P.tile8s_stride : (const uint8_t*)gtile;
       if (T.tid == 0 && tile_bytes) {
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(mbar, tile_bytes);
@@ -211,12 +215,14 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
     }
     // weight of a 16-bit tile entry in the key arithmetic's form: pre-shifted (C << H) + 1 for
     // 32-bit keys, the raw cost for 64-bit keys, absent (0xFFFF) -> the absent code of each
+    constexpr uint32_t kAbs = k8 ? 0xFFu : 0xFFFFu;  // the narrow copies' absent code
     auto w16 = [&](uint32_t c) -> int32_t {
-      if constexpr (k32) return c == 0xFFFFu ? (int32_t)kInf32 : (int32_t)((c << H) + 1u);
-      else return c == 0xFFFFu ? kAbsent : (int32_t)c;
+      if constexpr (k32) return c == kAbs ? (int32_t)kInf32 : (int32_t)((c << H) + 1u);
+      else return c == kAbs ? kAbsent : (int32_t)c;
     };
     auto wgt = [&](size_t idx) -> int32_t {
       if constexpr (k16) return w16(tile16[idx]);
+      else if constexpr (k8) return w16(tile8[idx]);
       else return tile[idx];
     };
     const int64_t M = P.supply[inst];
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
     if (kSmem && tile_bytes) {
       mbar_wait(mbar, phase);
       phase ^= 1u;
-      if constexpr (k32 && !k16) {  // pre-shift the weights in place: (C << H) + 1, absent -> INF
+      if constexpr (k32 && kTB == 4) {  // pre-shift the weights in place: (C << H) + 1, absent -> INF
         T.sync();
         int32_t* tw = (int32_t*)(base + L.tile);
         for (size_t k = T.tid; k < tile_elems; k += TPI) tw[k] = KT<true>::prep(tw[k], H);
@@ -276,7 +282,18 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
             const int v = vb + gi;
             K acc = INF;
             if (v < n) {
-              if constexpr (k16) {  // 4 weights per 8-byte load, widened
+              if constexpr (k8) {  // 4 weights per 4-byte load, widened
+                const uint32_t* row = (const uint32_t*)(tile8 + ((size_t)s * n + v) * ld);
+                for (int c = li; c < chunks; c += G) {
+                  const uint32_t w = row[c];
+                  K kk[4];
+                  load_keys4<k32>(ko + 4 * c, kk);
+                  acc = KT<k32>::relax(acc, kk[0], w16(w & 0xFFu), one);
+                  acc = KT<k32>::relax(acc, kk[1], w16((w >> 8) & 0xFFu), one);
+                  acc = KT<k32>::relax(acc, kk[2], w16((w >> 16) & 0xFFu), one);
+                  acc = KT<k32>::relax(acc, kk[3], w16(w >> 24), one);
+                }
+              } else if constexpr (k16) {  // 4 weights per 8-byte load, widened
                 const uint2* row = (const uint2*)(tile16 + ((size_t)s * n + v) * ld);
                 for (int c = li; c < chunks; c += G) {
                   const uint2 w = row[c];
@@ -605,10 +622,10 @@ __global__ void __launch_bounds__(TPI >= 128 ? TPI : 128, TPI >= 128 ? 1536 / TP
   }
 }
 
-template <int TPI, bool kSmem, bool k32, bool kRedo, bool k16 = false>
+template <int TPI, bool kSmem, bool k32, bool kRedo, int kTB = 4>
 cudaError_t launch_one(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms) {
-  const size_t ws = ssp_layout(P, kSmem, k32 ? 4 : 8, k16 ? 2 : 4).total;
-  auto k = ssp_kernel<TPI, kSmem, k32, kRedo, k16>;
+  const size_t ws = ssp_layout(P, kSmem, k32 ? 4 : 8, kTB).total;
+  auto k = ssp_kernel<TPI, kSmem, k32, kRedo, kTB>;
   if (kSmem) {
     const size_t limit = 227 * 1024;
     int teams = TPI >= 128 ? 1 : 128 / TPI;
@@ -638,11 +655,17 @@ cudaError_t launch_one(const Problem& P, const SspOut& o, cudaStream_t st, int n
 template <int TPI>
 cudaError_t launch_tpi(const Problem& P, const SspOut& o, cudaStream_t st, int num_sms, bool smem_tier) {
   if (!smem_tier) return launch_one<256, false, false, false>(P, o, st, num_sms);
-  if (P.tile16s) {  // the 16-bit shared-memory tiles
-    if (P.hbits == 0) return launch_one<TPI, true, false, false, true>(P, o, st, num_sms);
-    cudaError_t e = launch_one<TPI, true, true, false, true>(P, o, st, num_sms);
+  if (P.tile8s) {  // the 8-bit shared-memory tiles
+    if (P.hbits == 0) return launch_one<TPI, true, false, false, 1>(P, o, st, num_sms);
+    cudaError_t e = launch_one<TPI, true, true, false, 1>(P, o, st, num_sms);
     if (e != cudaSuccess) return e;
-    return launch_one<TPI, true, false, true, true>(P, o, st, num_sms);
+    return launch_one<TPI, true, false, true, 1>(P, o, st, num_sms);
+  }
+  if (P.tile16s) {  // the 16-bit shared-memory tiles
+    if (P.hbits == 0) return launch_one<TPI, true, false, false, 2>(P, o, st, num_sms);
+    cudaError_t e = launch_one<TPI, true, true, false, 2>(P, o, st, num_sms);
+    if (e != cudaSuccess) return e;
+    return launch_one<TPI, true, false, true, 2>(P, o, st, num_sms);
   }
   if (P.hbits == 0) return launch_one<TPI, true, false, false>(P, o, st, num_sms);
   cudaError_t e = launch_one<TPI, true, true, false>(P, o, st, num_sms);
@@ -678,7 +701,7 @@ cudaError_t launch_ssp(const Problem& P, const SspOut& o, cudaStream_t st, int n
   // that fit in an SM's shared memory would leave it with fewer than 512 threads
   int tpi = P.n <= 32 ? 32 : P.n <= 64 ? 64 : P.n <= 128 ? 128 : 256;
   const long long teams_per_sm =
-      std::max<long long>(1, (long long)(227 * 1024) / (long long)ssp_layout(P, true, 4, P.tile16s ? 2 : 4).total);
+      std::max<long long>(1, (long long)(227 * 1024) / (long long)ssp_layout(P, true, 4, P.tile8s ? 1 : P.tile16s ? 2 : 4).total);
   while (tpi < 512 && teams_per_sm * tpi < 512) tpi *= 2;
   // multi-warp teams (named barriers) keep doubling up to 1,024 threads per SM: measured with the
   // 16-bit tiles, llama 64.4 -> 56.5 ms at 256 threads per team, churn 704 -> 574 ms at 512; a
