@@ -485,12 +485,14 @@ def test_key_overflow_redo_queue(name):
         assert np.array_equal(sf[b], r.src_flow) and np.array_equal(kf[b], r.snk_flow), b
 
 
+@pytest.mark.parametrize("name,hi,big", [("llama", 20000, 70000), ("churn", 200, 1000)], ids=["tile16", "tile8"])
 @pytest.mark.parametrize("drop", [False, True], ids=["recost", "recost+drop"])
-def test_smem_tile16_edge_updates(drop):
-    """The shared-memory tier's 16-bit tile copy under edge updates: re-costed links are written into
-    the copy (it stays in use, a dropped link as 0xFFFF), a cost >= 65535 retires it (int32 tiles); either way
-    the solve equals the oracle's on the updated graph, full assignment."""
-    cfg = gen.CONFIGS["llama"]
+def test_smem_tile16_edge_updates(drop, name, hi, big):
+    """The shared-memory tier's narrow tile copies under edge updates: re-costed links are written into
+    the copy (it stays in use, a dropped link as the absent code), a cost past its range retires it (llama:
+    16-bit -> int32 at 70,000; churn: 8-bit -> 16-bit at 1,000); either way the solve equals the oracle's
+    on the updated graph, full assignment."""
+    cfg = gen.CONFIGS[name]
     B = 6
     fl, *_ = _gpu_flow(cfg, 0, B)
     bt, src, snk, link = harness.host_inputs(cfg, 0, B)
@@ -499,10 +501,10 @@ def test_smem_tile16_edge_updates(drop):
     for b in range(B):
         for _ in range(40):
             s, v, u = int(rng.integers(0, cfg.S - 1)), int(rng.integers(0, cfg.n)), int(rng.integers(0, cfg.n))
-            upd[(b, s, v, u)] = int(rng.integers(1, 20000))
+            upd[(b, s, v, u)] = int(rng.integers(1, hi))
     if drop:
         upd[(1, 3, 5, 7)] = gen.ABSENT
-        upd[(4, 0, 0, 0)] = 70000
+        upd[(4, 0, 0, 0)] = big
     upd = np.array([(*k, c) for k, c in upd.items()], np.int32)
     fl.apply_churn(None, torch.from_numpy(upd).cuda())
     for b, s, v, u, c in upd:
